@@ -1,0 +1,304 @@
+#!/usr/bin/env python
+"""Benchmark of the SIMPLE-TS loop-2 sweep (arXiv:1802.04243) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--variant V] [--impl ours|reference]
+
+A "step" is one time step of the hot path: a0 snapshot rotation, a1 explicit
+planes (explicit variants), then `passes` fixed loop-2 passes (a2-a9), over
+the paper's largest mesh (C3, 4032 x 4000 = 16.1 M FVs) per GPU.
+N > 1: weak scaling -- every rank owns an identical 4032 x 4000 slab of one
+long channel (4032 N x 4000) with a halo exchange over NCCL after every pass.
+Metric: fp64 finite-volume updates per second = FVs x passes / time.
+
+Rank 0 prints one JSON line.  --impl reference times the CPU oracle (the
+plain fp64 C transcription of the paper) on a bounded sample instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 finite-volume updates/sec at 1/2/4/8 B200; HBM GB/s vs roofline"
+UNIT = "FVU/s"
+# algorithmic HBM bytes per finite-volume update
+BYTES_PER_FVU = {"implicit": 96.0, "explicit": 120.0}
+CONV_BYTES_PER_FV = 56.0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                parts = [p.strip() for p in out.strip().split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def bench_case(args, world):
+    from paper_1802_04243_b200 import workloads as W
+    if world == 1:
+        return W.c3(200, args.variant, passes=args.passes)
+    return W.c3_long(world, args.variant, passes=args.passes)
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args):
+    """The CPU oracle as it stands, on the box's host cores, on a bounded sample
+    of the same workload: the full 4032 x 4000 mesh, `ref_passes` loop-2 passes
+    of one time step per bench step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_1802_04243_b200 import workloads as W
+    oracle.build()
+    case = W.c3(200, args.variant, passes=args.ref_passes)
+    o = oracle.Case(case)
+    nfv = W.n_fv(case)
+    for _ in range(args.warmup if args.ref_warmup else 0):
+        o.advance(1)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.advance(1)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = nfv * args.ref_passes * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (paper geometry, free-stream IC)",
+        "config": {"workload": case["name"] + "_" + args.variant, "nx": case["nx"], "ny": case["ny"],
+                   "passes_per_step": args.ref_passes},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{case['name']} full mesh, {args.ref_passes} loop-2 passes of one time step per bench step, single thread"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(variant, seconds_hint=20.0):
+    """Oracle (single thread) on a bounded sample of the bench workload: the full
+    C3 4032 x 4000 mesh, one time step of ONE loop-2 pass."""
+    import oracle
+    from paper_1802_04243_b200 import workloads as W
+    oracle.build()
+    case = W.c3(200, variant, passes=1)
+    o = oracle.Case(case)
+    t0 = time.perf_counter()
+    o.advance(1)
+    dt = time.perf_counter() - t0
+    return {"value": W.n_fv(case) / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{case['name']} full mesh (16.1 M FVs), 1 time step x 1 loop-2 pass, {dt:.1f} s, single thread"}
+
+
+# ------------------------------------------------------------ our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1802_04243_b200 import simplets as S
+    from paper_1802_04243_b200 import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if rank == 0:
+            print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(S.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tolist())
+
+    case = bench_case(args, world)
+    stream = torch.cuda.current_stream(dev)
+    g = S.Solver(case, rank=rank, world=world, device=local, nccl_id=nccl_id, stream=stream.cuda_stream)
+    nfv_rank = g.shape("p")[2] * case["ny"]
+    passes = case["max_passes"]
+    kind = "implicit" if case["time"] == W.IMPLICIT else "explicit"
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier(device_ids=[local])
+            torch.cuda.synchronize(dev)
+
+    # warm-up
+    for _ in range(args.warmup):
+        g.advance(1)
+    barrier()
+    g.profile(True)
+    g.profile_read(reset=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            g.advance(1)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    prof = g.profile_read(reset=True)
+    g.profile(False)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_fvu = nfv_rank * world * passes * args.steps
+    value = total_fvu / (ms_max / 1e3)
+
+    # roofline of the dominant kernel (pass_kernel): algorithmic bytes per launch / avg launch time
+    peak, peak_kind = _peaks()
+    pass_ms = prof["pass_ms"] / max(prof["pass_launches"], 1)
+    bytes_per_launch = BYTES_PER_FVU[kind] * nfv_rank
+    achieved = bytes_per_launch / (pass_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            traffic = tj.get(f"{case['name']}_{args.variant}", {}).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_kind, "kernel": f"pass_kernel<{kind},{args.variant.split('_')[1]}>",
+                "algorithmic_bytes_per_fvu": BYTES_PER_FVU[kind], "pass_ms_avg": pass_ms,
+                "pass_share_of_step": prof["pass_ms"] / ms if ms > 0 else None}
+
+    # e2e: through the public API with host (pinned) buffers, every step:
+    # H2D of the step's input state (u, v, p, T) + advance + D2H of the residual maxima
+    e2e = None
+    if not args.no_e2e:
+        names = ("u", "v", "p", "T")
+        host = {k: torch.from_numpy(g.get_field(k)).pin_memory() for k in names}
+        devb = {k: torch.empty_like(host[k], device=dev) for k in names}
+        h2d = sum(h.numel() * 8 for h in host.values())
+        e_steps = max(1, min(args.steps, 5))
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e_steps):
+            for k in names:
+                devb[k].copy_(host[k], non_blocking=True)
+                g.set_field_device(k, devb[k].data_ptr(), devb[k].numel())
+            g.advance(1)          # reads back the 9 residual slots (72 B) to the host
+        e1.record(stream)
+        barrier()
+        ems = e0.elapsed_time(e1)
+        te = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": nfv_rank * world * passes * e_steps / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": 72 * world, "steps": e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.variant)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: the paper's geometry (P:686, P:719), free-stream IC; no datasets",
+            "config": {"workload": f"{case['name']}_{args.variant}", "nx": case["nx"], "ny": case["ny"],
+                       "fv_per_gpu": nfv_rank, "passes_per_step": passes, "dt": case["dt"],
+                       "parallelism": f"x-slabs{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (>= 1.5 GB working set per GPU)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(prof["launches"]), "clocks": clk.summary(),
+            "hbm_gbs_algorithmic_step": value / world * BYTES_PER_FVU[kind] / 1e9,
+        }
+        print(json.dumps(line), flush=True)
+    g.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--passes", type=int, default=10)
+    ap.add_argument("--variant", default="implicit_upwind",
+                    choices=["implicit_upwind", "implicit_tvd", "explicit_upwind", "explicit_tvd"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-passes", type=int, default=1)
+    ap.add_argument("--ref-warmup", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        if args.steps > 5:
+            args.steps = 5     # each reference step is ~20 s of single-core work
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -74,10 +74,20 @@ double orc_vanleer(double r)
 /* upwind(phi1, phi2, v), Eq. pl15_12; tie v = 0 -> phi2 (R7). */
 double orc_upwind(double f1, double f2, double w) { return w > 0.0 ? f1 : f2; }
 
-/* psi_s, Eq. pl15_2.  Zero denominator -> 0 (R6). */
+/* Reading R37: the ratio r of psi_s / psi_c has the difference phi3 - phi2
+ * in its denominator; a difference at the rounding level of O(1)
+ * nondimensional fields counts as zero (R6 extended), so a flat stencil
+ * never yields an O(1) limiter value from rounding noise. */
+static int flat(double f2, double f3)
+{
+    return fabs(f3 - f2) <= 1e-12 * (1.0 + fabs(f2) + fabs(f3));
+}
+
+/* psi_s, Eq. pl15_2.  Zero denominator -> 0 (R6, R37). */
 double orc_psi_s(double f1, double f2, double f3, double f4,
                  double d1, double d2, double d3, double d4, double w)
 {
+    if (flat(f2, f3)) return 0.0;
     if (w > 0.0) {
         double den = (d1 + d2) * (f3 - f2);
         if (den == 0.0) return 0.0;
@@ -91,10 +101,11 @@ double orc_psi_s(double f1, double f2, double f3, double f4,
     }
 }
 
-/* psi_c, Eq. pl15_1.  Zero denominator -> 0 (R6). */
+/* psi_c, Eq. pl15_1.  Zero denominator -> 0 (R6, R37). */
 double orc_psi_c(double f1, double f2, double f3, double f4,
                  double d1, double d2, double d3, double w)
 {
+    if (flat(f2, f3)) return 0.0;
     if (w > 0.0) {
         double den = d1 * (f3 - f2);
         if (den == 0.0) return 0.0;

@@ -1,0 +1,796 @@
+// simplets.cu -- host orchestrator + C ABI of libsimplets.so (include/simplets.h).
+//
+// Loop 1 x loop 2 of the GPU columns of Figs. 1-2:
+// per time step: rotate the snapshot handles (n-1 := current, old := n-1;
+// no copies), [explicit] one conv_kernel launch, then loop-2 passes of
+// pass_kernel until converged or max_passes.  Only residual maxima cross to
+// the host during a run.  Multi-GPU slabs along x: halo exchange over
+// NCCL after every pass.
+#include "../../include/simplets.h"
+#include "sts_kernels.cuh"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace sts;
+
+// ------------------------------------------------------------- errors
+static thread_local std::string g_err;
+
+struct sts_ctx;
+static sts_status fail(sts_ctx* c, sts_status st, const std::string& msg);
+
+#define CU(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? STS_E_OOM : STS_E_CUDA,    \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));              \
+    } while (0)
+
+// ------------------------------------------------------------- NCCL (dlopen)
+typedef struct { char internal[128]; } nccl_uid;
+typedef void* nccl_comm;
+enum { NCCL_UINT64 = 5, NCCL_FLOAT64 = 8, NCCL_MAX = 2 };
+struct NcclApi {
+    void* h = nullptr;
+    int (*GetUniqueId)(nccl_uid*);
+    int (*CommInitRank)(nccl_comm*, int, nccl_uid, int);
+    int (*CommDestroy)(nccl_comm);
+    int (*GroupStart)();
+    int (*GroupEnd)();
+    int (*Send)(const void*, size_t, int, int, nccl_comm, cudaStream_t);
+    int (*Recv)(void*, size_t, int, int, nccl_comm, cudaStream_t);
+    int (*AllReduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t);
+    bool load()
+    {
+        if (h) return true;
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* n : names) { h = dlopen(n, RTLD_NOW | RTLD_GLOBAL); if (h) break; }
+        if (!h) return false;
+        GetUniqueId = (int (*)(nccl_uid*))dlsym(h, "ncclGetUniqueId");
+        CommInitRank = (int (*)(nccl_comm*, int, nccl_uid, int))dlsym(h, "ncclCommInitRank");
+        CommDestroy = (int (*)(nccl_comm))dlsym(h, "ncclCommDestroy");
+        GroupStart = (int (*)())dlsym(h, "ncclGroupStart");
+        GroupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
+        Send = (int (*)(const void*, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclSend");
+        Recv = (int (*)(void*, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclRecv");
+        AllReduce = (int (*)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclAllReduce");
+        return GetUniqueId && CommInitRank && CommDestroy && GroupStart && GroupEnd && Send && Recv && AllReduce;
+    }
+};
+static NcclApi g_nccl;
+
+// ------------------------------------------------------------- context
+struct Snapshot { double *u = nullptr, *v = nullptr, *p = nullptr, *T = nullptr; };
+
+struct sts_ctx {
+    // problem
+    int nx = 0, ny = 0;
+    double spacing = 0;
+    sts_gas gas{};
+    sts_scheme sch{};
+    std::vector<sts_square> squares;
+    double A = 0, B = 0, CT1 = 0, CT2 = 0, CT3 = 0, u_in = 0, u_wb = 0, u_wt = 0;
+    // decomposition
+    int rank = 0, world = 1, device = 0;
+    int gi0 = 0, nloc = 0, pitch = 0;
+    std::vector<int> col_start;            // world+1 entries
+    // device memory
+    Snapshot snap[3];
+    int cur = 0;                           // index of the current state snapshot
+    double *ue = nullptr, *ve = nullptr, *Te = nullptr;
+    uint8_t *ck = nullptr, *uk = nullptr, *vk = nullptr;
+    std::vector<uint8_t> h_ck, h_uk, h_vk; // host copies of the local kind maps
+    unsigned long long* red = nullptr;     // [max_passes][9]
+    unsigned long long* h_red = nullptr;   // pinned, 9 entries
+    double* stage = nullptr;               // device staging (global-shape field)
+    size_t stage_elems = 0;
+    double* halo = nullptr;                // send/recv buffers (multi-GPU)
+    size_t halo_elems = 0;
+    cudaStream_t stream = nullptr;
+    // multi-GPU
+    nccl_comm comm = nullptr;
+    // stats / profiling
+    sts_stats stats{};
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, int>> ev_used;   // (start idx, kind)
+    double prof_pass_n = 0, prof_pass_ms = 0, prof_conv_n = 0, prof_conv_ms = 0, launches = 0;
+    std::string err;
+};
+
+static sts_status fail(sts_ctx* c, sts_status st, const std::string& msg)
+{
+    g_err = msg;
+    if (c) c->err = msg;
+    return st;
+}
+
+extern "C" const char* sts_last_error(const sts_ctx* ctx)
+{
+    if (ctx && !ctx->err.empty()) return ctx->err.c_str();
+    return g_err.c_str();
+}
+
+// ------------------------------------------------------------- layout helpers
+static inline long long lidx(const sts_ctx* c, int gi, int gj) { return (long long)gj * c->pitch + (gi - c->gi0 + OFF); }
+static inline size_t cell_elems(const sts_ctx* c) { return (size_t)c->pitch * c->ny; }
+static inline size_t v_elems(const sts_ctx* c) { return (size_t)c->pitch * (c->ny + 1); }
+static inline bool is_periodic(const sts_ctx* c) { return c->gas.xbc == STS_X_PERIODIC; }
+
+// Host kind maps for the stored local columns [gi0-OFF, gi0-OFF+pitch) (DESIGN 3.5).
+static bool solid_global(const sts_ctx* c, int gi, int gj, const std::vector<uint8_t>& solid)
+{
+    return solid[(size_t)gj * c->nx + gi] != 0;
+}
+static uint8_t cell_kind_g(const sts_ctx* c, int gi, int gj, const std::vector<uint8_t>& solid)
+{
+    if (gj < 0 || gj >= c->ny) return CK_WALLY;
+    if (is_periodic(c)) { gi = ((gi % c->nx) + c->nx) % c->nx; }
+    else if (gi < 0) return CK_INLET;
+    else if (gi >= c->nx) return CK_OUTLET;
+    return solid_global(c, gi, gj, solid) ? CK_SOLID : CK_FLUID;
+}
+static uint8_t u_kind_g(const sts_ctx* c, int gf, int gj, const std::vector<uint8_t>& solid)
+{
+    if (gj < 0 || gj >= c->ny) return FK_NONE;
+    if (!is_periodic(c)) {
+        if (gf < 0 || gf > c->nx) return FK_NONE;
+        if (gf == 0) return FK_INLET;
+        if (gf == c->nx) return FK_OUTLET;
+    }
+    return (cell_kind_g(c, gf - 1, gj, solid) == CK_FLUID && cell_kind_g(c, gf, gj, solid) == CK_FLUID) ? FK_ACTIVE : FK_FIXED0;
+}
+static uint8_t v_kind_g(const sts_ctx* c, int gi, int gj, const std::vector<uint8_t>& solid)
+{
+    if (gj < 0 || gj > c->ny) return FK_NONE;
+    if (gj == 0 || gj == c->ny) return FK_WALL;
+    if (!is_periodic(c) && (gi < 0 || gi >= c->nx)) return FK_NONE;
+    return (cell_kind_g(c, gi, gj - 1, solid) == CK_FLUID && cell_kind_g(c, gi, gj, solid) == CK_FLUID) ? FK_ACTIVE : FK_FIXED0;
+}
+
+// ------------------------------------------------------------- pack / unpack
+// Global-shape field (device) <-> local padded slab with ghost columns
+// (inlet state, outlet copy, periodic wrap; DESIGN 3.5 items 2-4).
+struct PackArgs {
+    int nx, ny, gi0, pitch, xbc, field;   // field: 0 u, 1 v, 2 p, 3 T
+    double inlet_val;                      // u_in / 0 / p_in / T_in
+};
+__global__ void pack_kernel(PackArgs a, const double* __restrict__ g, double* __restrict__ l)
+{
+    const int rows = a.field == 1 ? a.ny + 1 : a.ny;
+    const int gw = a.field == 0 ? a.nx + 1 : a.nx;         // global row width
+    long long n = (long long)rows * a.pitch;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        int j = (int)(e / a.pitch), li = (int)(e - (long long)j * a.pitch);
+        int gi = a.gi0 - OFF + li;
+        double val;
+        if (a.xbc == 1) {
+            int w = ((gi % a.nx) + a.nx) % a.nx;
+            val = g[(long long)j * gw + w];
+        } else if (gi < 0) {
+            val = a.inlet_val;
+        } else if (a.field == 0) {
+            val = gi <= a.nx ? g[(long long)j * gw + gi] : a.inlet_val;
+        } else {
+            val = g[(long long)j * gw + (gi < a.nx ? gi : a.nx - 1)];
+        }
+        l[e] = val;
+    }
+}
+__global__ void unpack_kernel(int ny_rows, int ncols, int col0_local, int pitch, int gw, int gcol0,
+                              const double* __restrict__ l, double* __restrict__ g)
+{
+    long long n = (long long)ny_rows * ncols;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        int j = (int)(e / ncols), i = (int)(e - (long long)j * ncols);
+        g[(long long)j * gw + gcol0 + i] = l[(long long)j * pitch + col0_local + i];
+    }
+}
+// rho = p / T for the read-back of STS_RHO (Eq. pl5)
+__global__ void ratio_kernel(long long n, const double* __restrict__ p, const double* __restrict__ T, double* __restrict__ r)
+{
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+        r[e] = p[e] / T[e];
+}
+// Halo strips for the multi-GPU exchange: columns [c0, c0+OFF) of u, v, p, T.
+__global__ void halo_pack_kernel(int ny, int pitch, int c0, const double* u, const double* v, const double* p,
+                                 const double* T, double* buf)
+{
+    const int per = OFF * (ny + 1);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 4 * per; e += gridDim.x * blockDim.x) {
+        int f = e / per, r = e - f * per, j = r / OFF, i = r - j * OFF;
+        const double* src = f == 0 ? u : f == 1 ? v : f == 2 ? p : T;
+        int rows = f == 1 ? ny + 1 : ny;
+        buf[e] = j < rows ? src[(long long)j * pitch + c0 + i] : 0.0;
+    }
+}
+__global__ void halo_unpack_kernel(int ny, int pitch, int c0, double* u, double* v, double* p, double* T,
+                                   const double* buf)
+{
+    const int per = OFF * (ny + 1);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 4 * per; e += gridDim.x * blockDim.x) {
+        int f = e / per, r = e - f * per, j = r / OFF, i = r - j * OFF;
+        double* dst = f == 0 ? u : f == 1 ? v : f == 2 ? p : T;
+        int rows = f == 1 ? ny + 1 : ny;
+        if (j < rows) dst[(long long)j * pitch + c0 + i] = buf[e];
+    }
+}
+
+// ------------------------------------------------------------- kernel table
+typedef void (*pass_fn)(Params);
+static pass_fn pass_table(int impl, int tvd)
+{
+    if (impl) return tvd ? pass_kernel<true, true> : pass_kernel<true, false>;
+    return tvd ? pass_kernel<false, true> : pass_kernel<false, false>;
+}
+static pass_fn conv_table(int tvd) { return tvd ? conv_kernel<true> : conv_kernel<false>; }
+
+static sts_status set_smem_attrs(sts_ctx* ctx)
+{
+    static bool done = false;
+    if (done) return STS_OK;
+    const int bytes = (int)sizeof(Smem);
+    pass_fn fns[6] = {pass_table(0, 0), pass_table(0, 1), pass_table(1, 0), pass_table(1, 1), conv_table(0), conv_table(1)};
+    for (pass_fn f : fns) CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done = true;
+    return STS_OK;
+}
+
+static Params make_params(const sts_ctx* c)
+{
+    Params k{};
+    k.nx = c->nx; k.ny = c->ny; k.gi0 = c->gi0; k.nloc = c->nloc; k.pitch = c->pitch;
+    k.xbc = c->gas.xbc; k.mirror = (is_periodic(c) && c->world == 1) ? 1 : 0;
+    k.first_rank = c->rank == 0; k.last_rank = c->rank == c->world - 1;
+    k.dx = c->spacing; k.dy = c->spacing; k.dt = c->sch.dt;
+    k.A = c->A; k.B = c->B; k.CT1 = c->CT1; k.CT2 = c->CT2; k.CT3 = c->CT3; k.Kn = c->gas.Kn;
+    k.u_in = c->u_in; k.p_in = c->gas.p_in; k.T_in = c->gas.T_in;
+    k.u_wb = c->u_wb; k.u_wt = c->u_wt; k.T_wall = c->gas.T_wall; k.T_sq = c->gas.T_square;
+    k.g_x = c->gas.g_x; k.g_y = c->gas.g_y; k.pw_sign = c->gas.pw_sign;
+    k.ck = c->ck; k.uk = c->uk; k.vk = c->vk;
+    return k;
+}
+
+// ------------------------------------------------------------- profiling
+static cudaEvent_t ev_get(sts_ctx* c, size_t i)
+{
+    while (c->ev_pool.size() <= i) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[i];
+}
+static void prof_begin(sts_ctx* c, int kind)
+{
+    if (!c->profiling) return;
+    size_t i = 2 * c->ev_used.size();
+    cudaEventRecord(ev_get(c, i), c->stream);
+    c->ev_used.push_back({(int)i, kind});
+}
+static void prof_end(sts_ctx* c)
+{
+    if (!c->profiling) return;
+    cudaEventRecord(ev_get(c, c->ev_used.back().first + 1), c->stream);
+}
+static void prof_collect(sts_ctx* c)
+{
+    if (c->ev_used.empty()) return;
+    cudaEventSynchronize(c->ev_pool[c->ev_used.back().first + 1]);
+    for (auto& pr : c->ev_used) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev_pool[pr.first], c->ev_pool[pr.first + 1]);
+        if (pr.second == 0) { c->prof_pass_n += 1; c->prof_pass_ms += ms; }
+        else { c->prof_conv_n += 1; c->prof_conv_ms += ms; }
+    }
+    c->ev_used.clear();
+}
+
+// ------------------------------------------------------------- halo exchange
+static sts_status exchange(sts_ctx* ctx, const Snapshot& s)
+{
+    if (ctx->world == 1) return STS_OK;
+    const int per = 4 * OFF * (ctx->ny + 1);
+    const bool periodic = is_periodic(ctx);
+    const int left = ctx->rank > 0 ? ctx->rank - 1 : (periodic ? ctx->world - 1 : -1);
+    const int right = ctx->rank < ctx->world - 1 ? ctx->rank + 1 : (periodic ? 0 : -1);
+    double* sendL = ctx->halo;
+    double* sendR = ctx->halo + per;
+    double* recvL = ctx->halo + 2 * per;
+    double* recvR = ctx->halo + 3 * per;
+    const int blocks = (per + 255) / 256;
+    // my first OFF owned columns go left, my last OFF owned columns go right
+    if (left >= 0) { halo_pack_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->ny, ctx->pitch, OFF, s.u, s.v, s.p, s.T, sendL); ctx->launches++; }
+    if (right >= 0) { halo_pack_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->ny, ctx->pitch, ctx->nloc, s.u, s.v, s.p, s.T, sendR); ctx->launches++; }
+    CU(cudaGetLastError());
+    if (g_nccl.GroupStart()) return fail(ctx, STS_E_COMM, "ncclGroupStart");
+    if (left >= 0) {
+        if (g_nccl.Send(sendL, per, NCCL_FLOAT64, left, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclSend");
+        if (g_nccl.Recv(recvL, per, NCCL_FLOAT64, left, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclRecv");
+    }
+    if (right >= 0) {
+        if (g_nccl.Send(sendR, per, NCCL_FLOAT64, right, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclSend");
+        if (g_nccl.Recv(recvR, per, NCCL_FLOAT64, right, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclRecv");
+    }
+    if (g_nccl.GroupEnd()) return fail(ctx, STS_E_COMM, "ncclGroupEnd");
+    // left neighbour's last OFF owned columns are my ghost columns [0, OFF);
+    // right neighbour's first OFF owned columns are my ghosts [OFF+nloc, 2 OFF+nloc)
+    if (left >= 0) { halo_unpack_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->ny, ctx->pitch, 0, s.u, s.v, s.p, s.T, recvL); ctx->launches++; }
+    if (right >= 0) { halo_unpack_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->ny, ctx->pitch, OFF + ctx->nloc, s.u, s.v, s.p, s.T, recvR); ctx->launches++; }
+    CU(cudaGetLastError());
+    return STS_OK;
+}
+
+// ------------------------------------------------------------- ABI
+extern "C" sts_status sts_nccl_unique_id(void* out128)
+{
+    sts_ctx* ctx = nullptr;
+    if (!out128) return fail(ctx, STS_E_ARG, "null id buffer");
+    if (!g_nccl.load()) return fail(ctx, STS_E_COMM, "libnccl.so.2 not loadable");
+    nccl_uid id;
+    if (g_nccl.GetUniqueId(&id)) return fail(ctx, STS_E_COMM, "ncclGetUniqueId failed");
+    memcpy(out128, &id, 128);
+    return STS_OK;
+}
+
+extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares, int32_t n_squares,
+                                 const sts_gas* gas, const sts_scheme* scheme, const sts_dist* dist,
+                                 sts_ctx** out)
+{
+    sts_ctx* ctx = nullptr;
+    if (!grid || !gas || !scheme || !out || (n_squares > 0 && !squares)) return fail(ctx, STS_E_ARG, "null argument");
+    *out = nullptr;
+    if (!(grid->spacing > 0) || !(grid->length_x > 0) || !(grid->length_y > 0)) return fail(ctx, STS_E_CONFIG, "non-positive grid");
+    double fx = grid->length_x / grid->spacing, fy = grid->length_y / grid->spacing;
+    int nx = (int)llround(fx), ny = (int)llround(fy);
+    if (std::fabs(fx - nx) > 1e-9 || std::fabs(fy - ny) > 1e-9 || nx < 1 || ny < 1)
+        return fail(ctx, STS_E_CONFIG, "channel lengths are not multiples of the spacing");
+    if (!(gas->Kn > 0)) return fail(ctx, STS_E_CONFIG, "Kn must be > 0");
+    if (!(gas->pw_sign == 1.0 || gas->pw_sign == -1.0)) return fail(ctx, STS_E_CONFIG, "pw_sign must be +1 or -1");
+    if (gas->xbc != STS_X_INFLOW_OUTFLOW && gas->xbc != STS_X_PERIODIC) return fail(ctx, STS_E_ARG, "bad xbc");
+    if ((scheme->time != STS_EXPLICIT && scheme->time != STS_IMPLICIT) || (scheme->space != STS_UPWIND && scheme->space != STS_TVD_VANLEER))
+        return fail(ctx, STS_E_ARG, "bad scheme enum");
+    if (!(scheme->dt > 0) || scheme->max_passes < 1 || scheme->min_passes < 0) return fail(ctx, STS_E_CONFIG, "bad dt / passes");
+    if (!(gas->p_in > 0) || !(gas->T_in > 0)) return fail(ctx, STS_E_CONFIG, "inflow state must be positive");
+    int world = dist ? dist->world : 1, rank = dist ? dist->rank : 0;
+    if (world < 1 || rank < 0 || rank >= world) return fail(ctx, STS_E_ARG, "bad rank/world");
+
+    std::vector<uint8_t> solid((size_t)nx * ny, 0);
+    for (int s = 0; s < n_squares; s++) {
+        const sts_square& q = squares[s];
+        if (q.ni < 1 || q.nj < 1 || q.i0 < 0 || q.j0 < 0 || q.i0 + q.ni > nx || q.j0 + q.nj > ny)
+            return fail(ctx, STS_E_CONFIG, "square outside the channel");
+        if (gas->xbc == STS_X_INFLOW_OUTFLOW && (q.i0 < 1 || q.i0 + q.ni > nx - 1))
+            return fail(ctx, STS_E_CONFIG, "square must leave a fluid column at the inlet and outlet");
+        for (int j = q.j0; j < q.j0 + q.nj; j++)
+            for (int i = q.i0; i < q.i0 + q.ni; i++) solid[(size_t)j * nx + i] = 1;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return fail(ctx, STS_E_CUDA, "no CUDA device");
+
+    ctx = new sts_ctx();
+    ctx->nx = nx; ctx->ny = ny; ctx->spacing = grid->spacing;
+    ctx->gas = *gas; ctx->sch = *scheme;
+    ctx->squares.assign(squares, squares + n_squares);
+    ctx->rank = rank; ctx->world = world;
+    ctx->device = dist ? dist->device : 0;
+    if (ctx->device < 0 || ctx->device >= ndev) { delete ctx; return fail(nullptr, STS_E_ARG, "bad device"); }
+    if (cudaSetDevice(ctx->device) != cudaSuccess) { delete ctx; return fail(nullptr, STS_E_CUDA, "cudaSetDevice"); }
+    // Eq. pl37; u_in = M sqrt(gamma T_in / 2) (V0 = sqrt(2 R T0))
+    ctx->A = 0.5;
+    ctx->B = 5.0 * std::sqrt(M_PI) / 16.0 * gas->Kn;
+    ctx->CT1 = gas->Kn * std::sqrt(M_PI * 225.0 / 1024.0);
+    ctx->CT2 = std::sqrt(M_PI) / 4.0 * gas->Kn;
+    ctx->CT3 = 2.0 / 5.0;
+    ctx->u_in = gas->mach * std::sqrt(gas->gamma / 2.0 * gas->T_in);
+    ctx->u_wb = gas->particle_frame ? ctx->u_in : gas->u_wall_bottom;   // R14
+    ctx->u_wt = gas->particle_frame ? ctx->u_in : gas->u_wall_top;
+    // slab decomposition along x: near-equal, remainder to the low ranks
+    ctx->col_start.resize(world + 1);
+    for (int r = 0, acc = 0; r <= world; r++) {
+        ctx->col_start[r] = acc;
+        if (r < world) acc += nx / world + (r < nx % world ? 1 : 0);
+    }
+    ctx->gi0 = ctx->col_start[rank];
+    ctx->nloc = ctx->col_start[rank + 1] - ctx->gi0;
+    if (world > 1 && ctx->nloc < OFF) { delete ctx; return fail(nullptr, STS_E_CONFIG, "slab narrower than the halo"); }
+    ctx->pitch = ((ctx->nloc + 2 * OFF + 1) + 15) / 16 * 16;
+
+    sts_status st = set_smem_attrs(ctx);
+    if (st != STS_OK) { sts_destroy(ctx); return st; }
+    // kind maps
+    size_t nce = cell_elems(ctx), nve = v_elems(ctx);
+    ctx->h_ck.assign(nce, CK_WALLY); ctx->h_uk.assign(nce, FK_NONE); ctx->h_vk.assign(nve, FK_NONE);
+    for (int j = 0; j < ny; j++)
+        for (int li = 0; li < ctx->pitch; li++) {
+            int gi = ctx->gi0 - OFF + li;
+            ctx->h_ck[(size_t)j * ctx->pitch + li] = cell_kind_g(ctx, gi, j, solid);
+            ctx->h_uk[(size_t)j * ctx->pitch + li] = u_kind_g(ctx, gi, j, solid);
+        }
+    for (int j = 0; j <= ny; j++)
+        for (int li = 0; li < ctx->pitch; li++)
+            ctx->h_vk[(size_t)j * ctx->pitch + li] = v_kind_g(ctx, ctx->gi0 - OFF + li, j, solid);
+
+    auto alloc = [&](double** p, size_t n) -> sts_status {
+        CU(cudaMalloc(p, n * sizeof(double)));
+        CU(cudaMemset(*p, 0, n * sizeof(double)));
+        return STS_OK;
+    };
+#define ALLOC(p, n) do { sts_status s_ = alloc(&(p), (n)); if (s_ != STS_OK) { sts_destroy(ctx); return s_; } } while (0)
+    for (int k = 0; k < 3; k++) {
+        ALLOC(ctx->snap[k].u, nce); ALLOC(ctx->snap[k].v, nve); ALLOC(ctx->snap[k].p, nce); ALLOC(ctx->snap[k].T, nce);
+    }
+    ALLOC(ctx->ue, nce); ALLOC(ctx->ve, nve); ALLOC(ctx->Te, nce);
+    ctx->stage_elems = (size_t)(nx + 1) * (ny + 1);
+    ALLOC(ctx->stage, ctx->stage_elems);
+    if (world > 1) { ctx->halo_elems = (size_t)16 * OFF * (ny + 1); ALLOC(ctx->halo, ctx->halo_elems); }
+#undef ALLOC
+    if (cudaMalloc(&ctx->ck, nce) != cudaSuccess || cudaMalloc(&ctx->uk, nce) != cudaSuccess || cudaMalloc(&ctx->vk, nve) != cudaSuccess ||
+        cudaMalloc(&ctx->red, (size_t)scheme->max_passes * 9 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMallocHost(&ctx->h_red, 9 * sizeof(unsigned long long)) != cudaSuccess) {
+        sts_destroy(ctx);
+        return fail(nullptr, STS_E_OOM, "device allocation failed");
+    }
+    cudaMemcpy(ctx->ck, ctx->h_ck.data(), nce, cudaMemcpyHostToDevice);
+    cudaMemcpy(ctx->uk, ctx->h_uk.data(), nce, cudaMemcpyHostToDevice);
+    cudaMemcpy(ctx->vk, ctx->h_vk.data(), nve, cudaMemcpyHostToDevice);
+    if (world > 1) {
+        if (!dist->nccl_id) { sts_destroy(ctx); return fail(nullptr, STS_E_ARG, "world > 1 needs an NCCL id"); }
+        if (!g_nccl.load()) { sts_destroy(ctx); return fail(nullptr, STS_E_COMM, "libnccl.so.2 not loadable"); }
+        nccl_uid id;
+        memcpy(&id, dist->nccl_id, 128);
+        if (g_nccl.CommInitRank(&ctx->comm, world, id, rank)) { sts_destroy(ctx); return fail(nullptr, STS_E_COMM, "ncclCommInitRank failed"); }
+    }
+    ctx->stats.bad_cell = -1;
+    st = sts_init_freestream(ctx);
+    if (st != STS_OK) { sts_destroy(ctx); return st; }
+    *out = ctx;
+    return STS_OK;
+}
+
+extern "C" void sts_destroy(sts_ctx* ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    for (int k = 0; k < 3; k++) { cudaFree(ctx->snap[k].u); cudaFree(ctx->snap[k].v); cudaFree(ctx->snap[k].p); cudaFree(ctx->snap[k].T); }
+    cudaFree(ctx->ue); cudaFree(ctx->ve); cudaFree(ctx->Te); cudaFree(ctx->stage); cudaFree(ctx->halo);
+    cudaFree(ctx->ck); cudaFree(ctx->uk); cudaFree(ctx->vk); cudaFree(ctx->red);
+    if (ctx->h_red) cudaFreeHost(ctx->h_red);
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
+    delete ctx;
+}
+
+extern "C" sts_status sts_set_stream(sts_ctx* ctx, void* s)
+{
+    if (!ctx) return fail(ctx, STS_E_ARG, "null ctx");
+    ctx->stream = (cudaStream_t)s;
+    return STS_OK;
+}
+
+static size_t global_size(const sts_ctx* c, int field)
+{
+    if (field == STS_U || field == STS_UEXP) return (size_t)(c->nx + 1) * c->ny;
+    if (field == STS_V || field == STS_VEXP) return (size_t)c->nx * (c->ny + 1);
+    return (size_t)c->nx * c->ny;
+}
+
+// Pack a global-shape device field into all three snapshots (solid cells and
+// fixed faces must agree in every snapshot: they are never rewritten).
+static sts_status pack_into_all(sts_ctx* ctx, int field, const double* gdev)
+{
+    PackArgs a{ctx->nx, ctx->ny, ctx->gi0, ctx->pitch, ctx->gas.xbc, field,
+               field == 0 ? ctx->u_in : field == 1 ? 0.0 : field == 2 ? ctx->gas.p_in : ctx->gas.T_in};
+    for (int k = 0; k < 3; k++) {
+        double* dst = field == 0 ? ctx->snap[k].u : field == 1 ? ctx->snap[k].v : field == 2 ? ctx->snap[k].p : ctx->snap[k].T;
+        pack_kernel<<<592, 256, 0, ctx->stream>>>(a, gdev, dst);
+        ctx->launches++;
+    }
+    CU(cudaGetLastError());
+    return STS_OK;
+}
+
+// Host-side fixed faces of DESIGN 3.5 (inlet u_in, solid/wall faces 0) applied
+// to a global-shape host copy before packing.
+static void impose_fixed_host(const sts_ctx* c, int field, double* g)
+{
+    if (field == STS_U) {
+        for (int j = 0; j < c->ny; j++)
+            for (int i = 0; i <= c->nx; i++) {
+                int li = i - c->gi0 + OFF;
+                uint8_t k;
+                if (li >= 0 && li < c->pitch) k = c->h_uk[(size_t)j * c->pitch + li];
+                else continue;   // outside this rank: its owner imposes it
+                if (k == FK_FIXED0) g[(size_t)j * (c->nx + 1) + i] = 0.0;
+                else if (k == FK_INLET) g[(size_t)j * (c->nx + 1) + i] = c->u_in;
+            }
+        if (is_periodic(c))
+            for (int j = 0; j < c->ny; j++) g[(size_t)j * (c->nx + 1) + c->nx] = g[(size_t)j * (c->nx + 1)];
+    } else if (field == STS_V) {
+        for (int j = 0; j <= c->ny; j++)
+            for (int i = 0; i < c->nx; i++) {
+                int li = i - c->gi0 + OFF;
+                if (li < 0 || li >= c->pitch) continue;
+                uint8_t k = c->h_vk[(size_t)j * c->pitch + li];
+                if (k == FK_FIXED0 || k == FK_WALL) g[(size_t)j * c->nx + i] = 0.0;
+            }
+    }
+}
+
+extern "C" sts_status sts_set_field(sts_ctx* ctx, int32_t field, const double* host, int64_t n)
+{
+    if (!ctx || !host) return fail(ctx, STS_E_ARG, "null argument");
+    if (field < STS_U || field > STS_T) return fail(ctx, STS_E_ARG, "field not settable");
+    if ((size_t)n != global_size(ctx, field)) return fail(ctx, STS_E_ARG, "wrong buffer size");
+    CU(cudaSetDevice(ctx->device));
+    std::vector<double> g(host, host + n);
+    impose_fixed_host(ctx, field, g.data());
+    CU(cudaMemcpyAsync(ctx->stage, g.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    sts_status st = pack_into_all(ctx, field, ctx->stage);
+    if (st != STS_OK) return st;
+    CU(cudaStreamSynchronize(ctx->stream));
+    return STS_OK;
+}
+
+// Device variant: the caller guarantees fixed faces are already imposed
+// (e.g. a state read back with sts_get_field_device); used by the e2e bench.
+extern "C" sts_status sts_set_field_device(sts_ctx* ctx, int32_t field, const double* dev, int64_t n)
+{
+    if (!ctx || !dev) return fail(ctx, STS_E_ARG, "null argument");
+    if (field < STS_U || field > STS_T) return fail(ctx, STS_E_ARG, "field not settable");
+    if ((size_t)n != global_size(ctx, field)) return fail(ctx, STS_E_ARG, "wrong buffer size");
+    return pack_into_all(ctx, field, dev);
+}
+
+extern "C" sts_status sts_init_freestream(sts_ctx* ctx)
+{
+    if (!ctx) return fail(ctx, STS_E_ARG, "null ctx");
+    CU(cudaSetDevice(ctx->device));
+    for (int field = 0; field < 4; field++) {
+        size_t n = global_size(ctx, field);
+        double val = field == 0 ? ctx->u_in : field == 1 ? 0.0 : field == 2 ? ctx->gas.p_in : ctx->gas.T_in;
+        std::vector<double> g(n, val);
+        impose_fixed_host(ctx, field, g.data());
+        CU(cudaMemcpyAsync(ctx->stage, g.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        sts_status st = pack_into_all(ctx, field, ctx->stage);
+        if (st != STS_OK) return st;
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    CU(cudaMemsetAsync(ctx->ue, 0, cell_elems(ctx) * sizeof(double), ctx->stream));
+    CU(cudaMemsetAsync(ctx->ve, 0, v_elems(ctx) * sizeof(double), ctx->stream));
+    CU(cudaMemsetAsync(ctx->Te, 0, cell_elems(ctx) * sizeof(double), ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    ctx->cur = 0;
+    return STS_OK;
+}
+
+// Owned slab of a field -> device buffer laid out as this rank's part of the
+// global shape (single GPU: the global shape).
+static sts_status unpack_owned(sts_ctx* ctx, int field, double* gdev, int64_t n)
+{
+    const Snapshot& s = ctx->snap[ctx->cur];
+    int rows = (field == STS_V || field == STS_VEXP) ? ctx->ny + 1 : ctx->ny;
+    bool last = ctx->rank == ctx->world - 1;
+    int ncols = ctx->nloc + ((field == STS_U || field == STS_UEXP) && last ? 1 : 0);
+    if ((int64_t)rows * ncols != n) return fail(ctx, STS_E_ARG, "wrong buffer size");
+    const double* src;
+    switch (field) {
+    case STS_U: src = s.u; break;
+    case STS_V: src = s.v; break;
+    case STS_P: src = s.p; break;
+    case STS_T: src = s.T; break;
+    case STS_UEXP: src = ctx->ue; break;
+    case STS_VEXP: src = ctx->ve; break;
+    case STS_TEXP: src = ctx->Te; break;
+    default: return fail(ctx, STS_E_ARG, "bad field");
+    }
+    unpack_kernel<<<592, 256, 0, ctx->stream>>>(rows, ncols, OFF, ctx->pitch, ncols, 0, src, gdev);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    return STS_OK;
+}
+
+extern "C" sts_status sts_get_field(sts_ctx* ctx, int32_t field, double* host, int64_t n)
+{
+    if (!ctx || !host) return fail(ctx, STS_E_ARG, "null argument");
+    CU(cudaSetDevice(ctx->device));
+    if (field == STS_RHO) {
+        // rho needs a scratch cell array: compute into stage-sized buffer via a temporary
+        double* tmp = nullptr;
+        CU(cudaMalloc(&tmp, cell_elems(ctx) * sizeof(double)));
+        const Snapshot& s = ctx->snap[ctx->cur];
+        ratio_kernel<<<592, 256, 0, ctx->stream>>>((long long)cell_elems(ctx), s.p, s.T, tmp);
+        ctx->launches++;
+        int rows = ctx->ny, ncols = ctx->nloc;
+        if ((int64_t)rows * ncols != n) { cudaFree(tmp); return fail(ctx, STS_E_ARG, "wrong buffer size"); }
+        unpack_kernel<<<592, 256, 0, ctx->stream>>>(rows, ncols, OFF, ctx->pitch, ncols, 0, tmp, ctx->stage);
+        ctx->launches++;
+        CU(cudaMemcpyAsync(host, ctx->stage, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        cudaFree(tmp);
+        return STS_OK;
+    }
+    sts_status st = unpack_owned(ctx, field, ctx->stage, n);
+    if (st != STS_OK) return st;
+    CU(cudaMemcpyAsync(host, ctx->stage, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return STS_OK;
+}
+
+extern "C" sts_status sts_get_field_device(sts_ctx* ctx, int32_t field, double* dev, int64_t n)
+{
+    if (!ctx || !dev) return fail(ctx, STS_E_ARG, "null argument");
+    if (field == STS_RHO) return fail(ctx, STS_E_ARG, "STS_RHO only via sts_get_field");
+    return unpack_owned(ctx, field, dev, n);
+}
+
+extern "C" sts_status sts_get_map(sts_ctx* ctx, int32_t which, int32_t* host, int64_t n)
+{
+    if (!ctx || !host) return fail(ctx, STS_E_ARG, "null argument");
+    if (which == 3) {
+        if (n != 2 * ctx->world) return fail(ctx, STS_E_ARG, "wrong buffer size");
+        for (int r = 0; r < ctx->world; r++) { host[2 * r] = ctx->col_start[r]; host[2 * r + 1] = ctx->col_start[r + 1]; }
+        return STS_OK;
+    }
+    bool last = ctx->rank == ctx->world - 1;
+    int rows = which == 2 ? ctx->ny + 1 : ctx->ny;
+    int ncols = ctx->nloc + (which == 1 && last ? 1 : 0);
+    if (which < 0 || which > 2) return fail(ctx, STS_E_ARG, "bad map");
+    if ((int64_t)rows * ncols != n) return fail(ctx, STS_E_ARG, "wrong buffer size");
+    const std::vector<uint8_t>& m = which == 0 ? ctx->h_ck : which == 1 ? ctx->h_uk : ctx->h_vk;
+    for (int j = 0; j < rows; j++)
+        for (int i = 0; i < ncols; i++) {
+            uint8_t k = m[(size_t)j * ctx->pitch + OFF + i];
+            host[(size_t)j * ncols + i] = which == 0 ? (k == CK_SOLID ? 1 : 0) : k;
+        }
+    return STS_OK;
+}
+
+extern "C" sts_status sts_shape(sts_ctx* ctx, int32_t field, int64_t* nx, int64_t* ny, int64_t* i0, int64_t* ni)
+{
+    if (!ctx || !nx || !ny || !i0 || !ni) return fail(ctx, STS_E_ARG, "null argument");
+    bool last = ctx->rank == ctx->world - 1;
+    *nx = ctx->nloc + ((field == STS_U || field == STS_UEXP) && last ? 1 : 0);
+    *ny = (field == STS_V || field == STS_VEXP) ? ctx->ny + 1 : ctx->ny;
+    *i0 = ctx->gi0;
+    *ni = ctx->nloc;
+    return STS_OK;
+}
+
+extern "C" sts_status sts_constants(sts_ctx* ctx, double* out)
+{
+    if (!ctx || !out) return fail(ctx, STS_E_ARG, "null argument");
+    out[0] = ctx->A; out[1] = ctx->B; out[2] = ctx->CT1; out[3] = ctx->CT2; out[4] = ctx->CT3; out[5] = ctx->u_in; out[6] = ctx->sch.dt;
+    return STS_OK;
+}
+
+extern "C" sts_status sts_profile(sts_ctx* ctx, int32_t enable)
+{
+    if (!ctx) return fail(ctx, STS_E_ARG, "null ctx");
+    ctx->profiling = enable != 0;
+    return STS_OK;
+}
+
+extern "C" sts_status sts_profile_read(sts_ctx* ctx, double* out, int32_t reset)
+{
+    if (!ctx || !out) return fail(ctx, STS_E_ARG, "null argument");
+    prof_collect(ctx);
+    out[0] = ctx->prof_pass_n; out[1] = ctx->prof_pass_ms; out[2] = ctx->prof_conv_n; out[3] = ctx->prof_conv_ms; out[4] = ctx->launches;
+    if (reset) ctx->prof_pass_n = ctx->prof_pass_ms = ctx->prof_conv_n = ctx->prof_conv_ms = ctx->launches = 0;
+    return STS_OK;
+}
+
+// residual slots -> stats (reading R35); returns STS_E_STATE on a bad state
+static sts_status finish_residuals(sts_ctx* ctx, const unsigned long long* r)
+{
+    double v[7];
+    for (int q = 0; q < 7; q++) { long long b = (long long)r[q]; memcpy(&v[q], &b, 8); }
+    double vel = v[4], pm = v[5], Tm = v[6];
+    ctx->stats.res[0] = vel > 0 ? v[0] / vel : v[0];
+    ctx->stats.res[1] = vel > 0 ? v[1] / vel : v[1];
+    ctx->stats.res[2] = pm > 0 ? v[2] / pm : v[2];
+    ctx->stats.res[3] = Tm > 0 ? v[3] / Tm : v[3];
+    bool bad = r[7] != 0;
+    for (int q = 0; q < 7; q++) if (!(v[q] == v[q]) || std::isinf(v[q])) bad = true;
+    if (bad) {
+        ctx->stats.bad_cell = r[7] ? (long long)(0x7fffffffffffffffULL - r[7]) : -1;
+        ctx->stats.bad_field = (int)r[8];
+        return fail(ctx, STS_E_STATE, "non-finite or non-positive state (see sts_stats.bad_cell)");
+    }
+    return STS_OK;
+}
+
+static sts_status allreduce_red(sts_ctx* ctx, unsigned long long* slot)
+{
+    if (ctx->world == 1) return STS_OK;
+    if (g_nccl.AllReduce(slot, slot, 9, NCCL_UINT64, NCCL_MAX, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclAllReduce");
+    return STS_OK;
+}
+
+extern "C" sts_status sts_advance(sts_ctx* ctx, int32_t n_steps, sts_stats* out)
+{
+    if (!ctx || n_steps < 0) return fail(ctx, STS_E_ARG, "bad argument");
+    CU(cudaSetDevice(ctx->device));
+    const int impl = ctx->sch.time == STS_IMPLICIT, tvd = ctx->sch.space == STS_TVD_VANLEER;
+    pass_fn pass = pass_table(impl, tvd);
+    const dim3 grid((ctx->nloc + TX - 1) / TX, (ctx->ny + TY - 1) / TY);
+    const size_t smem = sizeof(Smem);
+    const bool tolmode = ctx->sch.tol > 0;
+    sts_status status = STS_OK;
+    unsigned long long* last_slot = nullptr;
+    for (int step = 0; step < n_steps; step++) {
+        // a0: n-1 := current state; old := n-1; ping-pong between the other two
+        const int n1 = ctx->cur, a = (n1 + 1) % 3, b = (n1 + 2) % 3;
+        Params k = make_params(ctx);
+        k.u_1 = ctx->snap[n1].u; k.v_1 = ctx->snap[n1].v; k.p_1 = ctx->snap[n1].p; k.T_1 = ctx->snap[n1].T;
+        k.ue = ctx->ue; k.ve = ctx->ve; k.Te = ctx->Te;
+        CU(cudaMemsetAsync(ctx->red, 0, (size_t)ctx->sch.max_passes * 9 * sizeof(unsigned long long), ctx->stream));
+        if (!impl) {   // a1: explicit planes, once per time step
+            k.ue_w = ctx->ue; k.ve_w = ctx->ve; k.Te_w = ctx->Te;
+            prof_begin(ctx, 1);
+            conv_table(tvd)<<<grid, NT, smem, ctx->stream>>>(k);
+            prof_end(ctx);
+            ctx->launches++;
+            CU(cudaGetLastError());
+            if (ctx->world > 1) {   // plane halos: reuse the exchange with the planes as fields
+                Snapshot pl{ctx->ue, ctx->ve, ctx->Te, ctx->Te};
+                sts_status st = exchange(ctx, pl);
+                if (st != STS_OK) return st;
+            }
+        }
+        int old = n1, nw = a, passes = 0;
+        bool conv = false;
+        for (int it = 0; it < ctx->sch.max_passes; it++) {
+            k.u_o = ctx->snap[old].u; k.v_o = ctx->snap[old].v; k.p_o = ctx->snap[old].p; k.T_o = ctx->snap[old].T;
+            k.u_w = ctx->snap[nw].u; k.v_w = ctx->snap[nw].v; k.p_w = ctx->snap[nw].p; k.T_w = ctx->snap[nw].T;
+            k.red = ctx->red + (size_t)it * 9;
+            prof_begin(ctx, 0);
+            pass<<<grid, NT, smem, ctx->stream>>>(k);
+            prof_end(ctx);
+            ctx->launches++;
+            CU(cudaGetLastError());
+            sts_status st = exchange(ctx, ctx->snap[nw]);
+            if (st != STS_OK) return st;
+            passes++;
+            last_slot = k.red;
+            old = nw;
+            nw = (nw == a) ? b : a;
+            if (tolmode && passes >= ctx->sch.min_passes) {
+                st = allreduce_red(ctx, k.red);
+                if (st != STS_OK) return st;
+                CU(cudaMemcpyAsync(ctx->h_red, k.red, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+                CU(cudaStreamSynchronize(ctx->stream));
+                st = finish_residuals(ctx, ctx->h_red);
+                if (st != STS_OK) { ctx->cur = old; return st; }
+                const double* r = ctx->stats.res;
+                if (r[0] < ctx->sch.tol && r[1] < ctx->sch.tol && r[2] < ctx->sch.tol && r[3] < ctx->sch.tol) { conv = true; break; }
+            }
+        }
+        ctx->cur = old;
+        ctx->stats.steps_done++;
+        ctx->stats.passes_done += passes;
+        ctx->stats.converged = conv ? 1 : 0;
+        if (tolmode && !conv) status = STS_E_NONCONVERGED;
+    }
+    if (last_slot && !tolmode) {
+        sts_status st = allreduce_red(ctx, last_slot);
+        if (st != STS_OK) return st;
+        CU(cudaMemcpyAsync(ctx->h_red, last_slot, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        st = finish_residuals(ctx, ctx->h_red);
+        if (st != STS_OK) { if (out) *out = ctx->stats; return st; }
+    }
+    if (out) *out = ctx->stats;
+    if (status == STS_E_NONCONVERGED) return fail(ctx, status, "loop 2 reached max_passes without convergence");
+    return STS_OK;
+}

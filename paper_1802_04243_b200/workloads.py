@@ -62,6 +62,13 @@ def c3(H=200, variant="implicit_upwind", passes=10):
     return _case(4032, ny, 0.05, squares, variant, 0.005, passes, name=f"C3_H{H}")
 
 
+def c3_long(G, variant="implicit_upwind", passes=10):
+    """Weak-scaling channel for G GPUs: G copies of the C3 H = 200 mesh laid end to
+    end (4032 G x 4000, a column of 20 squares every 201.6 units), one slab per GPU."""
+    squares = [(110 + 4032 * m, 90 + 200 * k, 20, 20) for m in range(G) for k in range(20)]
+    return _case(4032 * G, 4000, 0.05, squares, variant, 0.005, passes, name=f"C3L_G{G}")
+
+
 def c4(variant="implicit_upwind", passes=10):
     """C4: H = 200, L = 201.6, Delta = 0.02 -> 10080 x 10000 (100.8 M FVs);
     20 squares of 50x50 cells at i0 = 275, j0 = 225 + 500k."""
