@@ -104,7 +104,8 @@ typedef struct {
 /* Multi-GPU: one process per GPU; the channel is split into slabs along x
  * (DESIGN section 7).  nccl_id points to the 128-byte ncclUniqueId made by
  * sts_nccl_unique_id on rank 0 and broadcast by the caller.  NULL dist or
- * world == 1 -> single GPU. */
+ * world == 1 -> single GPU; world > 1 with nccl_id == NULL -> an in-process
+ * slab of a group driven by sts_advance_group. */
 typedef struct { int32_t rank, world, device; const void* nccl_id; } sts_dist;
 
 /* Statistics of the last sts_advance: steps/passes done (cumulative), last
@@ -148,6 +149,14 @@ sts_status sts_set_field_device(sts_ctx* ctx, int32_t field, const double* dev, 
 
 /* Loop 1 x loop 2 (Figs. 1-2, GPU columns): n_steps time steps. */
 sts_status sts_advance(sts_ctx* ctx, int32_t n_steps, sts_stats* out);
+
+/* Advance n in-process slab contexts in lockstep: contexts created with
+ * dist = {rank r, world n, device d, nccl_id = NULL} for r = 0..n-1 on the
+ * same device form one x-decomposed domain whose per-pass halo exchange is a
+ * device-to-device copy on ctxs[0]'s stream instead of NCCL (same pack /
+ * unpack kernels, same halo index maps).  Used to verify the slab
+ * decomposition on one GPU; stats are the group's. */
+sts_status sts_advance_group(sts_ctx** ctxs, int32_t n, int32_t n_steps, sts_stats* out);
 
 /* Copy this rank's owned part of a field to a host buffer of n doubles
  * (global shape for a single GPU; slab shape per sts_shape otherwise). */

@@ -8,12 +8,14 @@
 // NCCL after every pass.
 #include "../../include/simplets.h"
 #include "sts_kernels.cuh"
+#include "sts_march.cuh"
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -88,7 +90,10 @@ struct sts_ctx {
     int cur = 0;                           // index of the current state snapshot
     double *ue = nullptr, *ve = nullptr, *Te = nullptr;
     uint8_t *ck = nullptr, *uk = nullptr, *vk = nullptr;
+    uint32_t* kind32 = nullptr;            // packed ck | uk << 8 | vk << 16, (ny+1) x pitch
     std::vector<uint8_t> h_ck, h_uk, h_vk; // host copies of the local kind maps
+    bool use_tile = false;                 // STS_KERNEL=tile: v1 2-D tile kernel
+    int march_seg = 0, march_nseg = 0;
     unsigned long long* red = nullptr;     // [max_passes][9]
     unsigned long long* h_red = nullptr;   // pinned, 9 entries
     double* stage = nullptr;               // device staging (global-shape field)
@@ -98,6 +103,7 @@ struct sts_ctx {
     cudaStream_t stream = nullptr;
     // multi-GPU
     nccl_comm comm = nullptr;
+    bool local_group = false;              // world > 1 without NCCL: in-process slabs (sts_advance_group)
     // stats / profiling
     sts_stats stats{};
     bool profiling = false;
@@ -233,6 +239,12 @@ static pass_fn pass_table(int impl, int tvd)
     return tvd ? pass_kernel<false, true> : pass_kernel<false, false>;
 }
 static pass_fn conv_table(int tvd) { return tvd ? conv_kernel<true> : conv_kernel<false>; }
+typedef void (*march_fn)(MarchParams);
+static march_fn march_table(int impl, int tvd)
+{
+    if (impl) return tvd ? march_kernel<true, true> : march_kernel<true, false>;
+    return tvd ? march_kernel<false, true> : march_kernel<false, false>;
+}
 
 static sts_status set_smem_attrs(sts_ctx* ctx)
 {
@@ -241,6 +253,9 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
     const int bytes = (int)sizeof(Smem);
     pass_fn fns[6] = {pass_table(0, 0), pass_table(0, 1), pass_table(1, 0), pass_table(1, 1), conv_table(0), conv_table(1)};
     for (pass_fn f : fns) CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    march_fn mfs[4] = {march_table(0, 0), march_table(0, 1), march_table(1, 0), march_table(1, 1)};
+    for (march_fn f : mfs)
+        CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));
     done = true;
     return STS_OK;
 }
@@ -258,6 +273,50 @@ static Params make_params(const sts_ctx* c)
     k.g_x = c->gas.g_x; k.g_y = c->gas.g_y; k.pw_sign = c->gas.pw_sign;
     k.ck = c->ck; k.uk = c->uk; k.vk = c->vk;
     return k;
+}
+
+static MarchParams make_march(const sts_ctx* c, const Params& k)
+{
+    MarchParams m{};
+    m.k = k;
+    m.kind = c->kind32;
+    m.seg = c->march_seg;
+    const double dx = c->spacing, dy = c->spacing, dt = c->sch.dt;
+    m.inv_dx = 1.0 / dx; m.inv_dy = 1.0 / dy;
+    m.CT1_dydx = c->CT1 * dy / dx; m.CT1_dxdy = c->CT1 * dx / dy;
+    m.B_dydx = c->B * dy / dx; m.B_dxdy = c->B * dx / dy;
+    m.c_t = dx * dy / (2.0 * dt); m.dV = dx * dy; m.half_dV = 0.5 * dx * dy;
+    m.A_dy = c->A * dy; m.A_dx = c->A * dx;
+    return m;
+}
+
+// Segment height of the y-march: maximise (useful rows / (rows + warm-up)) x
+// (CTAs / (waves x resident CTAs on 148 SMs)).
+static void choose_segments(sts_ctx* c)
+{
+    int dev_sms = 148, per_sm = 3;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)march_table(1, 1), MX, sizeof(MarchSmem)) == cudaSuccess && nb > 0)
+        per_sm = nb;
+    const int strips = (c->nloc + MW - 1) / MW;
+    const long long slots = (long long)dev_sms * per_sm;
+    double best = -1;
+    int best_n = 1;
+    for (int n = 1; n <= std::max(1, c->ny / 16); n++) {
+        int seg = (c->ny + n - 1) / n;
+        long long ctas = (long long)strips * n;
+        long long waves = (ctas + slots - 1) / slots;
+        double eff = (double)ctas / (double)(waves * slots) * (double)seg / (double)(seg + WARM);
+        if (eff > best + 1e-9) { best = eff; best_n = n; }
+    }
+    c->march_nseg = best_n;
+    c->march_seg = (c->ny + best_n - 1) / best_n;
+    if (const char* sv = getenv("STS_SEG")) {         // test hook: force short segments
+        int v = atoi(sv);
+        if (v > 0) c->march_seg = v;
+    }
+    c->march_nseg = (c->ny + c->march_seg - 1) / c->march_seg;
 }
 
 // ------------------------------------------------------------- profiling
@@ -296,37 +355,71 @@ static void prof_collect(sts_ctx* c)
 }
 
 // ------------------------------------------------------------- halo exchange
-static sts_status exchange(sts_ctx* ctx, const Snapshot& s)
+// Slab halos: my first OFF owned columns go to the left
+// neighbour's right ghost columns, my last OFF owned columns to the right
+// neighbour's left ghosts; u, v, p, T (or the three explicit planes).
+static int left_of(const sts_ctx* c) { return c->rank > 0 ? c->rank - 1 : (is_periodic(c) ? c->world - 1 : -1); }
+static int right_of(const sts_ctx* c) { return c->rank < c->world - 1 ? c->rank + 1 : (is_periodic(c) ? 0 : -1); }
+static int halo_per(const sts_ctx* c) { return 4 * OFF * (c->ny + 1); }
+
+static sts_status halo_pack(sts_ctx* ctx, const Snapshot& s, cudaStream_t st)
 {
-    if (ctx->world == 1) return STS_OK;
-    const int per = 4 * OFF * (ctx->ny + 1);
-    const bool periodic = is_periodic(ctx);
-    const int left = ctx->rank > 0 ? ctx->rank - 1 : (periodic ? ctx->world - 1 : -1);
-    const int right = ctx->rank < ctx->world - 1 ? ctx->rank + 1 : (periodic ? 0 : -1);
-    double* sendL = ctx->halo;
-    double* sendR = ctx->halo + per;
-    double* recvL = ctx->halo + 2 * per;
-    double* recvR = ctx->halo + 3 * per;
-    const int blocks = (per + 255) / 256;
-    // my first OFF owned columns go left, my last OFF owned columns go right
-    if (left >= 0) { halo_pack_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->ny, ctx->pitch, OFF, s.u, s.v, s.p, s.T, sendL); ctx->launches++; }
-    if (right >= 0) { halo_pack_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->ny, ctx->pitch, ctx->nloc, s.u, s.v, s.p, s.T, sendR); ctx->launches++; }
+    const int per = halo_per(ctx), blocks = (per + 255) / 256;
+    if (left_of(ctx) >= 0) { halo_pack_kernel<<<blocks, 256, 0, st>>>(ctx->ny, ctx->pitch, OFF, s.u, s.v, s.p, s.T, ctx->halo); ctx->launches++; }
+    if (right_of(ctx) >= 0) { halo_pack_kernel<<<blocks, 256, 0, st>>>(ctx->ny, ctx->pitch, ctx->nloc, s.u, s.v, s.p, s.T, ctx->halo + per); ctx->launches++; }
     CU(cudaGetLastError());
+    return STS_OK;
+}
+static sts_status halo_unpack(sts_ctx* ctx, const Snapshot& s, cudaStream_t st)
+{
+    const int per = halo_per(ctx), blocks = (per + 255) / 256;
+    if (left_of(ctx) >= 0) { halo_unpack_kernel<<<blocks, 256, 0, st>>>(ctx->ny, ctx->pitch, 0, s.u, s.v, s.p, s.T, ctx->halo + 2 * per); ctx->launches++; }
+    if (right_of(ctx) >= 0) { halo_unpack_kernel<<<blocks, 256, 0, st>>>(ctx->ny, ctx->pitch, OFF + ctx->nloc, s.u, s.v, s.p, s.T, ctx->halo + 3 * per); ctx->launches++; }
+    CU(cudaGetLastError());
+    return STS_OK;
+}
+// NCCL transport: grouped send/recv with both neighbours on the context stream.
+static sts_status halo_nccl(sts_ctx* ctx)
+{
+    const int per = halo_per(ctx);
+    const int left = left_of(ctx), right = right_of(ctx);
     if (g_nccl.GroupStart()) return fail(ctx, STS_E_COMM, "ncclGroupStart");
     if (left >= 0) {
-        if (g_nccl.Send(sendL, per, NCCL_FLOAT64, left, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclSend");
-        if (g_nccl.Recv(recvL, per, NCCL_FLOAT64, left, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclRecv");
+        if (g_nccl.Send(ctx->halo, per, NCCL_FLOAT64, left, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclSend");
+        if (g_nccl.Recv(ctx->halo + 2 * per, per, NCCL_FLOAT64, left, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclRecv");
     }
     if (right >= 0) {
-        if (g_nccl.Send(sendR, per, NCCL_FLOAT64, right, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclSend");
-        if (g_nccl.Recv(recvR, per, NCCL_FLOAT64, right, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclRecv");
+        if (g_nccl.Send(ctx->halo + per, per, NCCL_FLOAT64, right, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclSend");
+        if (g_nccl.Recv(ctx->halo + 3 * per, per, NCCL_FLOAT64, right, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclRecv");
     }
     if (g_nccl.GroupEnd()) return fail(ctx, STS_E_COMM, "ncclGroupEnd");
-    // left neighbour's last OFF owned columns are my ghost columns [0, OFF);
-    // right neighbour's first OFF owned columns are my ghosts [OFF+nloc, 2 OFF+nloc)
-    if (left >= 0) { halo_unpack_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->ny, ctx->pitch, 0, s.u, s.v, s.p, s.T, recvL); ctx->launches++; }
-    if (right >= 0) { halo_unpack_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->ny, ctx->pitch, OFF + ctx->nloc, s.u, s.v, s.p, s.T, recvR); ctx->launches++; }
-    CU(cudaGetLastError());
+    return STS_OK;
+}
+// One halo exchange of snapshot `which` (0..2 = snapshots, 3 = explicit planes)
+// for a group of n contexts (n == 1: this process' rank, NCCL if world > 1;
+// n == world: in-process slabs, device-to-device copies on one stream).
+static Snapshot pick(sts_ctx* c, int which)
+{
+    if (which == 3) return Snapshot{c->ue, c->ve, c->Te, c->Te};
+    return c->snap[which];
+}
+static sts_status exchange_group(sts_ctx** cs, int n, const int* which, cudaStream_t st)
+{
+    if (cs[0]->world == 1) return STS_OK;
+    for (int r = 0; r < n; r++) { sts_status e = halo_pack(cs[r], pick(cs[r], which[r]), st); if (e) return e; }
+    if (n == 1) {
+        sts_status e = halo_nccl(cs[0]);
+        if (e) return e;
+    } else {
+        for (int r = 0; r < n; r++) {
+            sts_ctx* ctx = cs[r];
+            const int per = halo_per(ctx);
+            const int l = left_of(ctx), rr = right_of(ctx);
+            if (l >= 0) CU(cudaMemcpyAsync(ctx->halo + 2 * per, cs[l]->halo + per, per * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            if (rr >= 0) CU(cudaMemcpyAsync(ctx->halo + 3 * per, cs[rr]->halo, per * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    for (int r = 0; r < n; r++) { sts_status e = halo_unpack(cs[r], pick(cs[r], which[r]), st); if (e) return e; }
     return STS_OK;
 }
 
@@ -443,8 +536,24 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
     cudaMemcpy(ctx->ck, ctx->h_ck.data(), nce, cudaMemcpyHostToDevice);
     cudaMemcpy(ctx->uk, ctx->h_uk.data(), nce, cudaMemcpyHostToDevice);
     cudaMemcpy(ctx->vk, ctx->h_vk.data(), nve, cudaMemcpyHostToDevice);
-    if (world > 1) {
-        if (!dist->nccl_id) { sts_destroy(ctx); return fail(nullptr, STS_E_ARG, "world > 1 needs an NCCL id"); }
+    {
+        std::vector<uint32_t> packed(nve);
+        for (size_t e = 0; e < nve; e++) {
+            uint32_t ckv = e < nce ? ctx->h_ck[e] : (uint32_t)CK_WALLY;
+            uint32_t ukv = e < nce ? ctx->h_uk[e] : (uint32_t)FK_NONE;
+            packed[e] = ckv | (ukv << 8) | ((uint32_t)ctx->h_vk[e] << 16);
+        }
+        if (cudaMalloc(&ctx->kind32, nve * sizeof(uint32_t)) != cudaSuccess) { sts_destroy(ctx); return fail(nullptr, STS_E_OOM, "device allocation failed"); }
+        cudaMemcpy(ctx->kind32, packed.data(), nve * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    }
+    {
+        const char* kv = getenv("STS_KERNEL");
+        ctx->use_tile = kv && std::string(kv) == "tile";
+    }
+    choose_segments(ctx);
+    if (world > 1 && !dist->nccl_id) {
+        ctx->local_group = true;            // slabs of one process, driven by sts_advance_group
+    } else if (world > 1) {
         if (!g_nccl.load()) { sts_destroy(ctx); return fail(nullptr, STS_E_COMM, "libnccl.so.2 not loadable"); }
         nccl_uid id;
         memcpy(&id, dist->nccl_id, 128);
@@ -464,7 +573,7 @@ extern "C" void sts_destroy(sts_ctx* ctx)
     cudaDeviceSynchronize();
     for (int k = 0; k < 3; k++) { cudaFree(ctx->snap[k].u); cudaFree(ctx->snap[k].v); cudaFree(ctx->snap[k].p); cudaFree(ctx->snap[k].T); }
     cudaFree(ctx->ue); cudaFree(ctx->ve); cudaFree(ctx->Te); cudaFree(ctx->stage); cudaFree(ctx->halo);
-    cudaFree(ctx->ck); cudaFree(ctx->uk); cudaFree(ctx->vk); cudaFree(ctx->red);
+    cudaFree(ctx->ck); cudaFree(ctx->uk); cudaFree(ctx->vk); cudaFree(ctx->kind32); cudaFree(ctx->red);
     if (ctx->h_red) cudaFreeHost(ctx->h_red);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
@@ -710,87 +819,146 @@ static sts_status finish_residuals(sts_ctx* ctx, const unsigned long long* r)
     return STS_OK;
 }
 
-static sts_status allreduce_red(sts_ctx* ctx, unsigned long long* slot)
+// Max-combine the residual slots of a pass over all slabs: NCCL MAX allreduce
+// on the u64 bit patterns (order-independent, exact) or, in-process, on the host.
+static sts_status gather_red(sts_ctx** cs, int n, int it, unsigned long long* out, cudaStream_t st)
 {
-    if (ctx->world == 1) return STS_OK;
-    if (g_nccl.AllReduce(slot, slot, 9, NCCL_UINT64, NCCL_MAX, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclAllReduce");
+    sts_ctx* ctx = cs[0];
+    for (int q = 0; q < 9; q++) out[q] = 0;
+    if (n == 1 && ctx->world > 1) {
+        unsigned long long* slot = ctx->red + (size_t)it * 9;
+        if (g_nccl.AllReduce(slot, slot, 9, NCCL_UINT64, NCCL_MAX, ctx->comm, st)) return fail(ctx, STS_E_COMM, "ncclAllReduce");
+    }
+    for (int r = 0; r < n; r++) {
+        CU(cudaMemcpyAsync(cs[r]->h_red, cs[r]->red + (size_t)it * 9, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    }
+    CU(cudaStreamSynchronize(st));
+    for (int r = 0; r < n; r++)
+        for (int q = 0; q < 9; q++) out[q] = std::max(out[q], cs[r]->h_red[q]);
+    return STS_OK;
+}
+
+// Loop 1 x loop 2 for a group of slab contexts advanced in lockstep (n == 1
+// for the usual one-context-per-process case).
+static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
+{
+    sts_ctx* ctx = cs[0];
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const int impl = ctx->sch.time == STS_IMPLICIT, tvd = ctx->sch.space == STS_TVD_VANLEER;
+    pass_fn pass = pass_table(impl, tvd);
+    march_fn march = march_table(impl, tvd);
+    const size_t smem = sizeof(Smem);
+    const bool tolmode = ctx->sch.tol > 0;
+    sts_status status = STS_OK;
+    int last_it = -1;
+    std::vector<int> n1(n), a(n), b(n), old(n), nw(n), which(n);
+    unsigned long long red[9];
+    for (int step = 0; step < n_steps; step++) {
+        for (int r = 0; r < n; r++) {
+            sts_ctx* c = cs[r];
+            // a0: n-1 := current state; old := n-1; ping-pong between the other two
+            n1[r] = c->cur; a[r] = (n1[r] + 1) % 3; b[r] = (n1[r] + 2) % 3;
+            old[r] = n1[r]; nw[r] = a[r];
+            CU(cudaMemsetAsync(c->red, 0, (size_t)c->sch.max_passes * 9 * sizeof(unsigned long long), st));
+        }
+        auto base = [&](sts_ctx* c, int r) {
+            Params k = make_params(c);
+            k.u_1 = c->snap[n1[r]].u; k.v_1 = c->snap[n1[r]].v; k.p_1 = c->snap[n1[r]].p; k.T_1 = c->snap[n1[r]].T;
+            k.ue = c->ue; k.ve = c->ve; k.Te = c->Te;
+            return k;
+        };
+        if (!impl) {   // a1: explicit planes, once per time step (P:123, P:166-168)
+            for (int r = 0; r < n; r++) {
+                sts_ctx* c = cs[r];
+                Params k = base(c, r);
+                k.ue_w = c->ue; k.ve_w = c->ve; k.Te_w = c->Te;
+                const dim3 grid((c->nloc + TX - 1) / TX, (c->ny + TY - 1) / TY);
+                prof_begin(c, 1);
+                conv_table(tvd)<<<grid, NT, smem, st>>>(k);
+                prof_end(c);
+                c->launches++;
+                CU(cudaGetLastError());
+                which[r] = 3;
+            }
+            sts_status e = exchange_group(cs, n, which.data(), st);
+            if (e) return e;
+        }
+        int passes = 0;
+        bool conv = false;
+        for (int it = 0; it < ctx->sch.max_passes; it++) {
+            for (int r = 0; r < n; r++) {
+                sts_ctx* c = cs[r];
+                Params k = base(c, r);
+                k.u_o = c->snap[old[r]].u; k.v_o = c->snap[old[r]].v; k.p_o = c->snap[old[r]].p; k.T_o = c->snap[old[r]].T;
+                k.u_w = c->snap[nw[r]].u; k.v_w = c->snap[nw[r]].v; k.p_w = c->snap[nw[r]].p; k.T_w = c->snap[nw[r]].T;
+                k.red = c->red + (size_t)it * 9;
+                prof_begin(c, 0);
+                if (c->use_tile) {
+                    const dim3 grid((c->nloc + TX - 1) / TX, (c->ny + TY - 1) / TY);
+                    pass<<<grid, NT, smem, st>>>(k);
+                } else {
+                    const dim3 mgrid((c->nloc + MW - 1) / MW, c->march_nseg);
+                    march<<<mgrid, MX, sizeof(MarchSmem), st>>>(make_march(c, k));
+                }
+                prof_end(c);
+                c->launches++;
+                CU(cudaGetLastError());
+                which[r] = nw[r];
+            }
+            sts_status e = exchange_group(cs, n, which.data(), st);
+            if (e) return e;
+            passes++;
+            last_it = it;
+            for (int r = 0; r < n; r++) { old[r] = nw[r]; nw[r] = (nw[r] == a[r]) ? b[r] : a[r]; }
+            if (tolmode && passes >= ctx->sch.min_passes) {
+                e = gather_red(cs, n, it, red, st);
+                if (e) return e;
+                for (int r = 0; r < n; r++) cs[r]->cur = old[r];
+                e = finish_residuals(ctx, red);
+                for (int r = 1; r < n; r++) { cs[r]->stats = ctx->stats; }
+                if (e) return e;
+                const double* rs = ctx->stats.res;
+                if (rs[0] < ctx->sch.tol && rs[1] < ctx->sch.tol && rs[2] < ctx->sch.tol && rs[3] < ctx->sch.tol) { conv = true; break; }
+            }
+        }
+        for (int r = 0; r < n; r++) {
+            sts_ctx* c = cs[r];
+            c->cur = old[r];
+            c->stats.steps_done++;
+            c->stats.passes_done += passes;
+            c->stats.converged = conv ? 1 : 0;
+        }
+        if (tolmode && !conv) status = STS_E_NONCONVERGED;
+    }
+    if (last_it >= 0 && !tolmode) {
+        sts_status e = gather_red(cs, n, last_it, red, st);
+        if (e) return e;
+        e = finish_residuals(ctx, red);
+        for (int r = 1; r < n; r++) { cs[r]->stats.res[0] = ctx->stats.res[0]; cs[r]->stats.res[1] = ctx->stats.res[1];
+                                      cs[r]->stats.res[2] = ctx->stats.res[2]; cs[r]->stats.res[3] = ctx->stats.res[3]; }
+        if (e) { if (out) *out = ctx->stats; return e; }
+    }
+    if (out) *out = ctx->stats;
+    if (status == STS_E_NONCONVERGED) return fail(ctx, status, "loop 2 reached max_passes without convergence");
     return STS_OK;
 }
 
 extern "C" sts_status sts_advance(sts_ctx* ctx, int32_t n_steps, sts_stats* out)
 {
     if (!ctx || n_steps < 0) return fail(ctx, STS_E_ARG, "bad argument");
-    CU(cudaSetDevice(ctx->device));
-    const int impl = ctx->sch.time == STS_IMPLICIT, tvd = ctx->sch.space == STS_TVD_VANLEER;
-    pass_fn pass = pass_table(impl, tvd);
-    const dim3 grid((ctx->nloc + TX - 1) / TX, (ctx->ny + TY - 1) / TY);
-    const size_t smem = sizeof(Smem);
-    const bool tolmode = ctx->sch.tol > 0;
-    sts_status status = STS_OK;
-    unsigned long long* last_slot = nullptr;
-    for (int step = 0; step < n_steps; step++) {
-        // a0: n-1 := current state; old := n-1; ping-pong between the other two
-        const int n1 = ctx->cur, a = (n1 + 1) % 3, b = (n1 + 2) % 3;
-        Params k = make_params(ctx);
-        k.u_1 = ctx->snap[n1].u; k.v_1 = ctx->snap[n1].v; k.p_1 = ctx->snap[n1].p; k.T_1 = ctx->snap[n1].T;
-        k.ue = ctx->ue; k.ve = ctx->ve; k.Te = ctx->Te;
-        CU(cudaMemsetAsync(ctx->red, 0, (size_t)ctx->sch.max_passes * 9 * sizeof(unsigned long long), ctx->stream));
-        if (!impl) {   // a1: explicit planes, once per time step (P:123, P:166-168)
-            k.ue_w = ctx->ue; k.ve_w = ctx->ve; k.Te_w = ctx->Te;
-            prof_begin(ctx, 1);
-            conv_table(tvd)<<<grid, NT, smem, ctx->stream>>>(k);
-            prof_end(ctx);
-            ctx->launches++;
-            CU(cudaGetLastError());
-            if (ctx->world > 1) {   // plane halos: reuse the exchange with the planes as fields
-                Snapshot pl{ctx->ue, ctx->ve, ctx->Te, ctx->Te};
-                sts_status st = exchange(ctx, pl);
-                if (st != STS_OK) return st;
-            }
-        }
-        int old = n1, nw = a, passes = 0;
-        bool conv = false;
-        for (int it = 0; it < ctx->sch.max_passes; it++) {
-            k.u_o = ctx->snap[old].u; k.v_o = ctx->snap[old].v; k.p_o = ctx->snap[old].p; k.T_o = ctx->snap[old].T;
-            k.u_w = ctx->snap[nw].u; k.v_w = ctx->snap[nw].v; k.p_w = ctx->snap[nw].p; k.T_w = ctx->snap[nw].T;
-            k.red = ctx->red + (size_t)it * 9;
-            prof_begin(ctx, 0);
-            pass<<<grid, NT, smem, ctx->stream>>>(k);
-            prof_end(ctx);
-            ctx->launches++;
-            CU(cudaGetLastError());
-            sts_status st = exchange(ctx, ctx->snap[nw]);
-            if (st != STS_OK) return st;
-            passes++;
-            last_slot = k.red;
-            old = nw;
-            nw = (nw == a) ? b : a;
-            if (tolmode && passes >= ctx->sch.min_passes) {
-                st = allreduce_red(ctx, k.red);
-                if (st != STS_OK) return st;
-                CU(cudaMemcpyAsync(ctx->h_red, k.red, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
-                CU(cudaStreamSynchronize(ctx->stream));
-                st = finish_residuals(ctx, ctx->h_red);
-                if (st != STS_OK) { ctx->cur = old; return st; }
-                const double* r = ctx->stats.res;
-                if (r[0] < ctx->sch.tol && r[1] < ctx->sch.tol && r[2] < ctx->sch.tol && r[3] < ctx->sch.tol) { conv = true; break; }
-            }
-        }
-        ctx->cur = old;
-        ctx->stats.steps_done++;
-        ctx->stats.passes_done += passes;
-        ctx->stats.converged = conv ? 1 : 0;
-        if (tolmode && !conv) status = STS_E_NONCONVERGED;
+    if (ctx->local_group) return fail(ctx, STS_E_ARG, "in-process slab contexts advance with sts_advance_group");
+    return drive(&ctx, 1, n_steps, out);
+}
+
+extern "C" sts_status sts_advance_group(sts_ctx** ctxs, int32_t n, int32_t n_steps, sts_stats* out)
+{
+    sts_ctx* ctx = nullptr;
+    if (!ctxs || n < 1 || n_steps < 0) return fail(ctx, STS_E_ARG, "bad argument");
+    for (int r = 0; r < n; r++) {
+        if (!ctxs[r] || ctxs[r]->world != n || ctxs[r]->rank != r || (n > 1 && !ctxs[r]->local_group) ||
+            ctxs[r]->device != ctxs[0]->device)
+            return fail(ctxs[r], STS_E_ARG, "group must be ranks 0..n-1 of one in-process decomposition on one device");
     }
-    if (last_slot && !tolmode) {
-        sts_status st = allreduce_red(ctx, last_slot);
-        if (st != STS_OK) return st;
-        CU(cudaMemcpyAsync(ctx->h_red, last_slot, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-        st = finish_residuals(ctx, ctx->h_red);
-        if (st != STS_OK) { if (out) *out = ctx->stats; return st; }
-    }
-    if (out) *out = ctx->stats;
-    if (status == STS_E_NONCONVERGED) return fail(ctx, status, "loop 2 reached max_passes without convergence");
-    return STS_OK;
+    return drive(ctxs, n, n_steps, out);
 }

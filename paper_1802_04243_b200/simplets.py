@@ -24,7 +24,7 @@ STS_X_INFLOW_OUTFLOW, STS_X_PERIODIC = 0, 1
 FIELDS = {"u": 0, "v": 1, "p": 2, "T": 3, "rho": 4, "uexp": 6, "vexp": 7, "Texp": 8}
 
 EXPORTS = ["sts_create", "sts_destroy", "sts_last_error", "sts_set_stream", "sts_init_freestream",
-           "sts_set_field", "sts_set_field_device", "sts_advance", "sts_get_field", "sts_get_field_device",
+           "sts_set_field", "sts_set_field_device", "sts_advance", "sts_advance_group", "sts_get_field", "sts_get_field_device",
            "sts_get_map", "sts_shape", "sts_constants", "sts_profile", "sts_profile_read", "sts_nccl_unique_id"]
 
 
@@ -98,6 +98,8 @@ def lib():
             getattr(L, f).argtypes = [vp, ctypes.c_int32, vp, ctypes.c_int64]
         L.sts_advance.restype = st
         L.sts_advance.argtypes = [vp, ctypes.c_int32, ctypes.POINTER(sts_stats)]
+        L.sts_advance_group.restype = st
+        L.sts_advance_group.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(sts_stats)]
         L.sts_get_map.restype = st
         L.sts_get_map.argtypes = [vp, ctypes.c_int32, ip, ctypes.c_int64]
         L.sts_shape.restype = st
@@ -118,6 +120,15 @@ def _check(status, handle=None):
     if status != STS_OK:
         msg = lib().sts_last_error(handle)
         raise StsError(status, msg.decode() if msg else "")
+
+
+def advance_group(solvers, n_steps):
+    """Advance in-process slab solvers (ranks 0..n-1, nccl_id=None) in lockstep."""
+    n = len(solvers)
+    arr = (ctypes.c_void_p * n)(*[s._h.value for s in solvers])
+    st = sts_stats()
+    _check(lib().sts_advance_group(arr, n, int(n_steps), ctypes.byref(st)), solvers[0]._h)
+    return {"steps_done": st.steps_done, "passes_done": st.passes_done, "res": list(st.res), "converged": st.converged}
 
 
 def nccl_unique_id() -> bytes:
