@@ -92,6 +92,7 @@ struct sts_ctx {
     uint8_t *ck = nullptr, *uk = nullptr, *vk = nullptr;
     uint32_t* kind32 = nullptr;            // packed ck | uk << 8 | vk << 16, (ny+1) x pitch
     std::vector<uint8_t> h_ck, h_uk, h_vk; // host copies of the local kind maps
+    std::vector<uint8_t> h_solid;          // global solid map (nx x ny), for set_field
     bool use_tile = false;                 // STS_KERNEL=tile: v1 2-D tile kernel
     int march_seg = 0, march_nseg = 0;
     unsigned long long* red = nullptr;     // [max_passes][9]
@@ -474,6 +475,7 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
     ctx->nx = nx; ctx->ny = ny; ctx->spacing = grid->spacing;
     ctx->gas = *gas; ctx->sch = *scheme;
     ctx->squares.assign(squares, squares + n_squares);
+    ctx->h_solid = solid;
     ctx->rank = rank; ctx->world = world;
     ctx->device = dist ? dist->device : 0;
     if (ctx->device < 0 || ctx->device >= ndev) { delete ctx; return fail(nullptr, STS_E_ARG, "bad device"); }
@@ -613,13 +615,12 @@ static sts_status pack_into_all(sts_ctx* ctx, int field, const double* gdev)
 // to a global-shape host copy before packing.
 static void impose_fixed_host(const sts_ctx* c, int field, double* g)
 {
+    // over the whole global array: a slab packs its (possibly wrapped) ghost
+    // columns from columns it does not own
     if (field == STS_U) {
         for (int j = 0; j < c->ny; j++)
             for (int i = 0; i <= c->nx; i++) {
-                int li = i - c->gi0 + OFF;
-                uint8_t k;
-                if (li >= 0 && li < c->pitch) k = c->h_uk[(size_t)j * c->pitch + li];
-                else continue;   // outside this rank: its owner imposes it
+                const uint8_t k = u_kind_g(c, i, j, c->h_solid);
                 if (k == FK_FIXED0) g[(size_t)j * (c->nx + 1) + i] = 0.0;
                 else if (k == FK_INLET) g[(size_t)j * (c->nx + 1) + i] = c->u_in;
             }
@@ -628,9 +629,7 @@ static void impose_fixed_host(const sts_ctx* c, int field, double* g)
     } else if (field == STS_V) {
         for (int j = 0; j <= c->ny; j++)
             for (int i = 0; i < c->nx; i++) {
-                int li = i - c->gi0 + OFF;
-                if (li < 0 || li >= c->pitch) continue;
-                uint8_t k = c->h_vk[(size_t)j * c->pitch + li];
+                const uint8_t k = v_kind_g(c, i, j, c->h_solid);
                 if (k == FK_FIXED0 || k == FK_WALL) g[(size_t)j * c->nx + i] = 0.0;
             }
     }

@@ -1,4 +1,4 @@
-// sts_march.cuh -- v2 loop-2 pass kernel: y-marching row sweep (sm_100a, fp64).
+// sts_march.cuh -- v3 loop-2 pass kernel: y-marching row sweep (sm_100a, fp64).
 //
 // The paper's single kernel marches along y inside a work-group with row
 // buffers for p, u-hat/d^u, v-hat/d^v in local memory (P:248-253, P:550,
@@ -97,12 +97,16 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem)
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+struct RingRow {                 // one old-iterate row (slot-major: one base address per row)
+    double U[RW], V[RW], P[RW], T[RW], R[RW], G[RW];
+    uint32_t KK[RW];
+};
+struct FluxRow {                 // face densities / fluxes of one row, (p/T)^{n-1} of that row
+    double RU[RW], FX[RW], RV[RW], FY[RW], R1[RW];
+};
 struct MarchSmem {
-    // ring of old-iterate rows
-    double U[RS][RW], V[RS][RW], P[RS][RW], T[RS][RW], R[RS][RW], G[RS][RW];
-    uint32_t KK[RS][RW];
-    // per-row face / link pieces (indexed by ring column)
-    double RU[2][RW], FX[2][RW], RV[2][RW], FY[2][RW], R1[2][RW];
+    RingRow ring[RS];
+    FluxRow fr[2];
     double XTW[RW], XTE[RW], XUW[RW], XUE[RW], FBX[RW], XVE[RW], XVF[RW], GC[RW];
     double UH[RW], DU[RW], PN[RW];
 };
@@ -115,45 +119,46 @@ __device__ __forceinline__ uint8_t vkind(uint32_t w) { return (uint8_t)((w >> 16
 // Issue the loads of ring row j (global columns I0-4 .. I0-4+RW).  Rows outside
 // [0, ny] and unstored columns are filled directly: kind WALLY / NONE, u = wall
 // velocity beyond the walls (BC spec 8), p = T = 1, v = 0.
-__device__ __forceinline__ void ring_issue(MarchSmem& s, const MarchParams& m, int I0, int j)
+__device__ __forceinline__ void ring_issue(MarchSmem& s, const MarchParams& m, int I0, int j, int sl)
 {
     const Params& k = m.k;
-    const int sl = slot(j);
+    RingRow& r = s.ring[sl];
+    const long long ro = (long long)j * k.pitch;
     for (int lc = threadIdx.x; lc < RW; lc += MX) {
-        const int gi = I0 - 4 + lc;
-        const bool col_ok = stored_col(k, gi);
+        const int li = I0 - 4 + lc - k.gi0 + OFF;        // stored local column
+        const bool col_ok = li >= 0 && li < k.pitch;
         if (j >= 0 && j < k.ny && col_ok) {
-            const long long id = gidx(k, gi, j);
-            cp_async8(&s.U[sl][lc], k.u_o + id);
-            cp_async8(&s.V[sl][lc], k.v_o + id);
-            cp_async8(&s.P[sl][lc], k.p_o + id);
-            cp_async8(&s.T[sl][lc], k.T_o + id);
-            cp_async4(&s.KK[sl][lc], m.kind + id);
+            const long long id = ro + li;
+            cp_async8(&r.U[lc], k.u_o + id);
+            cp_async8(&r.V[lc], k.v_o + id);
+            cp_async8(&r.P[lc], k.p_o + id);
+            cp_async8(&r.T[lc], k.T_o + id);
+            cp_async4(&r.KK[lc], m.kind + id);
         } else if (j == k.ny && col_ok) {          // top wall row: v = 0 (WALL), no cells
-            const long long id = gidx(k, gi, j);
-            s.U[sl][lc] = k.u_wt;
-            cp_async8(&s.V[sl][lc], k.v_o + id);
-            s.P[sl][lc] = 1.0;
-            s.T[sl][lc] = 1.0;
-            cp_async4(&s.KK[sl][lc], m.kind + id);
+            const long long id = ro + li;
+            r.U[lc] = k.u_wt;
+            cp_async8(&r.V[lc], k.v_o + id);
+            r.P[lc] = 1.0;
+            r.T[lc] = 1.0;
+            cp_async4(&r.KK[lc], m.kind + id);
         } else {
-            s.U[sl][lc] = j < 0 ? k.u_wb : (j >= k.ny ? k.u_wt : 0.0);
-            s.V[sl][lc] = 0.0;
-            s.P[sl][lc] = 1.0;
-            s.T[sl][lc] = 1.0;
-            s.KK[sl][lc] = (uint32_t)CK_WALLY | ((uint32_t)FK_NONE << 8) | ((uint32_t)FK_NONE << 16);
+            r.U[lc] = j < 0 ? k.u_wb : (j >= k.ny ? k.u_wt : 0.0);
+            r.V[lc] = 0.0;
+            r.P[lc] = 1.0;
+            r.T[lc] = 1.0;
+            r.KK[lc] = (uint32_t)CK_WALLY | ((uint32_t)FK_NONE << 8) | ((uint32_t)FK_NONE << 16);
         }
     }
     cp_commit();
 }
 // rho = p/T (Eq. pl5), Gamma = sqrt(T) (Eq. pl37) of ring row j
-__device__ __forceinline__ void ring_derive(MarchSmem& s, int j)
+__device__ __forceinline__ void ring_derive(MarchSmem& s, int sl)
 {
-    const int sl = slot(j);
+    RingRow& r = s.ring[sl];
     for (int lc = threadIdx.x; lc < RW; lc += MX) {
-        const double Tv = s.T[sl][lc];
-        s.R[sl][lc] = fdiv(s.P[sl][lc], Tv);
-        s.G[sl][lc] = fsqrt(Tv);
+        const double Tv = r.T[lc];
+        r.R[lc] = fdiv(r.P[lc], Tv);
+        r.G[lc] = fsqrt(Tv);
     }
 }
 
@@ -175,11 +180,12 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
     const double dt = k.dt, dx = k.dx, dy = k.dy;
 
     // ---- prologue: ring rows js-1 .. js+2 (synchronous), issue js+3
-    for (int j = js - 1; j <= js + 2; j++) ring_issue(s, m, I0, j);
+    for (int j = js - 1; j <= js + 2; j++) ring_issue(s, m, I0, j, slot(j));
     cp_wait_all();
     __syncthreads();
-    for (int j = js - 1; j <= js + 2; j++) ring_derive(s, j);
-    ring_issue(s, m, I0, js + 3);
+    for (int j = js - 1; j <= js + 2; j++) ring_derive(s, slot(j));
+    ring_issue(s, m, I0, js + 3, slot(js + 3));
+    int sj = slot(js);                                  // ring slot of row j (incremental)
 
     // ---- n-1 / plane register pipeline (loaded one row step ahead)
     auto ld = [&](const double* a, int j) -> double {
@@ -206,8 +212,16 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
     int badf = 0;
 
     for (int j = js; j < J1; j++) {
-        const int c0 = slot(j), cm = slot(j - 1), c1 = slot(j + 1), c2 = slot(j + 2), c3 = slot(j + 3);
-        const int cb = j & 1, nb = (j + 1) & 1;
+        const int sa = sj + 1 == RS ? 0 : sj + 1, sb = sa + 1 == RS ? 0 : sa + 1;
+        const int sc = sb + 1 == RS ? 0 : sb + 1, sd = sc + 1 == RS ? 0 : sc + 1;
+        const int sm = sj == 0 ? RS - 1 : sj - 1;
+        RingRow& Rm = s.ring[sm];
+        RingRow& R0 = s.ring[sj];
+        RingRow& Ra = s.ring[sa];
+        RingRow& Rb = s.ring[sb];
+        RingRow& Rc = s.ring[sc];
+        FluxRow& Fc = s.fr[j & 1];
+        FluxRow& Fn = s.fr[(j + 1) & 1];
         const bool out_row = j >= J0;
 
         // prefetch the next row's n-1 / plane values (consumed one step later)
@@ -218,56 +232,56 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
 
         cp_wait_all();
         __syncthreads();                                    // B0: ring row j+3 landed
-        ring_issue(s, m, I0, j + 4);
+        ring_issue(s, m, I0, j + 4, sd);
 
         // ================= stage A: row j+1 fluxes, link pieces =================
-        ring_derive(s, j + 3);
-        const uint32_t kw0 = s.KK[c0][lc], kw1 = s.KK[c1][lc];
+        ring_derive(s, sc);
+        const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
         // (p/T)^{n-1} of row j+1
-        s.R1[nb][lc] = fdiv(p1n, T1n == 0.0 ? 1.0 : T1n);
+        Fn.R1[lc] = fdiv(p1n, T1n == 0.0 ? 1.0 : T1n);
         // F^x, rho^u at u-face (i, j+1)  (Eqs. pl8, pl10, R1)
         double Fx1 = 0.0;
         {
             double ru = 0.0;
             const uint8_t uk = ukind(kw1);
             if (flux_face(uk)) {
-                const double w = s.U[c1][lc], r1 = s.R[c1][lc - 1], r2 = s.R[c1][lc];
+                const double w = Ra.U[lc], r1 = Ra.R[lc - 1], r2 = Ra.R[lc];
                 ru = w > 0.0 ? r1 : r2;
-                if (TVD && ckind(s.KK[c1][lc - 2]) == CK_FLUID && ckind(s.KK[c1][lc - 1]) == CK_FLUID &&
-                    ckind(kw1) == CK_FLUID && ckind(s.KK[c1][lc + 1]) == CK_FLUID)
-                    ru += psi_f(s.R[c1][lc - 2], r1, r2, s.R[c1][lc + 1], w) * (r2 - r1);
+                if (TVD && ckind(Ra.KK[lc - 2]) == CK_FLUID && ckind(Ra.KK[lc - 1]) == CK_FLUID &&
+                    ckind(kw1) == CK_FLUID && ckind(Ra.KK[lc + 1]) == CK_FLUID)
+                    ru += psi_f(Ra.R[lc - 2], r1, r2, Ra.R[lc + 1], w) * (r2 - r1);
                 Fx1 = ru * w * dy;
             }
-            s.RU[nb][lc] = ru;
-            s.FX[nb][lc] = Fx1;
+            Fn.RU[lc] = ru;
+            Fn.FX[lc] = Fx1;
         }
         // F^y, rho^v at v-face (i, j+1)  (Eqs. pl9, pl11, R1)
         double Fy1 = 0.0;
         {
             double rv = 0.0;
             if (vkind(kw1) == FK_ACTIVE) {
-                const double w = s.V[c1][lc], r1 = s.R[c0][lc], r2 = s.R[c1][lc];
+                const double w = Ra.V[lc], r1 = R0.R[lc], r2 = Ra.R[lc];
                 rv = w > 0.0 ? r1 : r2;
-                if (TVD && ckind(s.KK[cm][lc]) == CK_FLUID && ckind(kw0) == CK_FLUID && ckind(kw1) == CK_FLUID &&
-                    ckind(s.KK[c2][lc]) == CK_FLUID)
-                    rv += psi_f(s.R[cm][lc], r1, r2, s.R[c2][lc], w) * (r2 - r1);
+                if (TVD && ckind(Rm.KK[lc]) == CK_FLUID && ckind(kw0) == CK_FLUID && ckind(kw1) == CK_FLUID &&
+                    ckind(Rb.KK[lc]) == CK_FLUID)
+                    rv += psi_f(Rm.R[lc], r1, r2, Rb.R[lc], w) * (r2 - r1);
                 Fy1 = rv * w * dx;
             }
-            s.RV[nb][lc] = rv;
-            s.FY[nb][lc] = Fy1;
+            Fn.RV[lc] = rv;
+            Fn.FY[lc] = Fy1;
         }
         // T-eq x-face pieces at u-face (i, j): a^T_1 of cell i, a^T_2 of cell i-1 (Eqs. pl31-pl33)
         {
             double pw = 0.0, pe = 0.0;
-            const uint8_t kl = ckind(s.KK[c0][lc - 1]), kr = ckind(kw0);
+            const uint8_t kl = ckind(R0.KK[lc - 1]), kr = ckind(kw0);
             if (!wallish(kl) && !wallish(kr)) {
-                const double F = s.FX[cb][lc];
-                const double g1 = s.G[c0][lc - 1], g2 = s.G[c0][lc];
+                const double F = Fc.FX[lc];
+                const double g1 = R0.G[lc - 1], g2 = R0.G[lc];
                 const double D = m.CT1_dydx * (2.0 * g1 * g2 * rcp(g1 + g2));
                 double ps = 0.0;
-                if (IMPL && TVD && ckind(s.KK[c0][lc - 2]) == CK_FLUID && kl == CK_FLUID && kr == CK_FLUID &&
-                    ckind(s.KK[c0][lc + 1]) == CK_FLUID)
-                    ps = psi_f(s.T[c0][lc - 2], s.T[c0][lc - 1], s.T[c0][lc], s.T[c0][lc + 1], s.U[c0][lc]);
+                if (IMPL && TVD && ckind(R0.KK[lc - 2]) == CK_FLUID && kl == CK_FLUID && kr == CK_FLUID &&
+                    ckind(R0.KK[lc + 1]) == CK_FLUID)
+                    ps = psi_f(R0.T[lc - 2], R0.T[lc - 1], R0.T[lc], R0.T[lc + 1], R0.U[lc]);
                 pw = (IMPL ? max0(F) - F * ps : 0.0) + D;
                 pe = (IMPL ? max0(-F) - F * ps : 0.0) + D;
             }
@@ -280,12 +294,12 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
             const uint8_t kb = ckind(kw0), kt = ckind(kw1);
             if (!wallish(kb) && !wallish(kt)) {
                 const double F = Fy1;
-                const double g1 = s.G[c0][lc], g2 = s.G[c1][lc];
+                const double g1 = R0.G[lc], g2 = Ra.G[lc];
                 const double D = m.CT1_dxdy * (2.0 * g1 * g2 * rcp(g1 + g2));
                 double ps = 0.0;
-                if (IMPL && TVD && ckind(s.KK[cm][lc]) == CK_FLUID && kb == CK_FLUID && kt == CK_FLUID &&
-                    ckind(s.KK[c2][lc]) == CK_FLUID)
-                    ps = psi_f(s.T[cm][lc], s.T[c0][lc], s.T[c1][lc], s.T[c2][lc], s.V[c1][lc]);
+                if (IMPL && TVD && ckind(Rm.KK[lc]) == CK_FLUID && kb == CK_FLUID && kt == CK_FLUID &&
+                    ckind(Rb.KK[lc]) == CK_FLUID)
+                    ps = psi_f(Rm.T[lc], R0.T[lc], Ra.T[lc], Rb.T[lc], Ra.V[lc]);
                 ytN = (IMPL ? max0(-F) - F * ps : 0.0) + D;
                 ytSn = (IMPL ? max0(F) - F * ps : 0.0) + D;
             }
@@ -294,13 +308,13 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
         {
             double xe = 0.0, xw = 0.0, Fb = 0.0;
             if (ckind(kw0) == CK_FLUID) {
-                const double ub = 0.5 * (s.U[c0][lc] + s.U[c0][lc + 1]);
-                Fb = s.R[c0][lc] * ub * dy;
-                const double D = 4.0 / 3.0 * m.B_dydx * s.G[c0][lc];
+                const double ub = 0.5 * (R0.U[lc] + R0.U[lc + 1]);
+                Fb = R0.R[lc] * ub * dy;
+                const double D = 4.0 / 3.0 * m.B_dydx * R0.G[lc];
                 double ps = 0.0;
-                if (IMPL && TVD && ukind(s.KK[c0][lc - 1]) == FK_ACTIVE && ukind(kw0) == FK_ACTIVE &&
-                    ukind(s.KK[c0][lc + 1]) == FK_ACTIVE && ukind(s.KK[c0][lc + 2]) == FK_ACTIVE)
-                    ps = psi_f(s.U[c0][lc - 1], s.U[c0][lc], s.U[c0][lc + 1], s.U[c0][lc + 2], ub);
+                if (IMPL && TVD && ukind(R0.KK[lc - 1]) == FK_ACTIVE && ukind(kw0) == FK_ACTIVE &&
+                    ukind(R0.KK[lc + 1]) == FK_ACTIVE && ukind(R0.KK[lc + 2]) == FK_ACTIVE)
+                    ps = psi_f(R0.U[lc - 1], R0.U[lc], R0.U[lc + 1], R0.U[lc + 2], ub);
                 xe = (IMPL ? max0(-Fb) - Fb * ps : 0.0) + D;
                 xw = (IMPL ? max0(Fb) - Fb * ps : 0.0) + D;
             }
@@ -310,22 +324,22 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
         }
         // u-eq tangential psi at (u column i, y^f_{j+1}) (fluxes need the neighbour: stage C)
         double upsi1 = 0.0, upsi2 = 0.0;
-        if (IMPL && TVD && ukind(s.KK[cm][lc]) == FK_ACTIVE && ukind(kw0) == FK_ACTIVE &&
-            ukind(kw1) == FK_ACTIVE && ukind(s.KK[c2][lc]) == FK_ACTIVE) {
-            const double f1 = s.U[cm][lc], f2 = s.U[c0][lc], f3 = s.U[c1][lc], f4 = s.U[c2][lc];
-            upsi1 = psi_f(f1, f2, f3, f4, s.V[c1][lc]);
-            upsi2 = psi_f(f1, f2, f3, f4, s.V[c1][lc - 1]);
+        if (IMPL && TVD && ukind(Rm.KK[lc]) == FK_ACTIVE && ukind(kw0) == FK_ACTIVE &&
+            ukind(kw1) == FK_ACTIVE && ukind(Rb.KK[lc]) == FK_ACTIVE) {
+            const double f1 = Rm.U[lc], f2 = R0.U[lc], f3 = Ra.U[lc], f4 = Rb.U[lc];
+            upsi1 = psi_f(f1, f2, f3, f4, Ra.V[lc]);
+            upsi2 = psi_f(f1, f2, f3, f4, Ra.V[lc - 1]);
         }
         // v-eq normal piece of cell (i, j+1): a^v_4 of v-face (i, j+1), a^v_3 of v-face (i, j+2)
         double vcN = 0.0, vcSn = 0.0, FbN = 0.0;
         if (ckind(kw1) == CK_FLUID) {
-            const double vb = 0.5 * (s.V[c1][lc] + s.V[c2][lc]);
-            FbN = s.R[c1][lc] * vb * dx;
-            const double D = 4.0 / 3.0 * m.B_dxdy * s.G[c1][lc];
+            const double vb = 0.5 * (Ra.V[lc] + Rb.V[lc]);
+            FbN = Ra.R[lc] * vb * dx;
+            const double D = 4.0 / 3.0 * m.B_dxdy * Ra.G[lc];
             double ps = 0.0;
             if (IMPL && TVD && vkind(kw0) == FK_ACTIVE && vkind(kw1) == FK_ACTIVE &&
-                vkind(s.KK[c2][lc]) == FK_ACTIVE && vkind(s.KK[c3][lc]) == FK_ACTIVE)
-                ps = psi_f(s.V[c0][lc], s.V[c1][lc], s.V[c2][lc], s.V[c3][lc], vb);
+                vkind(Rb.KK[lc]) == FK_ACTIVE && vkind(Rc.KK[lc]) == FK_ACTIVE)
+                ps = psi_f(R0.V[lc], Ra.V[lc], Rb.V[lc], Rc.V[lc], vb);
             vcN = (IMPL ? max0(-FbN) - FbN * ps : 0.0) + D;
             vcSn = (IMPL ? max0(FbN) - FbN * ps : 0.0) + D;
         }
@@ -334,11 +348,11 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
         {
             double sum = 0.0;
             int n = 0;
-            const uint8_t a = ckind(s.KK[c0][lc - 1]), b = ckind(kw0), c = ckind(s.KK[c1][lc - 1]), d = ckind(kw1);
-            if (!wallish(a)) { sum += s.G[c0][lc - 1]; n++; }
-            if (!wallish(b)) { sum += s.G[c0][lc]; n++; }
-            if (!wallish(c)) { sum += s.G[c1][lc - 1]; n++; }
-            if (!wallish(d)) { sum += s.G[c1][lc]; n++; }
+            const uint8_t a = ckind(R0.KK[lc - 1]), b = ckind(kw0), c = ckind(Ra.KK[lc - 1]), d = ckind(kw1);
+            if (!wallish(a)) { sum += R0.G[lc - 1]; n++; }
+            if (!wallish(b)) { sum += R0.G[lc]; n++; }
+            if (!wallish(c)) { sum += Ra.G[lc - 1]; n++; }
+            if (!wallish(d)) { sum += Ra.G[lc]; n++; }
             gcN = n == 4 ? 0.25 * sum : (n > 0 ? sum / n : 0.0);
             s.GC[lc] = gcN;
         }
@@ -346,13 +360,13 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
         // a^v_2 of v-face (i-1, j+1)
         double xvW, FwSum;
         {
-            const double F1 = Fx1, F2 = s.FX[cb][lc];     // rows j+1 (upper half) and j (lower half)
+            const double F1 = Fx1, F2 = Fc.FX[lc];     // rows j+1 (upper half) and j (lower half)
             double p1 = 0.0, p2 = 0.0;
-            if (IMPL && TVD && vkind(s.KK[c1][lc - 2]) == FK_ACTIVE && vkind(s.KK[c1][lc - 1]) == FK_ACTIVE &&
-                vkind(kw1) == FK_ACTIVE && vkind(s.KK[c1][lc + 1]) == FK_ACTIVE) {
-                const double f1 = s.V[c1][lc - 2], f2 = s.V[c1][lc - 1], f3 = s.V[c1][lc], f4 = s.V[c1][lc + 1];
-                p1 = psi_f(f1, f2, f3, f4, s.U[c1][lc]);
-                p2 = psi_f(f1, f2, f3, f4, s.U[c0][lc]);
+            if (IMPL && TVD && vkind(Ra.KK[lc - 2]) == FK_ACTIVE && vkind(Ra.KK[lc - 1]) == FK_ACTIVE &&
+                vkind(kw1) == FK_ACTIVE && vkind(Ra.KK[lc + 1]) == FK_ACTIVE) {
+                const double f1 = Ra.V[lc - 2], f2 = Ra.V[lc - 1], f3 = Ra.V[lc], f4 = Ra.V[lc + 1];
+                p1 = psi_f(f1, f2, f3, f4, Ra.U[lc]);
+                p2 = psi_f(f1, f2, f3, f4, R0.U[lc]);
             }
             const double D = m.B_dydx * gcN;
             xvW = (IMPL ? 0.5 * (max0(F1) - F1 * p1 + max0(F2) - F2 * p2) : 0.0) + D;
@@ -363,37 +377,37 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
         __syncthreads();                                    // B1
 
         // ================= stage C: T_{i,j}, u-hat_{i,j}, v-hat_{i,j+1} =================
-        const double rP = s.R[c0][lc], gP = s.G[c0][lc];
+        const double rP = R0.R[lc], gP = R0.G[lc];
         double TN = 0.0;
         if (ckind(kw0) == CK_FLUID) {
             const double tau = 2.1904 * k.Kn * rcp(rP);   // Eq. pl39
             double a1, a2, a3, a4, T1, T2, T3, T4, FW = 0.0, FE = 0.0, FSl = 0.0, FNl = 0.0;
-            uint8_t kn = ckind(s.KK[c0][lc - 1]);
+            uint8_t kn = ckind(R0.KK[lc - 1]);
             if (wallish(kn)) { a1 = k.CT1 * gP * dy * rcp(0.5 * dx + tau); T1 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { a1 = s.XTW[lc]; FW = s.FX[cb][lc]; T1 = s.T[c0][lc - 1]; }
-            kn = ckind(s.KK[c0][lc + 1]);
+            else { a1 = s.XTW[lc]; FW = Fc.FX[lc]; T1 = R0.T[lc - 1]; }
+            kn = ckind(R0.KK[lc + 1]);
             if (wallish(kn)) { a2 = k.CT1 * gP * dy * rcp(0.5 * dx + tau); T2 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { a2 = s.XTE[lc + 1]; FE = s.FX[cb][lc + 1]; T2 = s.T[c0][lc + 1]; }
-            kn = ckind(s.KK[cm][lc]);
+            else { a2 = s.XTE[lc + 1]; FE = Fc.FX[lc + 1]; T2 = R0.T[lc + 1]; }
+            kn = ckind(Rm.KK[lc]);
             if (wallish(kn)) { a3 = k.CT1 * gP * dx * rcp(0.5 * dy + tau); T3 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { a3 = ytS; FSl = FS; T3 = s.T[cm][lc]; }
+            else { a3 = ytS; FSl = FS; T3 = Rm.T[lc]; }
             kn = ckind(kw1);
             if (wallish(kn)) { a4 = k.CT1 * gP * dx * rcp(0.5 * dy + tau); T4 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { a4 = ytN; FNl = Fy1; T4 = s.T[c1][lc]; }
+            else { a4 = ytN; FNl = Fy1; T4 = Ra.T[lc]; }
             const double a0 = IMPL ? dt * (a1 + a2 + a3 + a4 + FE - FW + FNl - FSl) + rP * m.dV
                                    : dt * (a1 + a2 + a3 + a4) + rP * m.dV;
             // S^T_c, Eq. pl29 (R4 bilinear = 4-point mean; R9 sign)
-            const double dudx = (s.U[c0][lc + 1] - s.U[c0][lc]) * m.inv_dx;
-            const double dvdy = (s.V[c1][lc] - s.V[c0][lc]) * m.inv_dy;
-            const double vE = 0.25 * (s.V[c0][lc] + s.V[c0][lc + 1] + s.V[c1][lc] + s.V[c1][lc + 1]);
-            const double vW = 0.25 * (s.V[c0][lc - 1] + s.V[c0][lc] + s.V[c1][lc - 1] + s.V[c1][lc]);
-            const double uN = 0.25 * (s.U[c0][lc] + s.U[c0][lc + 1] + s.U[c1][lc] + s.U[c1][lc + 1]);
-            const double uS = 0.25 * (s.U[cm][lc] + s.U[cm][lc + 1] + s.U[c0][lc] + s.U[c0][lc + 1]);
+            const double dudx = (R0.U[lc + 1] - R0.U[lc]) * m.inv_dx;
+            const double dvdy = (Ra.V[lc] - R0.V[lc]) * m.inv_dy;
+            const double vE = 0.25 * (R0.V[lc] + R0.V[lc + 1] + Ra.V[lc] + Ra.V[lc + 1]);
+            const double vW = 0.25 * (R0.V[lc - 1] + R0.V[lc] + Ra.V[lc - 1] + Ra.V[lc]);
+            const double uN = 0.25 * (R0.U[lc] + R0.U[lc + 1] + Ra.U[lc] + Ra.U[lc + 1]);
+            const double uS = 0.25 * (Rm.U[lc] + Rm.U[lc + 1] + R0.U[lc] + R0.U[lc + 1]);
             const double shear = (vE - vW) * m.inv_dx + (uN - uS) * m.inv_dy;
             const double div = dudx + dvdy;
             const double Sc = (k.CT2 * gP * (2.0 * (dudx * dudx + dvdy * dvdy) + shear * shear - 2.0 / 3.0 * div * div)
-                               + k.pw_sign * k.CT3 * s.P[c0][lc] * div) * m.dV;
-            const double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + Sc + Tec) + s.R1[cb][lc] * T1c * m.dV;
+                               + k.pw_sign * k.CT3 * R0.P[lc] * div) * m.dV;
+            const double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + Sc + Tec) + Fc.R1[lc] * T1c * m.dV;
             TN = rhs * rcp(a0);
         }
         // u-eq at u-face (i, j)
@@ -401,36 +415,36 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
         double utSn, FsSumN;
         {
             // N tangential link pieces at y^f_{j+1} (both sides; the S side is carried)
-            const double F1 = Fy1, F2 = s.FY[nb][lc - 1];
+            const double F1 = Fy1, F2 = Fn.FY[lc - 1];
             const double D = m.B_dxdy * gcN;
             const double a4p = (IMPL ? 0.5 * (max0(-F1) - F1 * upsi1 + max0(-F2) - F2 * upsi2) : 0.0) + D;
             utSn = (IMPL ? 0.5 * (max0(F1) - F1 * upsi1 + max0(F2) - F2 * upsi2) : 0.0) + D;
             FsSumN = F1 + F2;
             if (ukind(kw0) == FK_ACTIVE) {
-                const double rL = s.R[c0][lc - 1], rR = rP, gL = s.G[c0][lc - 1], gR = gP;
+                const double rL = R0.R[lc - 1], rR = rP, gL = R0.G[lc - 1], gR = gP;
                 const double gadj = 0.5 * (gL + gR);
                 const double zeta = 1.1466 * k.Kn * rcp(0.5 * (rL + rR));     // Eq. pl38
                 const double a1 = s.XUW[lc - 1], a2 = s.XUE[lc];
                 const double FbW = s.FBX[lc - 1], FbE = s.FBX[lc];
                 double a3, a4, uS, uN, FsS = 0.0, FnS = 0.0;
-                const uint8_t kl = ckind(s.KK[cm][lc - 1]), kr = ckind(s.KK[cm][lc]);
+                const uint8_t kl = ckind(Rm.KK[lc - 1]), kr = ckind(Rm.KK[lc]);
                 if (kl == CK_WALLY || (kl == CK_SOLID && kr == CK_SOLID)) {
                     a3 = k.B * gadj * dx * rcp(0.5 * dy + zeta); uS = kl == CK_WALLY ? k.u_wb : 0.0;
-                } else { a3 = utS; FsS = FsSum; uS = s.U[cm][lc]; }
-                const uint8_t ml = ckind(s.KK[c1][lc - 1]), mr = ckind(kw1);
+                } else { a3 = utS; FsS = FsSum; uS = Rm.U[lc]; }
+                const uint8_t ml = ckind(Ra.KK[lc - 1]), mr = ckind(kw1);
                 if (ml == CK_WALLY || (ml == CK_SOLID && mr == CK_SOLID)) {
                     a4 = k.B * gadj * dx * rcp(0.5 * dy + zeta); uN = ml == CK_WALLY ? k.u_wt : 0.0;
-                } else { a4 = a4p; FnS = FsSumN; uN = s.U[c1][lc]; }
+                } else { a4 = a4p; FnS = FsSumN; uN = Ra.U[lc]; }
                 const double tterm = (rR + rL) * m.c_t;
                 const double a0 = IMPL ? a1 + a2 + a3 + a4 + FbE - FbW + 0.5 * (FnS - FsS) + tterm
                                        : a1 + a2 + a3 + a4 + tterm;
-                const double b = (s.R1[cb][lc] + s.R1[cb][lc - 1]) * m.c_t * u1c
-                               + k.B * (gcN * (s.V[c1][lc] - s.V[c1][lc - 1]) - gcP * (s.V[c0][lc] - s.V[c0][lc - 1])
-                                        - 2.0 / 3.0 * gR * (s.V[c1][lc] - s.V[c0][lc])
-                                        + 2.0 / 3.0 * gL * (s.V[c1][lc - 1] - s.V[c0][lc - 1]))
+                const double b = (Fc.R1[lc] + Fc.R1[lc - 1]) * m.c_t * u1c
+                               + k.B * (gcN * (Ra.V[lc] - Ra.V[lc - 1]) - gcP * (R0.V[lc] - R0.V[lc - 1])
+                                        - 2.0 / 3.0 * gR * (Ra.V[lc] - R0.V[lc])
+                                        + 2.0 / 3.0 * gL * (Ra.V[lc - 1] - R0.V[lc - 1]))
                                + k.g_x * (rR + rL) * m.half_dV;
                 const double r = rcp(a0);
-                uhat = (a1 * s.U[c0][lc - 1] + a2 * s.U[c0][lc + 1] + a3 * uS + a4 * uN + b + uec) * r;
+                uhat = (a1 * R0.U[lc - 1] + a2 * R0.U[lc + 1] + a3 * uS + a4 * uN + b + uec) * r;
                 du = m.A_dy * r;
             }
             s.UH[lc] = uhat;
@@ -439,54 +453,54 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
         // v-eq at v-face (i, j+1)
         double vhatN = 0.0, dvN = 0.0;
         if (vkind(kw1) == FK_ACTIVE) {
-            const double rB = rP, rT = s.R[c1][lc], gB = gP, gT = s.G[c1][lc];
+            const double rB = rP, rT = Ra.R[lc], gB = gP, gT = Ra.G[lc];
             const double gadj = 0.5 * (gB + gT);
             const double zeta = 1.1466 * k.Kn * rcp(0.5 * (rB + rT));
             double a1, a2, vW, vE, FwS = 0.0, FeS = 0.0;
-            if (ckind(s.KK[c0][lc - 1]) == CK_SOLID && ckind(s.KK[c1][lc - 1]) == CK_SOLID) {
+            if (ckind(R0.KK[lc - 1]) == CK_SOLID && ckind(Ra.KK[lc - 1]) == CK_SOLID) {
                 a1 = k.B * gadj * dy * rcp(0.5 * dx + zeta); vW = 0.0;
-            } else { a1 = xvW; FwS = FwSum; vW = s.V[c1][lc - 1]; }
-            if (ckind(s.KK[c0][lc + 1]) == CK_SOLID && ckind(s.KK[c1][lc + 1]) == CK_SOLID) {
+            } else { a1 = xvW; FwS = FwSum; vW = Ra.V[lc - 1]; }
+            if (ckind(R0.KK[lc + 1]) == CK_SOLID && ckind(Ra.KK[lc + 1]) == CK_SOLID) {
                 a2 = k.B * gadj * dy * rcp(0.5 * dx + zeta); vE = 0.0;
-            } else { a2 = s.XVE[lc + 1]; FeS = s.XVF[lc + 1]; vE = s.V[c1][lc + 1]; }
+            } else { a2 = s.XVE[lc + 1]; FeS = s.XVF[lc + 1]; vE = Ra.V[lc + 1]; }
             const double a3 = vcS, a4 = vcN;
             const double tterm = (rT + rB) * m.c_t;
             const double a0 = IMPL ? a1 + a2 + a3 + a4 + 0.5 * (FeS - FwS) + FbN - FbS + tterm
                                    : a1 + a2 + a3 + a4 + tterm;
-            const double b = (s.R1[nb][lc] + s.R1[cb][lc]) * m.c_t * v1n
-                           + k.B * (s.GC[lc + 1] * (s.U[c1][lc + 1] - s.U[c0][lc + 1]) - gcN * (s.U[c1][lc] - s.U[c0][lc])
-                                    - 2.0 / 3.0 * gT * (s.U[c1][lc + 1] - s.U[c1][lc])
-                                    + 2.0 / 3.0 * gB * (s.U[c0][lc + 1] - s.U[c0][lc]))
+            const double b = (Fn.R1[lc] + Fc.R1[lc]) * m.c_t * v1n
+                           + k.B * (s.GC[lc + 1] * (Ra.U[lc + 1] - R0.U[lc + 1]) - gcN * (Ra.U[lc] - R0.U[lc])
+                                    - 2.0 / 3.0 * gT * (Ra.U[lc + 1] - Ra.U[lc])
+                                    + 2.0 / 3.0 * gB * (R0.U[lc + 1] - R0.U[lc]))
                            + k.g_y * (rT + rB) * m.half_dV;
             const double r = rcp(a0);
-            vhatN = (a1 * vW + a2 * vE + a3 * s.V[c0][lc] + a4 * s.V[c2][lc] + b + ven) * r;
+            vhatN = (a1 * vW + a2 * vE + a3 * R0.V[lc] + a4 * Rb.V[lc] + b + ven) * r;
             dvN = m.A_dx * r;
         }
         __syncthreads();                                    // B2
 
         // ================= stage D: p_{i,j} (Eqs. pl23-pl24) =================
-        double pn = s.P[c0][lc];
+        double pn = R0.P[lc];
         if (ckind(kw0) == CK_FLUID) {
             double apW = 0.0, apE = 0.0, apS = 0.0, apN = 0.0, bpW = 0.0, bpE = 0.0, bpS = 0.0, bpN = 0.0, sum = 0.0;
-            const uint8_t kwf = ukind(kw0), kef = ukind(s.KK[c0][lc + 1]);
+            const uint8_t kwf = ukind(kw0), kef = ukind(R0.KK[lc + 1]);
             if (kwf == FK_ACTIVE) {
-                const double r = s.RU[cb][lc];
-                apW = r * du * dy; bpW = r * uhat * dy; sum += apW * s.P[c0][lc - 1];
-            } else if (kwf == FK_INLET) bpW = s.RU[cb][lc] * k.u_in * dy;
+                const double r = Fc.RU[lc];
+                apW = r * du * dy; bpW = r * uhat * dy; sum += apW * R0.P[lc - 1];
+            } else if (kwf == FK_INLET) bpW = Fc.RU[lc] * k.u_in * dy;
             if (kef == FK_ACTIVE) {
-                const double r = s.RU[cb][lc + 1];
-                apE = r * s.DU[lc + 1] * dy; bpE = r * s.UH[lc + 1] * dy; sum += apE * s.P[c0][lc + 1];
-            } else if (kef == FK_OUTLET) bpE = s.RU[cb][lc + 1] * s.U[c0][lc] * dy;
+                const double r = Fc.RU[lc + 1];
+                apE = r * s.DU[lc + 1] * dy; bpE = r * s.UH[lc + 1] * dy; sum += apE * R0.P[lc + 1];
+            } else if (kef == FK_OUTLET) bpE = Fc.RU[lc + 1] * R0.U[lc] * dy;
             if (vkind(kw0) == FK_ACTIVE) {
-                const double r = s.RV[cb][lc];
-                apS = r * dvP * dx; bpS = r * vhatP * dx; sum += apS * s.P[cm][lc];
+                const double r = Fc.RV[lc];
+                apS = r * dvP * dx; bpS = r * vhatP * dx; sum += apS * Rm.P[lc];
             }
             if (vkind(kw1) == FK_ACTIVE) {
-                const double r = s.RV[nb][lc];
-                apN = r * dvN * dx; bpN = r * vhatN * dx; sum += apN * s.P[c1][lc];
+                const double r = Fn.RV[lc];
+                apN = r * dvN * dx; bpN = r * vhatN * dx; sum += apN * Ra.P[lc];
             }
             const double a0 = m.dV * rcp(TN) + (apW + apE + apS + apN) * dt;
-            const double bp = s.R1[cb][lc] * m.dV - (bpE - bpW + bpN - bpS) * dt;
+            const double bp = Fc.R1[lc] * m.dV - (bpE - bpW + bpN - bpS) * dt;
             pn = (sum * dt + bp) * rcp(a0);
         }
         s.PN[lc] = pn;
@@ -498,8 +512,8 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
             if (ckind(kw0) == CK_FLUID) {
                 k.T_w[id] = TN;
                 k.p_w[id] = pn;
-                r_dT = nmax(r_dT, fabs(TN - s.T[c0][lc]));
-                r_dp = nmax(r_dp, fabs(pn - s.P[c0][lc]));
+                r_dT = nmax(r_dT, fabs(TN - R0.T[lc]));
+                r_dp = nmax(r_dp, fabs(pn - R0.P[lc]));
                 r_T = nmax(r_T, fabs(TN));
                 r_p = nmax(r_p, fabs(pn));
                 if (!(TN > 0.0) || !(pn > 0.0) || !isfinite(TN) || !isfinite(pn)) {
@@ -511,23 +525,23 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
             double un;
             if (ku == FK_ACTIVE) {
                 un = uhat - du * (pn - s.PN[lc - 1]);
-                r_du = nmax(r_du, fabs(un - s.U[c0][lc]));
+                r_du = nmax(r_du, fabs(un - R0.U[lc]));
                 r_vel = nmax(r_vel, fabs(un));
             } else if (ku == FK_INLET) un = k.u_in;
             else un = 0.0;
             k.u_w[id] = un;
-            if (gi == k.nx - 1 && k.xbc == 0) k.u_w[id + 1] = s.U[c0][lc];   // outlet face (BC spec 3)
+            if (gi == k.nx - 1 && k.xbc == 0) k.u_w[id + 1] = R0.U[lc];   // outlet face (BC spec 3)
             double vn = 0.0;
             if (vkind(kw0) == FK_ACTIVE) {
                 vn = vhatP - dvP * (pn - pnP);
-                r_dv = nmax(r_dv, fabs(vn - s.V[c0][lc]));
+                r_dv = nmax(r_dv, fabs(vn - R0.V[lc]));
                 r_vel = nmax(r_vel, fabs(vn));
             }
             k.v_w[id] = vn;
             if (k.xbc == 0) {
                 if (gi == k.nx - 1) {
-                    const double pv = ckind(kw0) == CK_FLUID ? pn : s.P[c0][lc];
-                    const double Tv = ckind(kw0) == CK_FLUID ? TN : s.T[c0][lc];
+                    const double pv = ckind(kw0) == CK_FLUID ? pn : R0.P[lc];
+                    const double Tv = ckind(kw0) == CK_FLUID ? TN : R0.T[lc];
                     for (int g = 1; g <= OFF - 1; g++) { k.p_w[id + g] = pv; k.T_w[id + g] = Tv; k.v_w[id + g] = vn; }
                 }
             } else if (k.mirror) {
@@ -550,6 +564,7 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
         pnP = pn; gcP = gcN;
         p1n = p1nn; T1c = T1n; T1n = T1nn; u1c = u1n; v1n = v1nn;
         if (!IMPL) { Tec = Ten; uec = uen; ven = vem; }
+        sj = sa;
     }
     cp_wait_all();
     double vals[7] = {r_du, r_dv, r_dp, r_dT, r_vel, r_p, r_T};
