@@ -94,7 +94,8 @@ struct sts_ctx {
     std::vector<uint8_t> h_ck, h_uk, h_vk; // host copies of the local kind maps
     std::vector<uint8_t> h_solid;          // global solid map (nx x ny), for set_field
     bool use_tile = false;                 // STS_KERNEL=tile: v1 2-D tile kernel
-    int march_seg = 0, march_nseg = 0;
+    int march_seg = 0, march_nseg = 0, march_nstrips = 0;
+    int* cta_order = nullptr;              // launch order of the march CTAs (longest first)
     unsigned long long* red = nullptr;     // [max_passes][9]
     unsigned long long* h_red = nullptr;   // pinned, 9 entries
     double* stage = nullptr;               // device staging (global-shape field)
@@ -282,6 +283,8 @@ static MarchParams make_march(const sts_ctx* c, const Params& k)
     m.k = k;
     m.kind = c->kind32;
     m.seg = c->march_seg;
+    m.nstrips = c->march_nstrips;
+    m.order = c->cta_order;
     const double dx = c->spacing, dy = c->spacing, dt = c->sch.dt;
     m.inv_dx = 1.0 / dx; m.inv_dy = 1.0 / dy;
     m.CT1_dydx = c->CT1 * dy / dx; m.CT1_dxdy = c->CT1 * dx / dy;
@@ -291,9 +294,16 @@ static MarchParams make_march(const sts_ctx* c, const Params& k)
     return m;
 }
 
-// Segment height of the y-march: maximise (useful rows / (rows + warm-up)) x
-// (CTAs / (waves x resident CTAs on 148 SMs)).
-static void choose_segments(sts_ctx* c)
+// Segment height and CTA order of the y-march.  Cost model per row step of a
+// CTA (it advances at the pace of its slowest warp, barriers every stage): a
+// warp whose 32 points are all regular costs 1, an all-general warp 1.35, a
+// mixed warp 2.35 (both instances).  For each candidate segment count the
+// CTAs (+4 warm-up rows each) are list-scheduled longest-first onto the
+// resident slots (148 SMs x CTAs/SM from the occupancy API); the count with
+// the smallest makespan wins, and the same longest-first order is the launch
+// order (blockIdx.x -> CTA), so the boundary CTAs (inlet, squares, walls)
+// start in the first wave.
+static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
 {
     int dev_sms = 148, per_sm = 3;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -301,23 +311,70 @@ static void choose_segments(sts_ctx* c)
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)march_table(1, 1), MX, sizeof(MarchSmem)) == cudaSuccess && nb > 0)
         per_sm = nb;
     const int strips = (c->nloc + MW - 1) / MW;
-    const long long slots = (long long)dev_sms * per_sm;
-    double best = -1;
-    int best_n = 1;
-    for (int n = 1; n <= std::max(1, c->ny / 16); n++) {
-        int seg = (c->ny + n - 1) / n;
-        long long ctas = (long long)strips * n;
-        long long waves = (ctas + slots - 1) / slots;
-        double eff = (double)ctas / (double)(waves * slots) * (double)seg / (double)(seg + WARM);
-        if (eff > best + 1e-9) { best = eff; best_n = n; }
+    const int slots = dev_sms * per_sm;
+    const int ny = c->ny;
+    // row cost of every (strip, row), prefix-summed over rows
+    std::vector<double> pre((size_t)strips * (ny + 1), 0.0);
+    for (int st = 0; st < strips; st++) {
+        const int I0 = c->gi0 + st * MW;
+        for (int j = 0; j < ny; j++) {
+            double rc = 1.0;
+            for (int w = 0; w < MX / 32; w++) {
+                int nreg = 0;
+                for (int l = 0; l < 32; l++) {
+                    const int li = I0 - 2 + 32 * w + l - c->gi0 + OFF;
+                    if (li >= 0 && li < c->pitch && (packed[(size_t)j * c->pitch + li] & REG_BIT)) nreg++;
+                }
+                const double wc = nreg == 32 ? 1.0 : (nreg == 0 ? 1.35 : 2.35);
+                rc = std::max(rc, wc);
+            }
+            pre[(size_t)st * (ny + 1) + j + 1] = pre[(size_t)st * (ny + 1) + j] + rc;
+        }
     }
-    c->march_nseg = best_n;
-    c->march_seg = (c->ny + best_n - 1) / best_n;
-    if (const char* sv = getenv("STS_SEG")) {         // test hook: force short segments
-        int v = atoi(sv);
-        if (v > 0) c->march_seg = v;
+    auto seg_cost = [&](int st, int J0, int J1) {
+        const double* p = &pre[(size_t)st * (ny + 1)];
+        return p[J1] - p[J0] + WARM * (J0 > 0 ? (p[J0] - p[J0 - 1]) : 1.0);
+    };
+    int forced = 0;
+    if (const char* sv = getenv("STS_SEG")) forced = std::max(0, atoi(sv));   // test hook
+    double best = 1e300;
+    int best_seg = ny;
+    std::vector<std::pair<double, int>> ctas;
+    auto schedule = [&](int seg, bool keep) -> double {
+        const int nseg = (ny + seg - 1) / seg;
+        ctas.clear();
+        for (int g = 0; g < nseg; g++)
+            for (int st = 0; st < strips; st++)
+                ctas.push_back({seg_cost(st, g * seg, std::min(ny, (g + 1) * seg)), st + strips * g});
+        std::stable_sort(ctas.begin(), ctas.end(), [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
+            return a.first > b.first;
+        });
+        std::vector<double> load(std::min<size_t>(slots, ctas.size()), 0.0);
+        for (auto& q : ctas) {
+            auto it = std::min_element(load.begin(), load.end());
+            *it += q.first;
+        }
+        (void)keep;
+        return *std::max_element(load.begin(), load.end());
+    };
+    if (forced > 0) {
+        best_seg = forced;
+    } else {
+        for (int seg = std::max(1, std::min(ny, 32)); seg <= ny; seg += (seg < 256 ? 8 : 32)) {
+            const double ms = schedule(seg, false);
+            if (ms < best * (1.0 - 1e-3)) { best = ms; best_seg = seg; }
+        }
     }
-    c->march_nseg = (c->ny + c->march_seg - 1) / c->march_seg;
+    schedule(best_seg, true);
+    c->march_seg = best_seg;
+    c->march_nseg = (ny + best_seg - 1) / best_seg;
+    c->march_nstrips = strips;
+    std::vector<int> order(ctas.size());
+    for (size_t q = 0; q < ctas.size(); q++) order[q] = ctas[q].second;
+    cudaFree(c->cta_order);
+    c->cta_order = nullptr;
+    cudaMalloc(&c->cta_order, order.size() * sizeof(int));
+    cudaMemcpy(c->cta_order, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice);
 }
 
 // ------------------------------------------------------------- profiling
@@ -545,14 +602,33 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
             uint32_t ukv = e < nce ? ctx->h_uk[e] : (uint32_t)FK_NONE;
             packed[e] = ckv | (ukv << 8) | ((uint32_t)ctx->h_vk[e] << 16);
         }
+        // "regular" bit (Fig. 9 split): every cell of the +-3 window is
+        // FLUID (separable 7-wide minimum of the fluid mask, x then y)
+        const int R = 3, W = ctx->pitch + 2 * R, H = ny + 2 * R;
+        std::vector<uint8_t> fl((size_t)W * H), hx((size_t)ctx->pitch * H);
+        for (int jj = 0; jj < H; jj++)
+            for (int c = 0; c < W; c++)
+                fl[(size_t)jj * W + c] = cell_kind_g(ctx, ctx->gi0 - OFF - R + c, jj - R, solid) == CK_FLUID;
+        for (int jj = 0; jj < H; jj++)
+            for (int li = 0; li < ctx->pitch; li++) {
+                uint8_t a = 1;
+                for (int d = 0; d <= 2 * R; d++) a &= fl[(size_t)jj * W + li + d];
+                hx[(size_t)jj * ctx->pitch + li] = a;
+            }
+        for (int j = 0; j < ny; j++)
+            for (int li = 0; li < ctx->pitch; li++) {
+                uint8_t a = 1;
+                for (int d = 0; d <= 2 * R; d++) a &= hx[(size_t)(j + d) * ctx->pitch + li];
+                if (a) packed[(size_t)j * ctx->pitch + li] |= REG_BIT;
+            }
         if (cudaMalloc(&ctx->kind32, nve * sizeof(uint32_t)) != cudaSuccess) { sts_destroy(ctx); return fail(nullptr, STS_E_OOM, "device allocation failed"); }
         cudaMemcpy(ctx->kind32, packed.data(), nve * sizeof(uint32_t), cudaMemcpyHostToDevice);
+        choose_segments(ctx, packed);
     }
     {
         const char* kv = getenv("STS_KERNEL");
         ctx->use_tile = kv && std::string(kv) == "tile";
     }
-    choose_segments(ctx);
     if (world > 1 && !dist->nccl_id) {
         ctx->local_group = true;            // slabs of one process, driven by sts_advance_group
     } else if (world > 1) {
@@ -575,7 +651,7 @@ extern "C" void sts_destroy(sts_ctx* ctx)
     cudaDeviceSynchronize();
     for (int k = 0; k < 3; k++) { cudaFree(ctx->snap[k].u); cudaFree(ctx->snap[k].v); cudaFree(ctx->snap[k].p); cudaFree(ctx->snap[k].T); }
     cudaFree(ctx->ue); cudaFree(ctx->ve); cudaFree(ctx->Te); cudaFree(ctx->stage); cudaFree(ctx->halo);
-    cudaFree(ctx->ck); cudaFree(ctx->uk); cudaFree(ctx->vk); cudaFree(ctx->kind32); cudaFree(ctx->red);
+    cudaFree(ctx->ck); cudaFree(ctx->uk); cudaFree(ctx->vk); cudaFree(ctx->kind32); cudaFree(ctx->cta_order); cudaFree(ctx->red);
     if (ctx->h_red) cudaFreeHost(ctx->h_red);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
@@ -897,7 +973,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                     const dim3 grid((c->nloc + TX - 1) / TX, (c->ny + TY - 1) / TY);
                     pass<<<grid, NT, smem, st>>>(k);
                 } else {
-                    const dim3 mgrid((c->nloc + MW - 1) / MW, c->march_nseg);
+                    const dim3 mgrid(c->march_nstrips * c->march_nseg);
                     march<<<mgrid, MX, sizeof(MarchSmem), st>>>(make_march(c, k));
                 }
                 prof_end(c);

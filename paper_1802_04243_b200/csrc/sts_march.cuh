@@ -1,4 +1,4 @@
-// sts_march.cuh -- v3 loop-2 pass kernel: y-marching row sweep (sm_100a, fp64).
+// sts_march.cuh -- v4 loop-2 pass kernel: y-marching row sweep (sm_100a, fp64).
 //
 // The paper's single kernel marches along y inside a work-group with row
 // buffers for p, u-hat/d^u, v-hat/d^v in local memory (P:248-253, P:550,
@@ -18,6 +18,12 @@
 //    stage C (T_{i,j}, u-hat_{i,j}, v-hat_{i,j+1}: Eqs. pl29_1-pl29_5), stage D
 //    (p_{i,j}, Eq. pl29_6), stage E (u_{i,j}, v_{i,j}, Eqs. pl29_7-pl29_8,
 //    writes, residual maxima) -- the paper's dependency order;
+//  - the paper separates fluid control volumes from wall control volumes
+//    (Fig. 9): here every stage has a "regular" instance (REG =
+//    true: the +-3 window of the point is all fluid, so no kind test, wall
+//    link or TVD-validity test is compiled in) and a general instance; the
+//    choice is a per-cell bit precomputed on the host, so it is a function of
+//    the cell alone (decomposition-invariant);
 //  - divisions become MUFU reciprocals + Newton steps; the mesh constants
 //    (dy/dx, dx dy/(2 dt), ...) are precomputed on the host.
 // A segment starts 4 rows early (warm-up) so that every carried quantity is
@@ -33,11 +39,14 @@ constexpr int MW = MX - 3;       // owned columns per strip
 constexpr int RW = MX + 8;       // ring row width (global columns I0-4 .. I0-4+RW)
 constexpr int RS = 6;            // ring slots
 constexpr int WARM = 4;          // warm-up rows per segment
+constexpr uint32_t REG_BIT = 1u << 24;   // kind-word bit: the +-3 window is all fluid
 
 struct MarchParams {
     Params k;                    // v1 parameter block (pointers, constants)
-    const uint32_t* kind;        // packed kinds: ck | uk << 8 | vk << 16, (ny+1) x pitch
+    const uint32_t* kind;        // packed kinds: ck | uk << 8 | vk << 16 | regular << 24, (ny+1) x pitch
     int seg;                     // rows per segment
+    int nstrips;                 // strips per row of CTAs
+    const int* order;            // CTA schedule (longest first); blockIdx.x -> strip + nstrips * segment
     double inv_dx, inv_dy, CT1_dydx, CT1_dxdy, B_dydx, B_dxdy, c_t, dV, A_dy, A_dx, half_dV;
 };
 
@@ -116,6 +125,13 @@ __device__ __forceinline__ uint8_t ckind(uint32_t w) { return (uint8_t)(w & 0xff
 __device__ __forceinline__ uint8_t ukind(uint32_t w) { return (uint8_t)((w >> 8) & 0xff); }
 __device__ __forceinline__ uint8_t vkind(uint32_t w) { return (uint8_t)((w >> 16) & 0xff); }
 
+// kind predicates; with REG every one folds to its regular-point value
+template <bool REG> __device__ __forceinline__ bool cF(uint32_t w) { return REG || ckind(w) == CK_FLUID; }
+template <bool REG> __device__ __forceinline__ bool cW(uint32_t w) { return !REG && wallish(ckind(w)); }
+template <bool REG> __device__ __forceinline__ bool uA(uint32_t w) { return REG || ukind(w) == FK_ACTIVE; }
+template <bool REG> __device__ __forceinline__ bool uFl(uint32_t w) { return REG || flux_face(ukind(w)); }
+template <bool REG> __device__ __forceinline__ bool vA(uint32_t w) { return REG || vkind(w) == FK_ACTIVE; }
+
 // Issue the loads of ring row j (global columns I0-4 .. I0-4+RW).  Rows outside
 // [0, ny] and unstored columns are filled directly: kind WALLY / NONE, u = wall
 // velocity beyond the walls (BC spec 8), p = T = 1, v = 0.
@@ -162,6 +178,408 @@ __device__ __forceinline__ void ring_derive(MarchSmem& s, int sl)
     }
 }
 
+// Quantities carried from row step j-1 to row step j (register rotation).
+struct Carry {
+    double ytS, FS;       // T-eq south link piece / flux at v-face (i, j)
+    double utS, FsSum;    // u-eq south tangential piece / half-flux sum at y^f_j
+    double vcS, FbS;      // v-eq south normal piece (cell (i, j)) / F-bar
+    double vhatP, dvP;    // v-hat, d^v at v-face (i, j)
+    double pnP;           // p_new(i, j-1)
+    double gcP;           // corner Gamma (i, j)
+};
+// Values passed between the stages of one row step.
+struct StepVars {
+    double Fx1, Fy1;              // F^x (i, j+1), F^y (i, j+1)
+    double ytN, ytSn;             // T-eq y pieces at v-face (i, j+1)
+    double upsi1, upsi2;          // u-eq tangential psi at y^f_{j+1}
+    double vcN, vcSn, FbN;        // v-eq normal pieces of cell (i, j+1)
+    double gcN;                   // corner Gamma (i, j+1)
+    double xvW, FwSum;            // v-eq tangential W piece / flux sum at x^f_i, v-row j+1
+    double TN, uhat, du, utSn, FsSumN, vhatN, dvN, pn;
+};
+struct NM1 {                      // n-1 state / explicit planes at this thread's points
+    double p1n, T1n;              // row j+1
+    double T1c, u1c, v1n;         // T^{n-1}(i, j), u^{n-1}(i, j), v^{n-1}(i, j+1)
+    double Tec, uec, ven;         // T^exp(i, j), u^exp(i, j), v^exp(i, j+1)
+};
+
+// ================= stage A: row j+1 fluxes, link pieces =================
+template <bool IMPL, bool TVD, bool REG>
+__device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
+                                        const RingRow& R0, const RingRow& Ra, const RingRow& Rb,
+                                        const RingRow& Rc, const FluxRow& Fc, FluxRow& Fn, const NM1& nm,
+                                        StepVars& v)
+{
+    const double dx = m.k.dx, dy = m.k.dy;
+    const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
+    // (p/T)^{n-1} of row j+1
+    Fn.R1[lc] = fdiv(nm.p1n, nm.T1n == 0.0 ? 1.0 : nm.T1n);
+    // F^x, rho^u at u-face (i, j+1)  (Eqs. pl8, pl10, R1)
+    {
+        double ru = 0.0, F = 0.0;
+        if (uFl<REG>(kw1)) {
+            const double w = Ra.U[lc], r1 = Ra.R[lc - 1], r2 = Ra.R[lc];
+            ru = w > 0.0 ? r1 : r2;
+            if (TVD && cF<REG>(Ra.KK[lc - 2]) && cF<REG>(Ra.KK[lc - 1]) && cF<REG>(kw1) && cF<REG>(Ra.KK[lc + 1]))
+                ru += psi_f(Ra.R[lc - 2], r1, r2, Ra.R[lc + 1], w) * (r2 - r1);
+            F = ru * w * dy;
+        }
+        Fn.RU[lc] = ru;
+        Fn.FX[lc] = F;
+        v.Fx1 = F;
+    }
+    // F^y, rho^v at v-face (i, j+1)  (Eqs. pl9, pl11, R1)
+    {
+        double rv = 0.0, F = 0.0;
+        if (vA<REG>(kw1)) {
+            const double w = Ra.V[lc], r1 = R0.R[lc], r2 = Ra.R[lc];
+            rv = w > 0.0 ? r1 : r2;
+            if (TVD && cF<REG>(Rm.KK[lc]) && cF<REG>(kw0) && cF<REG>(kw1) && cF<REG>(Rb.KK[lc]))
+                rv += psi_f(Rm.R[lc], r1, r2, Rb.R[lc], w) * (r2 - r1);
+            F = rv * w * dx;
+        }
+        Fn.RV[lc] = rv;
+        Fn.FY[lc] = F;
+        v.Fy1 = F;
+    }
+    // T-eq x-face pieces at u-face (i, j): a^T_1 of cell i, a^T_2 of cell i-1 (Eqs. pl31-pl33)
+    {
+        double pw = 0.0, pe = 0.0;
+        const uint32_t kl = R0.KK[lc - 1];
+        if (!cW<REG>(kl) && !cW<REG>(kw0)) {
+            const double F = Fc.FX[lc];
+            const double g1 = R0.G[lc - 1], g2 = R0.G[lc];
+            const double D = m.CT1_dydx * (2.0 * g1 * g2 * rcp(g1 + g2));
+            double ps = 0.0;
+            if (IMPL && TVD && cF<REG>(R0.KK[lc - 2]) && cF<REG>(kl) && cF<REG>(kw0) && cF<REG>(R0.KK[lc + 1]))
+                ps = psi_f(R0.T[lc - 2], R0.T[lc - 1], R0.T[lc], R0.T[lc + 1], R0.U[lc]);
+            pw = (IMPL ? max0(F) - F * ps : 0.0) + D;
+            pe = (IMPL ? max0(-F) - F * ps : 0.0) + D;
+        }
+        s.XTW[lc] = pw;
+        s.XTE[lc] = pe;
+    }
+    // T-eq y-face piece at v-face (i, j+1): a^T_4 of cell (i, j), a^T_3 of cell (i, j+1)
+    v.ytN = 0.0;
+    v.ytSn = 0.0;
+    if (!cW<REG>(kw0) && !cW<REG>(kw1)) {
+        const double F = v.Fy1;
+        const double g1 = R0.G[lc], g2 = Ra.G[lc];
+        const double D = m.CT1_dxdy * (2.0 * g1 * g2 * rcp(g1 + g2));
+        double ps = 0.0;
+        if (IMPL && TVD && cF<REG>(Rm.KK[lc]) && cF<REG>(kw0) && cF<REG>(kw1) && cF<REG>(Rb.KK[lc]))
+            ps = psi_f(Rm.T[lc], R0.T[lc], Ra.T[lc], Rb.T[lc], Ra.V[lc]);
+        v.ytN = (IMPL ? max0(-F) - F * ps : 0.0) + D;
+        v.ytSn = (IMPL ? max0(F) - F * ps : 0.0) + D;
+    }
+    // u-eq x pieces of cell (i, j): a^u_2 of face i, a^u_1 of face i+1 (transposed pl15)
+    {
+        double xe = 0.0, xw = 0.0, Fb = 0.0;
+        if (cF<REG>(kw0)) {
+            const double ub = 0.5 * (R0.U[lc] + R0.U[lc + 1]);
+            Fb = R0.R[lc] * ub * dy;
+            const double D = 4.0 / 3.0 * m.B_dydx * R0.G[lc];
+            double ps = 0.0;
+            if (IMPL && TVD && uA<REG>(R0.KK[lc - 1]) && uA<REG>(kw0) && uA<REG>(R0.KK[lc + 1]) &&
+                uA<REG>(R0.KK[lc + 2]))
+                ps = psi_f(R0.U[lc - 1], R0.U[lc], R0.U[lc + 1], R0.U[lc + 2], ub);
+            xe = (IMPL ? max0(-Fb) - Fb * ps : 0.0) + D;
+            xw = (IMPL ? max0(Fb) - Fb * ps : 0.0) + D;
+        }
+        s.XUE[lc] = xe;
+        s.XUW[lc] = xw;
+        s.FBX[lc] = Fb;
+    }
+    // u-eq tangential psi at (u column i, y^f_{j+1}) (fluxes need the neighbour: stage C)
+    v.upsi1 = 0.0;
+    v.upsi2 = 0.0;
+    if (IMPL && TVD && uA<REG>(Rm.KK[lc]) && uA<REG>(kw0) && uA<REG>(kw1) && uA<REG>(Rb.KK[lc])) {
+        const double f1 = Rm.U[lc], f2 = R0.U[lc], f3 = Ra.U[lc], f4 = Rb.U[lc];
+        v.upsi1 = psi_f(f1, f2, f3, f4, Ra.V[lc]);
+        v.upsi2 = psi_f(f1, f2, f3, f4, Ra.V[lc - 1]);
+    }
+    // v-eq normal piece of cell (i, j+1): a^v_4 of v-face (i, j+1), a^v_3 of v-face (i, j+2)
+    v.vcN = 0.0;
+    v.vcSn = 0.0;
+    v.FbN = 0.0;
+    if (cF<REG>(kw1)) {
+        const double vb = 0.5 * (Ra.V[lc] + Rb.V[lc]);
+        v.FbN = Ra.R[lc] * vb * dx;
+        const double D = 4.0 / 3.0 * m.B_dxdy * Ra.G[lc];
+        double ps = 0.0;
+        if (IMPL && TVD && vA<REG>(kw0) && vA<REG>(kw1) && vA<REG>(Rb.KK[lc]) && vA<REG>(Rc.KK[lc]))
+            ps = psi_f(R0.V[lc], Ra.V[lc], Rb.V[lc], Rc.V[lc], vb);
+        v.vcN = (IMPL ? max0(-v.FbN) - v.FbN * ps : 0.0) + D;
+        v.vcSn = (IMPL ? max0(v.FbN) - v.FbN * ps : 0.0) + D;
+    }
+    // corner Gamma at (x^f_i, y^f_{j+1}) (R4, R5; BC spec 8)
+    if (REG) {
+        v.gcN = 0.25 * (R0.G[lc - 1] + R0.G[lc] + Ra.G[lc - 1] + Ra.G[lc]);
+    } else {
+        double sum = 0.0;
+        int n = 0;
+        if (!wallish(ckind(R0.KK[lc - 1]))) { sum += R0.G[lc - 1]; n++; }
+        if (!wallish(ckind(kw0))) { sum += R0.G[lc]; n++; }
+        if (!wallish(ckind(Ra.KK[lc - 1]))) { sum += Ra.G[lc - 1]; n++; }
+        if (!wallish(ckind(kw1))) { sum += Ra.G[lc]; n++; }
+        v.gcN = n == 4 ? 0.25 * sum : (n > 0 ? sum / n : 0.0);
+    }
+    s.GC[lc] = v.gcN;
+    // v-eq tangential pieces at (u-face column i, v-row j+1): a^v_1 of v-face (i, j+1),
+    // a^v_2 of v-face (i-1, j+1)
+    {
+        const double F1 = v.Fx1, F2 = Fc.FX[lc];     // rows j+1 (upper half) and j (lower half)
+        double p1 = 0.0, p2 = 0.0;
+        if (IMPL && TVD && vA<REG>(Ra.KK[lc - 2]) && vA<REG>(Ra.KK[lc - 1]) && vA<REG>(kw1) &&
+            vA<REG>(Ra.KK[lc + 1])) {
+            const double f1 = Ra.V[lc - 2], f2 = Ra.V[lc - 1], f3 = Ra.V[lc], f4 = Ra.V[lc + 1];
+            p1 = psi_f(f1, f2, f3, f4, Ra.U[lc]);
+            p2 = psi_f(f1, f2, f3, f4, R0.U[lc]);
+        }
+        const double D = m.B_dydx * v.gcN;
+        v.xvW = (IMPL ? 0.5 * (max0(F1) - F1 * p1 + max0(F2) - F2 * p2) : 0.0) + D;
+        s.XVE[lc] = (IMPL ? 0.5 * (max0(-F1) - F1 * p1 + max0(-F2) - F2 * p2) : 0.0) + D;
+        v.FwSum = F1 + F2;
+        s.XVF[lc] = v.FwSum;
+    }
+}
+
+// ================= stage C: T_{i,j}, u-hat_{i,j}, v-hat_{i,j+1} =================
+template <bool IMPL, bool TVD, bool REG>
+__device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
+                                        const RingRow& R0, const RingRow& Ra, const RingRow& Rb,
+                                        const FluxRow& Fc, const FluxRow& Fn, const NM1& nm, const Carry& c,
+                                        StepVars& v)
+{
+    const Params& k = m.k;
+    const double dt = k.dt, dx = k.dx, dy = k.dy;
+    const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
+    const double rP = R0.R[lc], gP = R0.G[lc];
+    // ---- energy (Eqs. pl30-pl33, pl28-pl29 / pl31_1)
+    v.TN = 0.0;
+    if (cF<REG>(kw0)) {
+        double a1, a2, a3, a4, T1, T2, T3, T4, FW, FE, FSl, FNl;
+        if (REG) {
+            a1 = s.XTW[lc]; FW = Fc.FX[lc]; T1 = R0.T[lc - 1];
+            a2 = s.XTE[lc + 1]; FE = Fc.FX[lc + 1]; T2 = R0.T[lc + 1];
+            a3 = c.ytS; FSl = c.FS; T3 = Rm.T[lc];
+            a4 = v.ytN; FNl = v.Fy1; T4 = Ra.T[lc];
+        } else {
+            FW = FE = FSl = FNl = 0.0;
+            const double tau = 2.1904 * k.Kn * rcp(rP);   // Eq. pl39 (P:696)
+            uint8_t kn = ckind(R0.KK[lc - 1]);
+            if (wallish(kn)) { a1 = k.CT1 * gP * dy * rcp(0.5 * dx + tau); T1 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
+            else { a1 = s.XTW[lc]; FW = Fc.FX[lc]; T1 = R0.T[lc - 1]; }
+            kn = ckind(R0.KK[lc + 1]);
+            if (wallish(kn)) { a2 = k.CT1 * gP * dy * rcp(0.5 * dx + tau); T2 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
+            else { a2 = s.XTE[lc + 1]; FE = Fc.FX[lc + 1]; T2 = R0.T[lc + 1]; }
+            kn = ckind(Rm.KK[lc]);
+            if (wallish(kn)) { a3 = k.CT1 * gP * dx * rcp(0.5 * dy + tau); T3 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
+            else { a3 = c.ytS; FSl = c.FS; T3 = Rm.T[lc]; }
+            kn = ckind(kw1);
+            if (wallish(kn)) { a4 = k.CT1 * gP * dx * rcp(0.5 * dy + tau); T4 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
+            else { a4 = v.ytN; FNl = v.Fy1; T4 = Ra.T[lc]; }
+        }
+        const double a0 = IMPL ? dt * (a1 + a2 + a3 + a4 + FE - FW + FNl - FSl) + rP * m.dV
+                               : dt * (a1 + a2 + a3 + a4) + rP * m.dV;
+        // S^T_c, Eq. pl29 (R4 bilinear = 4-point mean; R9 sign)
+        const double dudx = (R0.U[lc + 1] - R0.U[lc]) * m.inv_dx;
+        const double dvdy = (Ra.V[lc] - R0.V[lc]) * m.inv_dy;
+        const double vE = 0.25 * (R0.V[lc] + R0.V[lc + 1] + Ra.V[lc] + Ra.V[lc + 1]);
+        const double vW = 0.25 * (R0.V[lc - 1] + R0.V[lc] + Ra.V[lc - 1] + Ra.V[lc]);
+        const double uN = 0.25 * (R0.U[lc] + R0.U[lc + 1] + Ra.U[lc] + Ra.U[lc + 1]);
+        const double uS = 0.25 * (Rm.U[lc] + Rm.U[lc + 1] + R0.U[lc] + R0.U[lc + 1]);
+        const double shear = (vE - vW) * m.inv_dx + (uN - uS) * m.inv_dy;
+        const double div = dudx + dvdy;
+        const double Sc = (k.CT2 * gP * (2.0 * (dudx * dudx + dvdy * dvdy) + shear * shear - 2.0 / 3.0 * div * div)
+                           + k.pw_sign * k.CT3 * R0.P[lc] * div) * m.dV;
+        const double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + Sc + nm.Tec) + Fc.R1[lc] * nm.T1c * m.dV;
+        v.TN = rhs * rcp(a0);
+    }
+    // ---- u pseudo-velocity at u-face (i, j)
+    {
+        // N tangential link pieces at y^f_{j+1} (both sides; the S side is carried)
+        const double F1 = v.Fy1, F2 = Fn.FY[lc - 1];
+        const double D = m.B_dxdy * v.gcN;
+        const double a4p = (IMPL ? 0.5 * (max0(-F1) - F1 * v.upsi1 + max0(-F2) - F2 * v.upsi2) : 0.0) + D;
+        v.utSn = (IMPL ? 0.5 * (max0(F1) - F1 * v.upsi1 + max0(F2) - F2 * v.upsi2) : 0.0) + D;
+        v.FsSumN = F1 + F2;
+        double uhat = 0.0, du = 0.0;
+        if (uA<REG>(kw0)) {
+            const double rL = R0.R[lc - 1], rR = rP, gL = R0.G[lc - 1], gR = gP;
+            const double a1 = s.XUW[lc - 1], a2 = s.XUE[lc];
+            const double FbW = s.FBX[lc - 1], FbE = s.FBX[lc];
+            double a3, a4, uS, uN, FsS, FnS;
+            if (REG) {
+                a3 = c.utS; FsS = c.FsSum; uS = Rm.U[lc];
+                a4 = a4p; FnS = v.FsSumN; uN = Ra.U[lc];
+            } else {
+                FsS = FnS = 0.0;
+                const double gadj = 0.5 * (gL + gR);
+                const double zeta = 1.1466 * k.Kn * rcp(0.5 * (rL + rR));     // Eq. pl38 (P:691)
+                const uint8_t kl = ckind(Rm.KK[lc - 1]), kr = ckind(Rm.KK[lc]);
+                if (kl == CK_WALLY || (kl == CK_SOLID && kr == CK_SOLID)) {
+                    a3 = k.B * gadj * dx * rcp(0.5 * dy + zeta); uS = kl == CK_WALLY ? k.u_wb : 0.0;
+                } else { a3 = c.utS; FsS = c.FsSum; uS = Rm.U[lc]; }
+                const uint8_t ml = ckind(Ra.KK[lc - 1]), mr = ckind(kw1);
+                if (ml == CK_WALLY || (ml == CK_SOLID && mr == CK_SOLID)) {
+                    a4 = k.B * gadj * dx * rcp(0.5 * dy + zeta); uN = ml == CK_WALLY ? k.u_wt : 0.0;
+                } else { a4 = a4p; FnS = v.FsSumN; uN = Ra.U[lc]; }
+            }
+            const double tterm = (rR + rL) * m.c_t;
+            const double a0 = IMPL ? a1 + a2 + a3 + a4 + FbE - FbW + 0.5 * (FnS - FsS) + tterm
+                                   : a1 + a2 + a3 + a4 + tterm;
+            const double b = (Fc.R1[lc] + Fc.R1[lc - 1]) * m.c_t * nm.u1c
+                           + k.B * (v.gcN * (Ra.V[lc] - Ra.V[lc - 1]) - c.gcP * (R0.V[lc] - R0.V[lc - 1])
+                                    - 2.0 / 3.0 * gR * (Ra.V[lc] - R0.V[lc])
+                                    + 2.0 / 3.0 * gL * (Ra.V[lc - 1] - R0.V[lc - 1]))
+                           + k.g_x * (rR + rL) * m.half_dV;
+            const double r = rcp(a0);
+            uhat = (a1 * R0.U[lc - 1] + a2 * R0.U[lc + 1] + a3 * uS + a4 * uN + b + nm.uec) * r;
+            du = m.A_dy * r;
+        }
+        v.uhat = uhat;
+        v.du = du;
+        s.UH[lc] = uhat;
+        s.DU[lc] = du;
+    }
+    // ---- v pseudo-velocity at v-face (i, j+1)
+    v.vhatN = 0.0;
+    v.dvN = 0.0;
+    if (vA<REG>(kw1)) {
+        const double rB = rP, rT = Ra.R[lc], gB = gP, gT = Ra.G[lc];
+        double a1, a2, vW, vE, FwS, FeS;
+        if (REG) {
+            a1 = v.xvW; FwS = v.FwSum; vW = Ra.V[lc - 1];
+            a2 = s.XVE[lc + 1]; FeS = s.XVF[lc + 1]; vE = Ra.V[lc + 1];
+        } else {
+            FwS = FeS = 0.0;
+            const double gadj = 0.5 * (gB + gT);
+            const double zeta = 1.1466 * k.Kn * rcp(0.5 * (rB + rT));
+            if (ckind(R0.KK[lc - 1]) == CK_SOLID && ckind(Ra.KK[lc - 1]) == CK_SOLID) {
+                a1 = k.B * gadj * dy * rcp(0.5 * dx + zeta); vW = 0.0;
+            } else { a1 = v.xvW; FwS = v.FwSum; vW = Ra.V[lc - 1]; }
+            if (ckind(R0.KK[lc + 1]) == CK_SOLID && ckind(Ra.KK[lc + 1]) == CK_SOLID) {
+                a2 = k.B * gadj * dy * rcp(0.5 * dx + zeta); vE = 0.0;
+            } else { a2 = s.XVE[lc + 1]; FeS = s.XVF[lc + 1]; vE = Ra.V[lc + 1]; }
+        }
+        const double a3 = c.vcS, a4 = v.vcN;
+        const double tterm = (rT + rB) * m.c_t;
+        const double a0 = IMPL ? a1 + a2 + a3 + a4 + 0.5 * (FeS - FwS) + v.FbN - c.FbS + tterm
+                               : a1 + a2 + a3 + a4 + tterm;
+        const double b = (Fn.R1[lc] + Fc.R1[lc]) * m.c_t * nm.v1n
+                       + k.B * (s.GC[lc + 1] * (Ra.U[lc + 1] - R0.U[lc + 1]) - v.gcN * (Ra.U[lc] - R0.U[lc])
+                                - 2.0 / 3.0 * gT * (Ra.U[lc + 1] - Ra.U[lc])
+                                + 2.0 / 3.0 * gB * (R0.U[lc + 1] - R0.U[lc]))
+                       + k.g_y * (rT + rB) * m.half_dV;
+        const double r = rcp(a0);
+        v.vhatN = (a1 * vW + a2 * vE + a3 * R0.V[lc] + a4 * Rb.V[lc] + b + nm.ven) * r;
+        v.dvN = m.A_dx * r;
+    }
+}
+
+// ================= stage D: p_{i,j} (Eqs. pl23-pl24) =================
+template <bool REG>
+__device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
+                                        const RingRow& R0, const RingRow& Ra, const FluxRow& Fc,
+                                        const FluxRow& Fn, const Carry& c, StepVars& v)
+{
+    const Params& k = m.k;
+    const double dt = k.dt, dx = k.dx, dy = k.dy;
+    const uint32_t kw0 = R0.KK[lc];
+    double pn = R0.P[lc];
+    if (cF<REG>(kw0)) {
+        double apW = 0.0, apE = 0.0, apS = 0.0, apN = 0.0, bpW = 0.0, bpE = 0.0, bpS = 0.0, bpN = 0.0, sum = 0.0;
+        if (REG) {
+            const double rw = Fc.RU[lc], re = Fc.RU[lc + 1], rs = Fc.RV[lc], rn = Fn.RV[lc];
+            apW = rw * v.du * dy; bpW = rw * v.uhat * dy;
+            apE = re * s.DU[lc + 1] * dy; bpE = re * s.UH[lc + 1] * dy;
+            apS = rs * c.dvP * dx; bpS = rs * c.vhatP * dx;
+            apN = rn * v.dvN * dx; bpN = rn * v.vhatN * dx;
+            sum = apW * R0.P[lc - 1] + apE * R0.P[lc + 1] + apS * Rm.P[lc] + apN * Ra.P[lc];
+        } else {
+            const uint8_t kwf = ukind(kw0), kef = ukind(R0.KK[lc + 1]);
+            if (kwf == FK_ACTIVE) {
+                const double r = Fc.RU[lc];
+                apW = r * v.du * dy; bpW = r * v.uhat * dy; sum += apW * R0.P[lc - 1];
+            } else if (kwf == FK_INLET) bpW = Fc.RU[lc] * k.u_in * dy;
+            if (kef == FK_ACTIVE) {
+                const double r = Fc.RU[lc + 1];
+                apE = r * s.DU[lc + 1] * dy; bpE = r * s.UH[lc + 1] * dy; sum += apE * R0.P[lc + 1];
+            } else if (kef == FK_OUTLET) bpE = Fc.RU[lc + 1] * R0.U[lc] * dy;
+            if (vkind(kw0) == FK_ACTIVE) {
+                const double r = Fc.RV[lc];
+                apS = r * c.dvP * dx; bpS = r * c.vhatP * dx; sum += apS * Rm.P[lc];
+            }
+            if (vkind(Ra.KK[lc]) == FK_ACTIVE) {
+                const double r = Fn.RV[lc];
+                apN = r * v.dvN * dx; bpN = r * v.vhatN * dx; sum += apN * Ra.P[lc];
+            }
+        }
+        const double a0 = m.dV * rcp(v.TN) + (apW + apE + apS + apN) * dt;
+        const double bp = Fc.R1[lc] * m.dV - (bpE - bpW + bpN - bpS) * dt;
+        pn = (sum * dt + bp) * rcp(a0);
+    }
+    v.pn = pn;
+    s.PN[lc] = pn;
+}
+
+struct Resid { double du, dv, dp, dT, vel, p, T; long long bad; int badf; };
+
+// ================= stage E: corrections, writes, residuals =================
+template <bool REG>
+__device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int lc, int gi, int j,
+                                        const RingRow& R0, const Carry& c, const StepVars& v, Resid& rs)
+{
+    const Params& k = m.k;
+    const long long id = gidx(k, gi, j);
+    const uint32_t kw0 = R0.KK[lc];
+    const bool fluid = cF<REG>(kw0);
+    if (fluid) {
+        k.T_w[id] = v.TN;
+        k.p_w[id] = v.pn;
+        rs.dT = nmax(rs.dT, fabs(v.TN - R0.T[lc]));
+        rs.dp = nmax(rs.dp, fabs(v.pn - R0.P[lc]));
+        rs.T = nmax(rs.T, fabs(v.TN));
+        rs.p = nmax(rs.p, fabs(v.pn));
+        if (!(v.TN > 0.0) || !(v.pn > 0.0) || !isfinite(v.TN) || !isfinite(v.pn)) {
+            const long long flat = (long long)j * k.nx + gi;
+            if (rs.bad < 0 || flat < rs.bad) { rs.bad = flat; rs.badf = (!(v.TN > 0.0) || !isfinite(v.TN)) ? 3 : 2; }
+        }
+    }
+    double un = 0.0;
+    if (uA<REG>(kw0)) {
+        un = v.uhat - v.du * (v.pn - s.PN[lc - 1]);
+        rs.du = nmax(rs.du, fabs(un - R0.U[lc]));
+        rs.vel = nmax(rs.vel, fabs(un));
+    } else if (ukind(kw0) == FK_INLET) un = k.u_in;
+    k.u_w[id] = un;
+    double vn = 0.0;
+    if (vA<REG>(kw0)) {
+        vn = c.vhatP - c.dvP * (v.pn - c.pnP);
+        rs.dv = nmax(rs.dv, fabs(vn - R0.V[lc]));
+        rs.vel = nmax(rs.vel, fabs(vn));
+    }
+    k.v_w[id] = vn;
+    if (!REG && k.xbc == 0 && gi == k.nx - 1) {
+        k.u_w[id + 1] = R0.U[lc];                    // outlet face: u_old(nx-1), BC spec 3
+        const double pv = fluid ? v.pn : R0.P[lc];
+        const double Tv = fluid ? v.TN : R0.T[lc];
+        for (int g = 1; g <= OFF - 1; g++) { k.p_w[id + g] = pv; k.T_w[id + g] = Tv; k.v_w[id + g] = vn; }
+    }
+    if (k.mirror) {                                  // single-rank periodic: wrapped ghosts
+        int tgt = -1000;
+        if (gi < OFF) tgt = gi + k.nx;
+        else if (gi >= k.nx - OFF) tgt = gi - k.nx;
+        if (tgt > -1000) {
+            const long long tt = gidx(k, tgt, j);
+            if (fluid) { k.p_w[tt] = v.pn; k.T_w[tt] = v.TN; }
+            k.u_w[tt] = un;
+            k.v_w[tt] = vn;
+        }
+    }
+}
+
 template <bool IMPL, bool TVD>
 __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
 {
@@ -170,14 +588,15 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
     const Params& k = m.k;
     const int t = threadIdx.x;
     const int lc = t + 2;                               // ring column of this thread's column
-    const int I0 = k.gi0 + blockIdx.x * MW;             // first owned column of the strip
+    const int cta = m.order[blockIdx.x];
+    const int strip = cta % m.nstrips, segi = cta / m.nstrips;
+    const int I0 = k.gi0 + strip * MW;                  // first owned column of the strip
     const int gi = I0 - 2 + t;                          // this thread's global column
-    const int J0 = blockIdx.y * m.seg;
+    const int J0 = segi * m.seg;
     const int J1 = min(J0 + m.seg, k.ny);
     const int js = J0 - WARM;
     const bool col_stored = stored_col(k, gi);
     const bool owner = t >= 2 && t < 2 + MW && gi < k.gi0 + k.nloc;
-    const double dt = k.dt, dx = k.dx, dy = k.dy;
 
     // ---- prologue: ring rows js-1 .. js+2 (synchronous), issue js+3
     for (int j = js - 1; j <= js + 2; j++) ring_issue(s, m, I0, j, slot(j));
@@ -194,22 +613,15 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
     auto ldv = [&](const double* a, int j) -> double {
         return (col_stored && j >= 0 && j <= k.ny) ? __ldg(a + gidx(k, gi, j)) : 0.0;
     };
-    double p1n = ld(k.p_1, js + 1), T1n = ld(k.T_1, js + 1);     // row j+1 at step js
-    double T1c = ld(k.T_1, js), u1c = ld(k.u_1, js), v1n = ldv(k.v_1, js + 1);
-    double Tec = 0.0, uec = 0.0, ven = 0.0;
-    if (!IMPL) { Tec = ld(k.Te, js); uec = ld(k.ue, js); ven = ldv(k.ve, js + 1); }
+    NM1 nm;
+    nm.p1n = ld(k.p_1, js + 1); nm.T1n = ld(k.T_1, js + 1);
+    nm.T1c = ld(k.T_1, js); nm.u1c = ld(k.u_1, js); nm.v1n = ldv(k.v_1, js + 1);
+    nm.Tec = nm.uec = nm.ven = 0.0;
+    if (!IMPL) { nm.Tec = ld(k.Te, js); nm.uec = ld(k.ue, js); nm.ven = ldv(k.ve, js + 1); }
 
-    // ---- carried (row-rotated) quantities, valid after the warm-up
-    double ytS = 0.0, FS = 0.0;           // T-eq south link piece / flux at v-face (i, j)
-    double utS = 0.0, FsSum = 0.0;        // u-eq south tangential piece / half-flux sum
-    double vcS = 0.0, FbS = 0.0;          // v-eq south normal piece (cell (i, j)) / F-bar
-    double vhatP = 0.0, dvP = 0.0;        // v-hat, d^v at v-face (i, j)
-    double pnP = 1.0;                     // p_new(i, j-1)
-    double gcP = 1.0;                     // corner Gamma (i, j)
-
-    double r_du = 0.0, r_dv = 0.0, r_dp = 0.0, r_dT = 0.0, r_vel = 0.0, r_p = 0.0, r_T = 0.0;
-    long long bad = -1;
-    int badf = 0;
+    Carry c{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 1.0};
+    Resid rs{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, -1, 0};
+    StepVars v;
 
     for (int j = js; j < J1; j++) {
         const int sa = sj + 1 == RS ? 0 : sj + 1, sb = sa + 1 == RS ? 0 : sa + 1;
@@ -222,373 +634,66 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
         RingRow& Rc = s.ring[sc];
         FluxRow& Fc = s.fr[j & 1];
         FluxRow& Fn = s.fr[(j + 1) & 1];
-        const bool out_row = j >= J0;
 
         // prefetch the next row's n-1 / plane values (consumed one step later)
-        double p1nn = ld(k.p_1, j + 2), T1nn = ld(k.T_1, j + 2);
-        double u1n = ld(k.u_1, j + 1), v1nn = ldv(k.v_1, j + 2);
+        const double p1nn = ld(k.p_1, j + 2), T1nn = ld(k.T_1, j + 2);
+        const double u1n = ld(k.u_1, j + 1), v1nn = ldv(k.v_1, j + 2);
         double Ten = 0.0, uen = 0.0, vem = 0.0;
         if (!IMPL) { Ten = ld(k.Te, j + 1); uen = ld(k.ue, j + 1); vem = ldv(k.ve, j + 2); }
 
         cp_wait_all();
         __syncthreads();                                    // B0: ring row j+3 landed
         ring_issue(s, m, I0, j + 4, sd);
-
-        // ================= stage A: row j+1 fluxes, link pieces =================
         ring_derive(s, sc);
-        const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
-        // (p/T)^{n-1} of row j+1
-        Fn.R1[lc] = fdiv(p1n, T1n == 0.0 ? 1.0 : T1n);
-        // F^x, rho^u at u-face (i, j+1)  (Eqs. pl8, pl10, R1)
-        double Fx1 = 0.0;
-        {
-            double ru = 0.0;
-            const uint8_t uk = ukind(kw1);
-            if (flux_face(uk)) {
-                const double w = Ra.U[lc], r1 = Ra.R[lc - 1], r2 = Ra.R[lc];
-                ru = w > 0.0 ? r1 : r2;
-                if (TVD && ckind(Ra.KK[lc - 2]) == CK_FLUID && ckind(Ra.KK[lc - 1]) == CK_FLUID &&
-                    ckind(kw1) == CK_FLUID && ckind(Ra.KK[lc + 1]) == CK_FLUID)
-                    ru += psi_f(Ra.R[lc - 2], r1, r2, Ra.R[lc + 1], w) * (r2 - r1);
-                Fx1 = ru * w * dy;
-            }
-            Fn.RU[lc] = ru;
-            Fn.FX[lc] = Fx1;
-        }
-        // F^y, rho^v at v-face (i, j+1)  (Eqs. pl9, pl11, R1)
-        double Fy1 = 0.0;
-        {
-            double rv = 0.0;
-            if (vkind(kw1) == FK_ACTIVE) {
-                const double w = Ra.V[lc], r1 = R0.R[lc], r2 = Ra.R[lc];
-                rv = w > 0.0 ? r1 : r2;
-                if (TVD && ckind(Rm.KK[lc]) == CK_FLUID && ckind(kw0) == CK_FLUID && ckind(kw1) == CK_FLUID &&
-                    ckind(Rb.KK[lc]) == CK_FLUID)
-                    rv += psi_f(Rm.R[lc], r1, r2, Rb.R[lc], w) * (r2 - r1);
-                Fy1 = rv * w * dx;
-            }
-            Fn.RV[lc] = rv;
-            Fn.FY[lc] = Fy1;
-        }
-        // T-eq x-face pieces at u-face (i, j): a^T_1 of cell i, a^T_2 of cell i-1 (Eqs. pl31-pl33)
-        {
-            double pw = 0.0, pe = 0.0;
-            const uint8_t kl = ckind(R0.KK[lc - 1]), kr = ckind(kw0);
-            if (!wallish(kl) && !wallish(kr)) {
-                const double F = Fc.FX[lc];
-                const double g1 = R0.G[lc - 1], g2 = R0.G[lc];
-                const double D = m.CT1_dydx * (2.0 * g1 * g2 * rcp(g1 + g2));
-                double ps = 0.0;
-                if (IMPL && TVD && ckind(R0.KK[lc - 2]) == CK_FLUID && kl == CK_FLUID && kr == CK_FLUID &&
-                    ckind(R0.KK[lc + 1]) == CK_FLUID)
-                    ps = psi_f(R0.T[lc - 2], R0.T[lc - 1], R0.T[lc], R0.T[lc + 1], R0.U[lc]);
-                pw = (IMPL ? max0(F) - F * ps : 0.0) + D;
-                pe = (IMPL ? max0(-F) - F * ps : 0.0) + D;
-            }
-            s.XTW[lc] = pw;
-            s.XTE[lc] = pe;
-        }
-        // T-eq y-face piece at v-face (i, j+1): a^T_4 of cell (i, j), a^T_3 of cell (i, j+1)
-        double ytN = 0.0, ytSn = 0.0;
-        {
-            const uint8_t kb = ckind(kw0), kt = ckind(kw1);
-            if (!wallish(kb) && !wallish(kt)) {
-                const double F = Fy1;
-                const double g1 = R0.G[lc], g2 = Ra.G[lc];
-                const double D = m.CT1_dxdy * (2.0 * g1 * g2 * rcp(g1 + g2));
-                double ps = 0.0;
-                if (IMPL && TVD && ckind(Rm.KK[lc]) == CK_FLUID && kb == CK_FLUID && kt == CK_FLUID &&
-                    ckind(Rb.KK[lc]) == CK_FLUID)
-                    ps = psi_f(Rm.T[lc], R0.T[lc], Ra.T[lc], Rb.T[lc], Ra.V[lc]);
-                ytN = (IMPL ? max0(-F) - F * ps : 0.0) + D;
-                ytSn = (IMPL ? max0(F) - F * ps : 0.0) + D;
-            }
-        }
-        // u-eq x pieces of cell (i, j): a^u_2 of face i, a^u_1 of face i+1 (transposed pl15)
-        {
-            double xe = 0.0, xw = 0.0, Fb = 0.0;
-            if (ckind(kw0) == CK_FLUID) {
-                const double ub = 0.5 * (R0.U[lc] + R0.U[lc + 1]);
-                Fb = R0.R[lc] * ub * dy;
-                const double D = 4.0 / 3.0 * m.B_dydx * R0.G[lc];
-                double ps = 0.0;
-                if (IMPL && TVD && ukind(R0.KK[lc - 1]) == FK_ACTIVE && ukind(kw0) == FK_ACTIVE &&
-                    ukind(R0.KK[lc + 1]) == FK_ACTIVE && ukind(R0.KK[lc + 2]) == FK_ACTIVE)
-                    ps = psi_f(R0.U[lc - 1], R0.U[lc], R0.U[lc + 1], R0.U[lc + 2], ub);
-                xe = (IMPL ? max0(-Fb) - Fb * ps : 0.0) + D;
-                xw = (IMPL ? max0(Fb) - Fb * ps : 0.0) + D;
-            }
-            s.XUE[lc] = xe;
-            s.XUW[lc] = xw;
-            s.FBX[lc] = Fb;
-        }
-        // u-eq tangential psi at (u column i, y^f_{j+1}) (fluxes need the neighbour: stage C)
-        double upsi1 = 0.0, upsi2 = 0.0;
-        if (IMPL && TVD && ukind(Rm.KK[lc]) == FK_ACTIVE && ukind(kw0) == FK_ACTIVE &&
-            ukind(kw1) == FK_ACTIVE && ukind(Rb.KK[lc]) == FK_ACTIVE) {
-            const double f1 = Rm.U[lc], f2 = R0.U[lc], f3 = Ra.U[lc], f4 = Rb.U[lc];
-            upsi1 = psi_f(f1, f2, f3, f4, Ra.V[lc]);
-            upsi2 = psi_f(f1, f2, f3, f4, Ra.V[lc - 1]);
-        }
-        // v-eq normal piece of cell (i, j+1): a^v_4 of v-face (i, j+1), a^v_3 of v-face (i, j+2)
-        double vcN = 0.0, vcSn = 0.0, FbN = 0.0;
-        if (ckind(kw1) == CK_FLUID) {
-            const double vb = 0.5 * (Ra.V[lc] + Rb.V[lc]);
-            FbN = Ra.R[lc] * vb * dx;
-            const double D = 4.0 / 3.0 * m.B_dxdy * Ra.G[lc];
-            double ps = 0.0;
-            if (IMPL && TVD && vkind(kw0) == FK_ACTIVE && vkind(kw1) == FK_ACTIVE &&
-                vkind(Rb.KK[lc]) == FK_ACTIVE && vkind(Rc.KK[lc]) == FK_ACTIVE)
-                ps = psi_f(R0.V[lc], Ra.V[lc], Rb.V[lc], Rc.V[lc], vb);
-            vcN = (IMPL ? max0(-FbN) - FbN * ps : 0.0) + D;
-            vcSn = (IMPL ? max0(FbN) - FbN * ps : 0.0) + D;
-        }
-        // corner Gamma at (x^f_i, y^f_{j+1}) (R4, R5; BC spec 8)
-        double gcN;
-        {
-            double sum = 0.0;
-            int n = 0;
-            const uint8_t a = ckind(R0.KK[lc - 1]), b = ckind(kw0), c = ckind(Ra.KK[lc - 1]), d = ckind(kw1);
-            if (!wallish(a)) { sum += R0.G[lc - 1]; n++; }
-            if (!wallish(b)) { sum += R0.G[lc]; n++; }
-            if (!wallish(c)) { sum += Ra.G[lc - 1]; n++; }
-            if (!wallish(d)) { sum += Ra.G[lc]; n++; }
-            gcN = n == 4 ? 0.25 * sum : (n > 0 ? sum / n : 0.0);
-            s.GC[lc] = gcN;
-        }
-        // v-eq tangential pieces at (u-face column i, v-row j+1): a^v_1 of v-face (i, j+1),
-        // a^v_2 of v-face (i-1, j+1)
-        double xvW, FwSum;
-        {
-            const double F1 = Fx1, F2 = Fc.FX[lc];     // rows j+1 (upper half) and j (lower half)
-            double p1 = 0.0, p2 = 0.0;
-            if (IMPL && TVD && vkind(Ra.KK[lc - 2]) == FK_ACTIVE && vkind(Ra.KK[lc - 1]) == FK_ACTIVE &&
-                vkind(kw1) == FK_ACTIVE && vkind(Ra.KK[lc + 1]) == FK_ACTIVE) {
-                const double f1 = Ra.V[lc - 2], f2 = Ra.V[lc - 1], f3 = Ra.V[lc], f4 = Ra.V[lc + 1];
-                p1 = psi_f(f1, f2, f3, f4, Ra.U[lc]);
-                p2 = psi_f(f1, f2, f3, f4, R0.U[lc]);
-            }
-            const double D = m.B_dydx * gcN;
-            xvW = (IMPL ? 0.5 * (max0(F1) - F1 * p1 + max0(F2) - F2 * p2) : 0.0) + D;
-            s.XVE[lc] = (IMPL ? 0.5 * (max0(-F1) - F1 * p1 + max0(-F2) - F2 * p2) : 0.0) + D;
-            FwSum = F1 + F2;
-            s.XVF[lc] = FwSum;
-        }
+        // per-point choice (a function of the cell alone, so any decomposition
+        // gives bit-identical results); warps mixing both kinds run both
+        // instances -- such CTAs are scheduled first (host longest-first order)
+        const bool reg = (R0.KK[lc] & REG_BIT) != 0u;
+        if (reg) stage_A<IMPL, TVD, true>(s, m, lc, Rm, R0, Ra, Rb, Rc, Fc, Fn, nm, v);
+        else stage_A<IMPL, TVD, false>(s, m, lc, Rm, R0, Ra, Rb, Rc, Fc, Fn, nm, v);
         __syncthreads();                                    // B1
-
-        // ================= stage C: T_{i,j}, u-hat_{i,j}, v-hat_{i,j+1} =================
-        const double rP = R0.R[lc], gP = R0.G[lc];
-        double TN = 0.0;
-        if (ckind(kw0) == CK_FLUID) {
-            const double tau = 2.1904 * k.Kn * rcp(rP);   // Eq. pl39 (P:696)
-            double a1, a2, a3, a4, T1, T2, T3, T4, FW = 0.0, FE = 0.0, FSl = 0.0, FNl = 0.0;
-            uint8_t kn = ckind(R0.KK[lc - 1]);
-            if (wallish(kn)) { a1 = k.CT1 * gP * dy * rcp(0.5 * dx + tau); T1 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { a1 = s.XTW[lc]; FW = Fc.FX[lc]; T1 = R0.T[lc - 1]; }
-            kn = ckind(R0.KK[lc + 1]);
-            if (wallish(kn)) { a2 = k.CT1 * gP * dy * rcp(0.5 * dx + tau); T2 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { a2 = s.XTE[lc + 1]; FE = Fc.FX[lc + 1]; T2 = R0.T[lc + 1]; }
-            kn = ckind(Rm.KK[lc]);
-            if (wallish(kn)) { a3 = k.CT1 * gP * dx * rcp(0.5 * dy + tau); T3 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { a3 = ytS; FSl = FS; T3 = Rm.T[lc]; }
-            kn = ckind(kw1);
-            if (wallish(kn)) { a4 = k.CT1 * gP * dx * rcp(0.5 * dy + tau); T4 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { a4 = ytN; FNl = Fy1; T4 = Ra.T[lc]; }
-            const double a0 = IMPL ? dt * (a1 + a2 + a3 + a4 + FE - FW + FNl - FSl) + rP * m.dV
-                                   : dt * (a1 + a2 + a3 + a4) + rP * m.dV;
-            // S^T_c, Eq. pl29 (R4 bilinear = 4-point mean; R9 sign)
-            const double dudx = (R0.U[lc + 1] - R0.U[lc]) * m.inv_dx;
-            const double dvdy = (Ra.V[lc] - R0.V[lc]) * m.inv_dy;
-            const double vE = 0.25 * (R0.V[lc] + R0.V[lc + 1] + Ra.V[lc] + Ra.V[lc + 1]);
-            const double vW = 0.25 * (R0.V[lc - 1] + R0.V[lc] + Ra.V[lc - 1] + Ra.V[lc]);
-            const double uN = 0.25 * (R0.U[lc] + R0.U[lc + 1] + Ra.U[lc] + Ra.U[lc + 1]);
-            const double uS = 0.25 * (Rm.U[lc] + Rm.U[lc + 1] + R0.U[lc] + R0.U[lc + 1]);
-            const double shear = (vE - vW) * m.inv_dx + (uN - uS) * m.inv_dy;
-            const double div = dudx + dvdy;
-            const double Sc = (k.CT2 * gP * (2.0 * (dudx * dudx + dvdy * dvdy) + shear * shear - 2.0 / 3.0 * div * div)
-                               + k.pw_sign * k.CT3 * R0.P[lc] * div) * m.dV;
-            const double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + Sc + Tec) + Fc.R1[lc] * T1c * m.dV;
-            TN = rhs * rcp(a0);
-        }
-        // u-eq at u-face (i, j)
-        double uhat = 0.0, du = 0.0;
-        double utSn, FsSumN;
-        {
-            // N tangential link pieces at y^f_{j+1} (both sides; the S side is carried)
-            const double F1 = Fy1, F2 = Fn.FY[lc - 1];
-            const double D = m.B_dxdy * gcN;
-            const double a4p = (IMPL ? 0.5 * (max0(-F1) - F1 * upsi1 + max0(-F2) - F2 * upsi2) : 0.0) + D;
-            utSn = (IMPL ? 0.5 * (max0(F1) - F1 * upsi1 + max0(F2) - F2 * upsi2) : 0.0) + D;
-            FsSumN = F1 + F2;
-            if (ukind(kw0) == FK_ACTIVE) {
-                const double rL = R0.R[lc - 1], rR = rP, gL = R0.G[lc - 1], gR = gP;
-                const double gadj = 0.5 * (gL + gR);
-                const double zeta = 1.1466 * k.Kn * rcp(0.5 * (rL + rR));     // Eq. pl38 (P:691)
-                const double a1 = s.XUW[lc - 1], a2 = s.XUE[lc];
-                const double FbW = s.FBX[lc - 1], FbE = s.FBX[lc];
-                double a3, a4, uS, uN, FsS = 0.0, FnS = 0.0;
-                const uint8_t kl = ckind(Rm.KK[lc - 1]), kr = ckind(Rm.KK[lc]);
-                if (kl == CK_WALLY || (kl == CK_SOLID && kr == CK_SOLID)) {
-                    a3 = k.B * gadj * dx * rcp(0.5 * dy + zeta); uS = kl == CK_WALLY ? k.u_wb : 0.0;
-                } else { a3 = utS; FsS = FsSum; uS = Rm.U[lc]; }
-                const uint8_t ml = ckind(Ra.KK[lc - 1]), mr = ckind(kw1);
-                if (ml == CK_WALLY || (ml == CK_SOLID && mr == CK_SOLID)) {
-                    a4 = k.B * gadj * dx * rcp(0.5 * dy + zeta); uN = ml == CK_WALLY ? k.u_wt : 0.0;
-                } else { a4 = a4p; FnS = FsSumN; uN = Ra.U[lc]; }
-                const double tterm = (rR + rL) * m.c_t;
-                const double a0 = IMPL ? a1 + a2 + a3 + a4 + FbE - FbW + 0.5 * (FnS - FsS) + tterm
-                                       : a1 + a2 + a3 + a4 + tterm;
-                const double b = (Fc.R1[lc] + Fc.R1[lc - 1]) * m.c_t * u1c
-                               + k.B * (gcN * (Ra.V[lc] - Ra.V[lc - 1]) - gcP * (R0.V[lc] - R0.V[lc - 1])
-                                        - 2.0 / 3.0 * gR * (Ra.V[lc] - R0.V[lc])
-                                        + 2.0 / 3.0 * gL * (Ra.V[lc - 1] - R0.V[lc - 1]))
-                               + k.g_x * (rR + rL) * m.half_dV;
-                const double r = rcp(a0);
-                uhat = (a1 * R0.U[lc - 1] + a2 * R0.U[lc + 1] + a3 * uS + a4 * uN + b + uec) * r;
-                du = m.A_dy * r;
-            }
-            s.UH[lc] = uhat;
-            s.DU[lc] = du;
-        }
-        // v-eq at v-face (i, j+1)
-        double vhatN = 0.0, dvN = 0.0;
-        if (vkind(kw1) == FK_ACTIVE) {
-            const double rB = rP, rT = Ra.R[lc], gB = gP, gT = Ra.G[lc];
-            const double gadj = 0.5 * (gB + gT);
-            const double zeta = 1.1466 * k.Kn * rcp(0.5 * (rB + rT));
-            double a1, a2, vW, vE, FwS = 0.0, FeS = 0.0;
-            if (ckind(R0.KK[lc - 1]) == CK_SOLID && ckind(Ra.KK[lc - 1]) == CK_SOLID) {
-                a1 = k.B * gadj * dy * rcp(0.5 * dx + zeta); vW = 0.0;
-            } else { a1 = xvW; FwS = FwSum; vW = Ra.V[lc - 1]; }
-            if (ckind(R0.KK[lc + 1]) == CK_SOLID && ckind(Ra.KK[lc + 1]) == CK_SOLID) {
-                a2 = k.B * gadj * dy * rcp(0.5 * dx + zeta); vE = 0.0;
-            } else { a2 = s.XVE[lc + 1]; FeS = s.XVF[lc + 1]; vE = Ra.V[lc + 1]; }
-            const double a3 = vcS, a4 = vcN;
-            const double tterm = (rT + rB) * m.c_t;
-            const double a0 = IMPL ? a1 + a2 + a3 + a4 + 0.5 * (FeS - FwS) + FbN - FbS + tterm
-                                   : a1 + a2 + a3 + a4 + tterm;
-            const double b = (Fn.R1[lc] + Fc.R1[lc]) * m.c_t * v1n
-                           + k.B * (s.GC[lc + 1] * (Ra.U[lc + 1] - R0.U[lc + 1]) - gcN * (Ra.U[lc] - R0.U[lc])
-                                    - 2.0 / 3.0 * gT * (Ra.U[lc + 1] - Ra.U[lc])
-                                    + 2.0 / 3.0 * gB * (R0.U[lc + 1] - R0.U[lc]))
-                           + k.g_y * (rT + rB) * m.half_dV;
-            const double r = rcp(a0);
-            vhatN = (a1 * vW + a2 * vE + a3 * R0.V[lc] + a4 * Rb.V[lc] + b + ven) * r;
-            dvN = m.A_dx * r;
-        }
+        if (reg) stage_C<IMPL, TVD, true>(s, m, lc, Rm, R0, Ra, Rb, Fc, Fn, nm, c, v);
+        else stage_C<IMPL, TVD, false>(s, m, lc, Rm, R0, Ra, Rb, Fc, Fn, nm, c, v);
         __syncthreads();                                    // B2
-
-        // ================= stage D: p_{i,j} (Eqs. pl23-pl24) =================
-        double pn = R0.P[lc];
-        if (ckind(kw0) == CK_FLUID) {
-            double apW = 0.0, apE = 0.0, apS = 0.0, apN = 0.0, bpW = 0.0, bpE = 0.0, bpS = 0.0, bpN = 0.0, sum = 0.0;
-            const uint8_t kwf = ukind(kw0), kef = ukind(R0.KK[lc + 1]);
-            if (kwf == FK_ACTIVE) {
-                const double r = Fc.RU[lc];
-                apW = r * du * dy; bpW = r * uhat * dy; sum += apW * R0.P[lc - 1];
-            } else if (kwf == FK_INLET) bpW = Fc.RU[lc] * k.u_in * dy;
-            if (kef == FK_ACTIVE) {
-                const double r = Fc.RU[lc + 1];
-                apE = r * s.DU[lc + 1] * dy; bpE = r * s.UH[lc + 1] * dy; sum += apE * R0.P[lc + 1];
-            } else if (kef == FK_OUTLET) bpE = Fc.RU[lc + 1] * R0.U[lc] * dy;
-            if (vkind(kw0) == FK_ACTIVE) {
-                const double r = Fc.RV[lc];
-                apS = r * dvP * dx; bpS = r * vhatP * dx; sum += apS * Rm.P[lc];
-            }
-            if (vkind(kw1) == FK_ACTIVE) {
-                const double r = Fn.RV[lc];
-                apN = r * dvN * dx; bpN = r * vhatN * dx; sum += apN * Ra.P[lc];
-            }
-            const double a0 = m.dV * rcp(TN) + (apW + apE + apS + apN) * dt;
-            const double bp = Fc.R1[lc] * m.dV - (bpE - bpW + bpN - bpS) * dt;
-            pn = (sum * dt + bp) * rcp(a0);
-        }
-        s.PN[lc] = pn;
+        if (reg) stage_D<true>(s, m, lc, Rm, R0, Ra, Fc, Fn, c, v);
+        else stage_D<false>(s, m, lc, Rm, R0, Ra, Fc, Fn, c, v);
         __syncthreads();                                    // B3
-
-        // ================= stage E: corrections, writes, residuals =================
-        if (out_row && owner) {
-            const long long id = gidx(k, gi, j);
-            if (ckind(kw0) == CK_FLUID) {
-                k.T_w[id] = TN;
-                k.p_w[id] = pn;
-                r_dT = nmax(r_dT, fabs(TN - R0.T[lc]));
-                r_dp = nmax(r_dp, fabs(pn - R0.P[lc]));
-                r_T = nmax(r_T, fabs(TN));
-                r_p = nmax(r_p, fabs(pn));
-                if (!(TN > 0.0) || !(pn > 0.0) || !isfinite(TN) || !isfinite(pn)) {
-                    const long long flat = (long long)j * k.nx + gi;
-                    if (bad < 0 || flat < bad) { bad = flat; badf = (!(TN > 0.0) || !isfinite(TN)) ? 3 : 2; }
-                }
-            }
-            const uint8_t ku = ukind(kw0);
-            double un;
-            if (ku == FK_ACTIVE) {
-                un = uhat - du * (pn - s.PN[lc - 1]);
-                r_du = nmax(r_du, fabs(un - R0.U[lc]));
-                r_vel = nmax(r_vel, fabs(un));
-            } else if (ku == FK_INLET) un = k.u_in;
-            else un = 0.0;
-            k.u_w[id] = un;
-            if (gi == k.nx - 1 && k.xbc == 0) k.u_w[id + 1] = R0.U[lc];   // outlet face (BC spec 3)
-            double vn = 0.0;
-            if (vkind(kw0) == FK_ACTIVE) {
-                vn = vhatP - dvP * (pn - pnP);
-                r_dv = nmax(r_dv, fabs(vn - R0.V[lc]));
-                r_vel = nmax(r_vel, fabs(vn));
-            }
-            k.v_w[id] = vn;
-            if (k.xbc == 0) {
-                if (gi == k.nx - 1) {
-                    const double pv = ckind(kw0) == CK_FLUID ? pn : R0.P[lc];
-                    const double Tv = ckind(kw0) == CK_FLUID ? TN : R0.T[lc];
-                    for (int g = 1; g <= OFF - 1; g++) { k.p_w[id + g] = pv; k.T_w[id + g] = Tv; k.v_w[id + g] = vn; }
-                }
-            } else if (k.mirror) {
-                int tgt = -1000;
-                if (gi < OFF) tgt = gi + k.nx;
-                else if (gi >= k.nx - OFF) tgt = gi - k.nx;
-                if (tgt > -1000) {
-                    const long long tt = gidx(k, tgt, j);
-                    if (ckind(kw0) == CK_FLUID) { k.p_w[tt] = pn; k.T_w[tt] = TN; }
-                    k.u_w[tt] = un;
-                    k.v_w[tt] = vn;
-                }
-            }
+        if (j >= J0 && owner) {
+            if (reg) stage_E<true>(s, m, lc, gi, j, R0, c, v, rs);
+            else stage_E<false>(s, m, lc, gi, j, R0, c, v, rs);
         }
         // ---- carry row j+1 quantities to the next step
-        ytS = ytSn; FS = Fy1;
-        utS = utSn; FsSum = FsSumN;
-        vcS = vcSn; FbS = FbN;
-        vhatP = vhatN; dvP = dvN;
-        pnP = pn; gcP = gcN;
-        p1n = p1nn; T1c = T1n; T1n = T1nn; u1c = u1n; v1n = v1nn;
-        if (!IMPL) { Tec = Ten; uec = uen; ven = vem; }
+        c.ytS = v.ytSn; c.FS = v.Fy1;
+        c.utS = v.utSn; c.FsSum = v.FsSumN;
+        c.vcS = v.vcSn; c.FbS = v.FbN;
+        c.vhatP = v.vhatN; c.dvP = v.dvN;
+        c.pnP = v.pn; c.gcP = v.gcN;
+        nm.p1n = p1nn; nm.T1c = nm.T1n; nm.T1n = T1nn; nm.u1c = u1n; nm.v1n = v1nn;
+        if (!IMPL) { nm.Tec = Ten; nm.uec = uen; nm.ven = vem; }
         sj = sa;
     }
     cp_wait_all();
-    double vals[7] = {r_du, r_dv, r_dp, r_dT, r_vel, r_p, r_T};
+    double vals[7] = {rs.du, rs.dv, rs.dp, rs.dT, rs.vel, rs.p, rs.T};
     __syncthreads();
-    // reuse the v1 block reduction (NT = 256 there; here MX = 128 threads -> 4 warps)
     __shared__ double part[MX / 32][8];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int q = 0; q < 7; q++) {
-        double v = vals[q];
-        const bool isn = v != v;
+        double val = vals[q];
+        const bool isn = val != val;
         const unsigned nanmask = __ballot_sync(0xffffffffu, isn);
-        v = warp_max(isn ? 0.0 : v);
-        if (nanmask) v = __longlong_as_double(0x7ff8000000000000LL);
-        if (lane == 0) part[wid][q] = v;
+        val = warp_max(isn ? 0.0 : val);
+        if (nanmask) val = __longlong_as_double(0x7ff8000000000000LL);
+        if (lane == 0) part[wid][q] = val;
     }
     __syncthreads();
     if (threadIdx.x < 7) {
-        double v = 0.0;
-        for (int w = 0; w < MX / 32; w++) v = nmax(v, part[w][threadIdx.x]);
-        atomicMax(&k.red[threadIdx.x], (unsigned long long)__double_as_longlong(v));
+        double val = 0.0;
+        for (int w = 0; w < MX / 32; w++) val = nmax(val, part[w][threadIdx.x]);
+        atomicMax(&k.red[threadIdx.x], (unsigned long long)__double_as_longlong(val));
     }
-    if (bad >= 0) {
-        atomicMax(&k.red[7], 0x7fffffffffffffffULL - (unsigned long long)bad);
-        k.red[8] = (unsigned long long)badf;
+    if (rs.bad >= 0) {
+        atomicMax(&k.red[7], 0x7fffffffffffffffULL - (unsigned long long)rs.bad);
+        k.red[8] = (unsigned long long)rs.badf;
     }
 }
 
