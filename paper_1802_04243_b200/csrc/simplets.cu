@@ -9,6 +9,7 @@
 #include "../../include/simplets.h"
 #include "sts_kernels.cuh"
 #include "sts_march.cuh"
+#include "sts_conv.cuh"
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -247,6 +248,7 @@ static march_fn march_table(int impl, int tvd)
     if (impl) return tvd ? march_kernel<true, true> : march_kernel<true, false>;
     return tvd ? march_kernel<false, true> : march_kernel<false, false>;
 }
+static march_fn conv_march_table(int tvd) { return tvd ? conv_march_kernel<true> : conv_march_kernel<false>; }
 
 static sts_status set_smem_attrs(sts_ctx* ctx)
 {
@@ -258,6 +260,9 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
     march_fn mfs[4] = {march_table(0, 0), march_table(0, 1), march_table(1, 0), march_table(1, 1)};
     for (march_fn f : mfs)
         CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));
+    for (int tvd = 0; tvd < 2; tvd++)
+        CU(cudaFuncSetAttribute((const void*)conv_march_table(tvd), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(ConvSmem)));
     done = true;
     return STS_OK;
 }
@@ -948,9 +953,14 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 sts_ctx* c = cs[r];
                 Params k = base(c, r);
                 k.ue_w = c->ue; k.ve_w = c->ve; k.Te_w = c->Te;
-                const dim3 grid((c->nloc + TX - 1) / TX, (c->ny + TY - 1) / TY);
                 prof_begin(c, 1);
-                conv_table(tvd)<<<grid, NT, smem, st>>>(k);
+                if (c->use_tile) {
+                    const dim3 grid((c->nloc + TX - 1) / TX, (c->ny + TY - 1) / TY);
+                    conv_table(tvd)<<<grid, NT, smem, st>>>(k);
+                } else {
+                    const dim3 mgrid(c->march_nstrips * c->march_nseg);
+                    conv_march_table(tvd)<<<mgrid, MX, sizeof(ConvSmem), st>>>(make_march(c, k));
+                }
                 prof_end(c);
                 c->launches++;
                 CU(cudaGetLastError());

@@ -253,8 +253,9 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             double ps = 0.0;
             if (IMPL && TVD && cF<REG>(R0.KK[lc - 2]) && cF<REG>(kl) && cF<REG>(kw0) && cF<REG>(R0.KK[lc + 1]))
                 ps = psi_f(R0.T[lc - 2], R0.T[lc - 1], R0.T[lc], R0.T[lc + 1], R0.U[lc]);
+            // max(0,-F) = max(0,F) - F: the E-side coefficient is the W-side one minus F
             pw = (IMPL ? max0(F) - F * ps : 0.0) + D;
-            pe = (IMPL ? max0(-F) - F * ps : 0.0) + D;
+            pe = IMPL ? pw - F : pw;
         }
         s.XTW[lc] = pw;
         s.XTE[lc] = pe;
@@ -269,8 +270,8 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         double ps = 0.0;
         if (IMPL && TVD && cF<REG>(Rm.KK[lc]) && cF<REG>(kw0) && cF<REG>(kw1) && cF<REG>(Rb.KK[lc]))
             ps = psi_f(Rm.T[lc], R0.T[lc], Ra.T[lc], Rb.T[lc], Ra.V[lc]);
-        v.ytN = (IMPL ? max0(-F) - F * ps : 0.0) + D;
         v.ytSn = (IMPL ? max0(F) - F * ps : 0.0) + D;
+        v.ytN = IMPL ? v.ytSn - F : v.ytSn;
     }
     // u-eq x pieces of cell (i, j): a^u_2 of face i, a^u_1 of face i+1 (transposed pl15)
     {
@@ -283,8 +284,8 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             if (IMPL && TVD && uA<REG>(R0.KK[lc - 1]) && uA<REG>(kw0) && uA<REG>(R0.KK[lc + 1]) &&
                 uA<REG>(R0.KK[lc + 2]))
                 ps = psi_f(R0.U[lc - 1], R0.U[lc], R0.U[lc + 1], R0.U[lc + 2], ub);
-            xe = (IMPL ? max0(-Fb) - Fb * ps : 0.0) + D;
             xw = (IMPL ? max0(Fb) - Fb * ps : 0.0) + D;
+            xe = IMPL ? xw - Fb : xw;
         }
         s.XUE[lc] = xe;
         s.XUW[lc] = xw;
@@ -309,8 +310,8 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         double ps = 0.0;
         if (IMPL && TVD && vA<REG>(kw0) && vA<REG>(kw1) && vA<REG>(Rb.KK[lc]) && vA<REG>(Rc.KK[lc]))
             ps = psi_f(R0.V[lc], Ra.V[lc], Rb.V[lc], Rc.V[lc], vb);
-        v.vcN = (IMPL ? max0(-v.FbN) - v.FbN * ps : 0.0) + D;
         v.vcSn = (IMPL ? max0(v.FbN) - v.FbN * ps : 0.0) + D;
+        v.vcN = IMPL ? v.vcSn - v.FbN : v.vcSn;
     }
     // corner Gamma at (x^f_i, y^f_{j+1}) (R4, R5; BC spec 8)
     if (REG) {
@@ -337,9 +338,9 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             p2 = psi_f(f1, f2, f3, f4, R0.U[lc]);
         }
         const double D = m.B_dydx * v.gcN;
-        v.xvW = (IMPL ? 0.5 * (max0(F1) - F1 * p1 + max0(F2) - F2 * p2) : 0.0) + D;
-        s.XVE[lc] = (IMPL ? 0.5 * (max0(-F1) - F1 * p1 + max0(-F2) - F2 * p2) : 0.0) + D;
         v.FwSum = F1 + F2;
+        v.xvW = (IMPL ? 0.5 * (max0(F1) - F1 * p1 + max0(F2) - F2 * p2) : 0.0) + D;
+        s.XVE[lc] = IMPL ? v.xvW - 0.5 * v.FwSum : v.xvW;
         s.XVF[lc] = v.FwSum;
     }
 }
@@ -401,9 +402,9 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         // N tangential link pieces at y^f_{j+1} (both sides; the S side is carried)
         const double F1 = v.Fy1, F2 = Fn.FY[lc - 1];
         const double D = m.B_dxdy * v.gcN;
-        const double a4p = (IMPL ? 0.5 * (max0(-F1) - F1 * v.upsi1 + max0(-F2) - F2 * v.upsi2) : 0.0) + D;
-        v.utSn = (IMPL ? 0.5 * (max0(F1) - F1 * v.upsi1 + max0(F2) - F2 * v.upsi2) : 0.0) + D;
         v.FsSumN = F1 + F2;
+        v.utSn = (IMPL ? 0.5 * (max0(F1) - F1 * v.upsi1 + max0(F2) - F2 * v.upsi2) : 0.0) + D;
+        const double a4p = IMPL ? v.utSn - 0.5 * v.FsSumN : v.utSn;
         double uhat = 0.0, du = 0.0;
         if (uA<REG>(kw0)) {
             const double rL = R0.R[lc - 1], rR = rP, gL = R0.G[lc - 1], gR = gP;

@@ -92,10 +92,12 @@ def test_segments_bitwise(S, seg):
         assert np.array_equal(ref[f], g.get_field(f)), f
 
 
-def test_tile_kernel_agrees(S, oracle_mod):
-    """The v1 2-D tile kernel (STS_KERNEL=tile) and the y-march kernel agree to the
-    parity tolerance (different reciprocal arithmetic, same discrete spec)."""
-    case = W.c1("implicit_upwind", passes=10)
+@pytest.mark.parametrize("variant", list(W.VARIANTS))
+def test_tile_kernel_agrees(S, oracle_mod, variant):
+    """The v1 2-D tile kernels (STS_KERNEL=tile: pass_kernel, conv_kernel) and the
+    y-march kernels (march_kernel, conv_march_kernel) agree to the parity tolerance
+    (different reciprocal arithmetic, same discrete spec)."""
+    case = W.c1(variant, passes=10)
     a = S.Solver(case)
     os.environ["STS_KERNEL"] = "tile"
     try:
