@@ -205,6 +205,22 @@ __global__ void unpack_kernel(int ny_rows, int ncols, int col0_local, int pitch,
     }
 }
 // rho = p / T for the read-back of STS_RHO (Eq. pl5)
+// Owned slab (rows x ncols, row-major) -> local columns [OFF, OFF+ncols) of up to
+// three snapshot arrays; optionally replicate local column `rep_src` into the
+// outlet ghost columns (rep_src+1 .. rep_src+OFF-1) (BC spec 3).
+__global__ void slab_pack_kernel(int rows, int ncols, int pitch, const double* __restrict__ src, double* d0,
+                                 double* d1, double* d2, int rep_src)
+{
+    const long long n = (long long)rows * ncols;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(e / ncols), i = (int)(e - (long long)j * ncols);
+        const double val = src[e];
+        const long long id = (long long)j * pitch + OFF + i;
+        d0[id] = val; d1[id] = val; d2[id] = val;
+        if (rep_src >= 0 && OFF + i == rep_src)
+            for (int g = 1; g < OFF; g++) { d0[id + g] = val; d1[id + g] = val; d2[id + g] = val; }
+    }
+}
 __global__ void ratio_kernel(long long n, const double* __restrict__ p, const double* __restrict__ T, double* __restrict__ r)
 {
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
@@ -271,7 +287,7 @@ static Params make_params(const sts_ctx* c)
 {
     Params k{};
     k.nx = c->nx; k.ny = c->ny; k.gi0 = c->gi0; k.nloc = c->nloc; k.pitch = c->pitch;
-    k.xbc = c->gas.xbc; k.mirror = (is_periodic(c) && c->world == 1) ? 1 : 0;
+    k.xbc = c->gas.xbc; k.mirror = (is_periodic(c) && c->world == 1 && !c->comm) ? 1 : 0;
     k.first_rank = c->rank == 0; k.last_rank = c->rank == c->world - 1;
     k.dx = c->spacing; k.dy = c->spacing; k.dt = c->sch.dt;
     k.A = c->A; k.B = c->B; k.CT1 = c->CT1; k.CT2 = c->CT2; k.CT3 = c->CT3; k.Kn = c->gas.Kn;
@@ -313,7 +329,8 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     int dev_sms = 148, per_sm = 3;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)march_table(1, 1), MX, sizeof(MarchSmem)) == cudaSuccess && nb > 0)
+    const void* fn = (const void*)march_table(c->sch.time == STS_IMPLICIT, c->sch.space == STS_TVD_VANLEER);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, MX, sizeof(MarchSmem)) == cudaSuccess && nb > 0)
         per_sm = nb;
     const int strips = (c->nloc + MW - 1) / MW;
     const int slots = dev_sms * per_sm;
@@ -446,15 +463,20 @@ static sts_status halo_nccl(sts_ctx* ctx)
 {
     const int per = halo_per(ctx);
     const int left = left_of(ctx), right = right_of(ctx);
+    // NCCL matches the messages of one (sender, receiver) pair in issue order.
+    // When the left and right neighbour are the same rank (2-rank ring, or a
+    // periodic single rank talking to itself) every rank must send its RIGHT
+    // strip first and receive into its LEFT ghosts first: a rank's left ghosts
+    // take its left neighbour's right strip.
     if (g_nccl.GroupStart()) return fail(ctx, STS_E_COMM, "ncclGroupStart");
-    if (left >= 0) {
-        if (g_nccl.Send(ctx->halo, per, NCCL_FLOAT64, left, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclSend");
-        if (g_nccl.Recv(ctx->halo + 2 * per, per, NCCL_FLOAT64, left, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclRecv");
-    }
-    if (right >= 0) {
-        if (g_nccl.Send(ctx->halo + per, per, NCCL_FLOAT64, right, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclSend");
-        if (g_nccl.Recv(ctx->halo + 3 * per, per, NCCL_FLOAT64, right, ctx->comm, ctx->stream)) return fail(ctx, STS_E_COMM, "ncclRecv");
-    }
+    if (right >= 0 && g_nccl.Send(ctx->halo + per, per, NCCL_FLOAT64, right, ctx->comm, ctx->stream))
+        return fail(ctx, STS_E_COMM, "ncclSend");
+    if (left >= 0 && g_nccl.Send(ctx->halo, per, NCCL_FLOAT64, left, ctx->comm, ctx->stream))
+        return fail(ctx, STS_E_COMM, "ncclSend");
+    if (left >= 0 && g_nccl.Recv(ctx->halo + 2 * per, per, NCCL_FLOAT64, left, ctx->comm, ctx->stream))
+        return fail(ctx, STS_E_COMM, "ncclRecv");
+    if (right >= 0 && g_nccl.Recv(ctx->halo + 3 * per, per, NCCL_FLOAT64, right, ctx->comm, ctx->stream))
+        return fail(ctx, STS_E_COMM, "ncclRecv");
     if (g_nccl.GroupEnd()) return fail(ctx, STS_E_COMM, "ncclGroupEnd");
     return STS_OK;
 }
@@ -468,7 +490,7 @@ static Snapshot pick(sts_ctx* c, int which)
 }
 static sts_status exchange_group(sts_ctx** cs, int n, const int* which, cudaStream_t st)
 {
-    if (cs[0]->world == 1) return STS_OK;
+    if (cs[0]->world == 1 && !cs[0]->comm) return STS_OK;
     for (int r = 0; r < n; r++) { sts_status e = halo_pack(cs[r], pick(cs[r], which[r]), st); if (e) return e; }
     if (n == 1) {
         sts_status e = halo_nccl(cs[0]);
@@ -589,7 +611,10 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
     ALLOC(ctx->ue, nce); ALLOC(ctx->ve, nve); ALLOC(ctx->Te, nce);
     ctx->stage_elems = (size_t)(nx + 1) * (ny + 1);
     ALLOC(ctx->stage, ctx->stage_elems);
-    if (world > 1) { ctx->halo_elems = (size_t)16 * OFF * (ny + 1); ALLOC(ctx->halo, ctx->halo_elems); }
+    if (world > 1 || (dist && dist->nccl_id && gas->xbc == STS_X_PERIODIC)) {
+        ctx->halo_elems = (size_t)16 * OFF * (ny + 1);
+        ALLOC(ctx->halo, ctx->halo_elems);
+    }
 #undef ALLOC
     if (cudaMalloc(&ctx->ck, nce) != cudaSuccess || cudaMalloc(&ctx->uk, nce) != cudaSuccess || cudaMalloc(&ctx->vk, nve) != cudaSuccess ||
         cudaMalloc(&ctx->red, (size_t)scheme->max_passes * 9 * sizeof(unsigned long long)) != cudaSuccess ||
@@ -636,7 +661,9 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
     }
     if (world > 1 && !dist->nccl_id) {
         ctx->local_group = true;            // slabs of one process, driven by sts_advance_group
-    } else if (world > 1) {
+    } else if (world > 1 || (dist && dist->nccl_id && gas->xbc == STS_X_PERIODIC)) {
+        // NCCL transport; a single periodic rank given an id exchanges its wrapped
+        // halo with itself over ncclSend/ncclRecv (exercises the transport on 1 GPU)
         if (!g_nccl.load()) { sts_destroy(ctx); return fail(nullptr, STS_E_COMM, "libnccl.so.2 not loadable"); }
         nccl_uid id;
         memcpy(&id, dist->nccl_id, 128);
@@ -737,8 +764,28 @@ extern "C" sts_status sts_set_field_device(sts_ctx* ctx, int32_t field, const do
 {
     if (!ctx || !dev) return fail(ctx, STS_E_ARG, "null argument");
     if (field < STS_U || field > STS_T) return fail(ctx, STS_E_ARG, "field not settable");
-    if ((size_t)n != global_size(ctx, field)) return fail(ctx, STS_E_ARG, "wrong buffer size");
-    return pack_into_all(ctx, field, dev);
+    if ((size_t)n == global_size(ctx, field)) return pack_into_all(ctx, field, dev);
+    // this rank's owned slab (sts_shape): owned columns into all snapshots, outlet
+    // ghosts replicated on the last in/outflow rank, then one halo exchange of the
+    // current snapshot so neighbour ghosts are consistent (multi-GPU e2e path)
+    const bool last = ctx->rank == ctx->world - 1;
+    const int rows = field == STS_V ? ctx->ny + 1 : ctx->ny;
+    const int ncols = ctx->nloc + (field == STS_U && last ? 1 : 0);
+    if ((int64_t)rows * ncols != n) return fail(ctx, STS_E_ARG, "wrong buffer size (neither global nor slab shape)");
+    CU(cudaSetDevice(ctx->device));
+    const int rep = (!is_periodic(ctx) && last && field != STS_U) ? OFF + ctx->nloc - 1 : -1;
+    double* d[3];
+    for (int k = 0; k < 3; k++)
+        d[k] = field == STS_U ? ctx->snap[k].u : field == STS_V ? ctx->snap[k].v : field == STS_P ? ctx->snap[k].p : ctx->snap[k].T;
+    slab_pack_kernel<<<592, 256, 0, ctx->stream>>>(rows, ncols, ctx->pitch, dev, d[0], d[1], d[2], rep);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    if (ctx->world > 1 && !ctx->local_group) {
+        const int which = ctx->cur;
+        sts_ctx* one[1] = {ctx};
+        return exchange_group(one, 1, &which, ctx->stream);
+    }
+    return STS_OK;
 }
 
 extern "C" sts_status sts_init_freestream(sts_ctx* ctx)
@@ -905,7 +952,7 @@ static sts_status gather_red(sts_ctx** cs, int n, int it, unsigned long long* ou
 {
     sts_ctx* ctx = cs[0];
     for (int q = 0; q < 9; q++) out[q] = 0;
-    if (n == 1 && ctx->world > 1) {
+    if (n == 1 && ctx->comm) {
         unsigned long long* slot = ctx->red + (size_t)it * 9;
         if (g_nccl.AllReduce(slot, slot, 9, NCCL_UINT64, NCCL_MAX, ctx->comm, st)) return fail(ctx, STS_E_COMM, "ncclAllReduce");
     }

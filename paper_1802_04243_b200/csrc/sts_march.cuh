@@ -36,7 +36,7 @@ namespace sts {
 
 constexpr int MX = 128;          // threads per CTA = columns handled per strip
 constexpr int MW = MX - 3;       // owned columns per strip
-constexpr int RW = MX + 8;       // ring row width (global columns I0-4 .. I0-4+RW)
+constexpr int RW = MX + 4;       // ring row width (global columns I0-4 .. I0-4+RW)
 constexpr int RS = 6;            // ring slots
 constexpr int WARM = 4;          // warm-up rows per segment
 constexpr uint32_t REG_BIT = 1u << 24;   // kind-word bit: the +-3 window is all fluid
@@ -110,14 +110,19 @@ struct RingRow {                 // one old-iterate row (slot-major: one base ad
     double U[RW], V[RW], P[RW], T[RW], R[RW], G[RW];
     uint32_t KK[RW];
 };
-struct FluxRow {                 // face densities / fluxes of one row, (p/T)^{n-1} of that row
-    double RU[RW], FX[RW], RV[RW], FY[RW], R1[RW];
+struct FluxRow {                 // face densities / fluxes of one row
+    double RU[RW], FX[RW], RV[RW], FY[RW];
 };
+// 56.8 KB: four CTAs (16 warps) per SM.  Pieces a neighbour can recompute with
+// the same operations (E-side coefficients = W-side - F, F-bar^x, corner Gamma)
+// are not stored; p_new reuses the T-eq piece row (dead after stage C).
 struct MarchSmem {
     RingRow ring[RS];
     FluxRow fr[2];
-    double XTW[RW], XTE[RW], XUW[RW], XUE[RW], FBX[RW], XVE[RW], XVF[RW], GC[RW];
-    double UH[RW], DU[RW], PN[RW];
+    double R1[RW];               // (p/T)^{n-1} of row j (row j+1 is written in stage E)
+    double XTW[RW];              // T-eq W coefficient of face i (stage C); p_new (stages D-E)
+    double XUW[RW], XVW[RW], XVF[RW];
+    double UH[RW], DU[RW];
 };
 
 __device__ __forceinline__ int slot(int j) { return (j + 4 * RS) % RS; }
@@ -195,6 +200,8 @@ struct StepVars {
     double vcN, vcSn, FbN;        // v-eq normal pieces of cell (i, j+1)
     double gcN;                   // corner Gamma (i, j+1)
     double xvW, FwSum;            // v-eq tangential W piece / flux sum at x^f_i, v-row j+1
+    double xe, Fb;                // u-eq E coefficient of face i / F-bar^x of cell (i, j)
+    double r1n;                   // (p/T)^{n-1} (i, j+1)
     double TN, uhat, du, utSn, FsSumN, vhatN, dvN, pn;
 };
 struct NM1 {                      // n-1 state / explicit planes at this thread's points
@@ -212,8 +219,8 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
 {
     const double dx = m.k.dx, dy = m.k.dy;
     const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
-    // (p/T)^{n-1} of row j+1
-    Fn.R1[lc] = fdiv(nm.p1n, nm.T1n == 0.0 ? 1.0 : nm.T1n);
+    // (p/T)^{n-1} of row j+1 (to shared memory in stage E)
+    v.r1n = fdiv(nm.p1n, nm.T1n == 0.0 ? 1.0 : nm.T1n);
     // F^x, rho^u at u-face (i, j+1)  (Eqs. pl8, pl10, R1)
     {
         double ru = 0.0, F = 0.0;
@@ -243,8 +250,9 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         v.Fy1 = F;
     }
     // T-eq x-face pieces at u-face (i, j): a^T_1 of cell i, a^T_2 of cell i-1 (Eqs. pl31-pl33)
+    // (max(0,-F) = max(0,F) - F: the consumer forms the E-side coefficient as XTW - F)
     {
-        double pw = 0.0, pe = 0.0;
+        double pw = 0.0;
         const uint32_t kl = R0.KK[lc - 1];
         if (!cW<REG>(kl) && !cW<REG>(kw0)) {
             const double F = Fc.FX[lc];
@@ -253,12 +261,9 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             double ps = 0.0;
             if (IMPL && TVD && cF<REG>(R0.KK[lc - 2]) && cF<REG>(kl) && cF<REG>(kw0) && cF<REG>(R0.KK[lc + 1]))
                 ps = psi_f(R0.T[lc - 2], R0.T[lc - 1], R0.T[lc], R0.T[lc + 1], R0.U[lc]);
-            // max(0,-F) = max(0,F) - F: the E-side coefficient is the W-side one minus F
             pw = (IMPL ? max0(F) - F * ps : 0.0) + D;
-            pe = IMPL ? pw - F : pw;
         }
         s.XTW[lc] = pw;
-        s.XTE[lc] = pe;
     }
     // T-eq y-face piece at v-face (i, j+1): a^T_4 of cell (i, j), a^T_3 of cell (i, j+1)
     v.ytN = 0.0;
@@ -287,9 +292,9 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             xw = (IMPL ? max0(Fb) - Fb * ps : 0.0) + D;
             xe = IMPL ? xw - Fb : xw;
         }
-        s.XUE[lc] = xe;
-        s.XUW[lc] = xw;
-        s.FBX[lc] = Fb;
+        s.XUW[lc] = xw;              // a^u_1 of face i+1 (neighbour); a^u_2 and F-bar stay here
+        v.xe = xe;
+        v.Fb = Fb;
     }
     // u-eq tangential psi at (u column i, y^f_{j+1}) (fluxes need the neighbour: stage C)
     v.upsi1 = 0.0;
@@ -325,7 +330,6 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         if (!wallish(ckind(kw1))) { sum += Ra.G[lc]; n++; }
         v.gcN = n == 4 ? 0.25 * sum : (n > 0 ? sum / n : 0.0);
     }
-    s.GC[lc] = v.gcN;
     // v-eq tangential pieces at (u-face column i, v-row j+1): a^v_1 of v-face (i, j+1),
     // a^v_2 of v-face (i-1, j+1)
     {
@@ -340,7 +344,7 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         const double D = m.B_dydx * v.gcN;
         v.FwSum = F1 + F2;
         v.xvW = (IMPL ? 0.5 * (max0(F1) - F1 * p1 + max0(F2) - F2 * p2) : 0.0) + D;
-        s.XVE[lc] = IMPL ? v.xvW - 0.5 * v.FwSum : v.xvW;
+        s.XVW[lc] = v.xvW;           // the E side of v-face (i-1, j+1) is XVW - XVF/2
         s.XVF[lc] = v.FwSum;
     }
 }
@@ -362,7 +366,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         double a1, a2, a3, a4, T1, T2, T3, T4, FW, FE, FSl, FNl;
         if (REG) {
             a1 = s.XTW[lc]; FW = Fc.FX[lc]; T1 = R0.T[lc - 1];
-            a2 = s.XTE[lc + 1]; FE = Fc.FX[lc + 1]; T2 = R0.T[lc + 1];
+            FE = Fc.FX[lc + 1]; a2 = IMPL ? s.XTW[lc + 1] - FE : s.XTW[lc + 1]; T2 = R0.T[lc + 1];
             a3 = c.ytS; FSl = c.FS; T3 = Rm.T[lc];
             a4 = v.ytN; FNl = v.Fy1; T4 = Ra.T[lc];
         } else {
@@ -373,7 +377,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
             else { a1 = s.XTW[lc]; FW = Fc.FX[lc]; T1 = R0.T[lc - 1]; }
             kn = ckind(R0.KK[lc + 1]);
             if (wallish(kn)) { a2 = k.CT1 * gP * dy * rcp(0.5 * dx + tau); T2 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { a2 = s.XTE[lc + 1]; FE = Fc.FX[lc + 1]; T2 = R0.T[lc + 1]; }
+            else { FE = Fc.FX[lc + 1]; a2 = IMPL ? s.XTW[lc + 1] - FE : s.XTW[lc + 1]; T2 = R0.T[lc + 1]; }
             kn = ckind(Rm.KK[lc]);
             if (wallish(kn)) { a3 = k.CT1 * gP * dx * rcp(0.5 * dy + tau); T3 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
             else { a3 = c.ytS; FSl = c.FS; T3 = Rm.T[lc]; }
@@ -394,7 +398,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         const double div = dudx + dvdy;
         const double Sc = (k.CT2 * gP * (2.0 * (dudx * dudx + dvdy * dvdy) + shear * shear - 2.0 / 3.0 * div * div)
                            + k.pw_sign * k.CT3 * R0.P[lc] * div) * m.dV;
-        const double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + Sc + nm.Tec) + Fc.R1[lc] * nm.T1c * m.dV;
+        const double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + Sc + nm.Tec) + s.R1[lc] * nm.T1c * m.dV;
         v.TN = rhs * rcp(a0);
     }
     // ---- u pseudo-velocity at u-face (i, j)
@@ -408,8 +412,9 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         double uhat = 0.0, du = 0.0;
         if (uA<REG>(kw0)) {
             const double rL = R0.R[lc - 1], rR = rP, gL = R0.G[lc - 1], gR = gP;
-            const double a1 = s.XUW[lc - 1], a2 = s.XUE[lc];
-            const double FbW = s.FBX[lc - 1], FbE = s.FBX[lc];
+            const double a1 = s.XUW[lc - 1], a2 = v.xe;
+            // F-bar^x of cell i-1, recomputed with the same operations as its owner
+            const double FbW = rL * (0.5 * (R0.U[lc - 1] + R0.U[lc])) * dy, FbE = v.Fb;
             double a3, a4, uS, uN, FsS, FnS;
             if (REG) {
                 a3 = c.utS; FsS = c.FsSum; uS = Rm.U[lc];
@@ -430,7 +435,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
             const double tterm = (rR + rL) * m.c_t;
             const double a0 = IMPL ? a1 + a2 + a3 + a4 + FbE - FbW + 0.5 * (FnS - FsS) + tterm
                                    : a1 + a2 + a3 + a4 + tterm;
-            const double b = (Fc.R1[lc] + Fc.R1[lc - 1]) * m.c_t * nm.u1c
+            const double b = (s.R1[lc] + s.R1[lc - 1]) * m.c_t * nm.u1c
                            + k.B * (v.gcN * (Ra.V[lc] - Ra.V[lc - 1]) - c.gcP * (R0.V[lc] - R0.V[lc - 1])
                                     - 2.0 / 3.0 * gR * (Ra.V[lc] - R0.V[lc])
                                     + 2.0 / 3.0 * gL * (Ra.V[lc - 1] - R0.V[lc - 1]))
@@ -452,7 +457,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         double a1, a2, vW, vE, FwS, FeS;
         if (REG) {
             a1 = v.xvW; FwS = v.FwSum; vW = Ra.V[lc - 1];
-            a2 = s.XVE[lc + 1]; FeS = s.XVF[lc + 1]; vE = Ra.V[lc + 1];
+            FeS = s.XVF[lc + 1]; a2 = IMPL ? s.XVW[lc + 1] - 0.5 * FeS : s.XVW[lc + 1]; vE = Ra.V[lc + 1];
         } else {
             FwS = FeS = 0.0;
             const double gadj = 0.5 * (gB + gT);
@@ -462,14 +467,27 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
             } else { a1 = v.xvW; FwS = v.FwSum; vW = Ra.V[lc - 1]; }
             if (ckind(R0.KK[lc + 1]) == CK_SOLID && ckind(Ra.KK[lc + 1]) == CK_SOLID) {
                 a2 = k.B * gadj * dy * rcp(0.5 * dx + zeta); vE = 0.0;
-            } else { a2 = s.XVE[lc + 1]; FeS = s.XVF[lc + 1]; vE = Ra.V[lc + 1]; }
+            } else { FeS = s.XVF[lc + 1]; a2 = IMPL ? s.XVW[lc + 1] - 0.5 * FeS : s.XVW[lc + 1]; vE = Ra.V[lc + 1]; }
+        }
+        // corner Gamma (i+1, j+1), recomputed with the same operations as its owner
+        double gcE;
+        if (REG) {
+            gcE = 0.25 * (R0.G[lc] + R0.G[lc + 1] + Ra.G[lc] + Ra.G[lc + 1]);
+        } else {
+            double sum = 0.0;
+            int n = 0;
+            if (!wallish(ckind(R0.KK[lc]))) { sum += R0.G[lc]; n++; }
+            if (!wallish(ckind(R0.KK[lc + 1]))) { sum += R0.G[lc + 1]; n++; }
+            if (!wallish(ckind(Ra.KK[lc]))) { sum += Ra.G[lc]; n++; }
+            if (!wallish(ckind(Ra.KK[lc + 1]))) { sum += Ra.G[lc + 1]; n++; }
+            gcE = n == 4 ? 0.25 * sum : (n > 0 ? sum / n : 0.0);
         }
         const double a3 = c.vcS, a4 = v.vcN;
         const double tterm = (rT + rB) * m.c_t;
         const double a0 = IMPL ? a1 + a2 + a3 + a4 + 0.5 * (FeS - FwS) + v.FbN - c.FbS + tterm
                                : a1 + a2 + a3 + a4 + tterm;
-        const double b = (Fn.R1[lc] + Fc.R1[lc]) * m.c_t * nm.v1n
-                       + k.B * (s.GC[lc + 1] * (Ra.U[lc + 1] - R0.U[lc + 1]) - v.gcN * (Ra.U[lc] - R0.U[lc])
+        const double b = (v.r1n + s.R1[lc]) * m.c_t * nm.v1n
+                       + k.B * (gcE * (Ra.U[lc + 1] - R0.U[lc + 1]) - v.gcN * (Ra.U[lc] - R0.U[lc])
                                 - 2.0 / 3.0 * gT * (Ra.U[lc + 1] - Ra.U[lc])
                                 + 2.0 / 3.0 * gB * (R0.U[lc + 1] - R0.U[lc]))
                        + k.g_y * (rT + rB) * m.half_dV;
@@ -518,11 +536,11 @@ __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int 
             }
         }
         const double a0 = m.dV * rcp(v.TN) + (apW + apE + apS + apN) * dt;
-        const double bp = Fc.R1[lc] * m.dV - (bpE - bpW + bpN - bpS) * dt;
+        const double bp = s.R1[lc] * m.dV - (bpE - bpW + bpN - bpS) * dt;
         pn = (sum * dt + bp) * rcp(a0);
     }
     v.pn = pn;
-    s.PN[lc] = pn;
+    s.XTW[lc] = pn;                  // p_new row (the T-eq piece row is dead after stage C)
 }
 
 struct Resid { double du, dv, dp, dT, vel, p, T; long long bad; int badf; };
@@ -550,7 +568,7 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
     }
     double un = 0.0;
     if (uA<REG>(kw0)) {
-        un = v.uhat - v.du * (v.pn - s.PN[lc - 1]);
+        un = v.uhat - v.du * (v.pn - s.XTW[lc - 1]);     // XTW holds p_new in stage E
         rs.du = nmax(rs.du, fabs(un - R0.U[lc]));
         rs.vel = nmax(rs.vel, fabs(un));
     } else if (ukind(kw0) == FK_INLET) un = k.u_in;
@@ -582,7 +600,7 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
 }
 
 template <bool IMPL, bool TVD>
-__global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
+__global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MarchSmem& s = *reinterpret_cast<MarchSmem*>(smem_raw);
@@ -663,6 +681,7 @@ __global__ void __launch_bounds__(MX, 3) march_kernel(MarchParams m)
             if (reg) stage_E<true>(s, m, lc, gi, j, R0, c, v, rs);
             else stage_E<false>(s, m, lc, gi, j, R0, c, v, rs);
         }
+        s.R1[lc] = v.r1n;                                   // (p/T)^{n-1} of row j+1 for step j+1
         // ---- carry row j+1 quantities to the next step
         c.ytS = v.ytSn; c.FS = v.Fy1;
         c.utS = v.utSn; c.FsSum = v.FsSumN;

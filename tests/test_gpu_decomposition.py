@@ -71,6 +71,28 @@ def test_slabs_periodic_bitwise(S):
         assert np.array_equal(a, got[f]), f
 
 
+@pytest.mark.parametrize("variant", ["implicit_tvd", "explicit_tvd"])
+def test_nccl_transport_self_ring(S, variant):
+    """The real NCCL path on one GPU: a periodic single rank given an NCCL id
+    exchanges its wrapped halo with itself through halo_pack -> ncclSend/ncclRecv
+    (right strip first, left ghosts first) -> halo_unpack, and reduces the residual
+    with ncclAllReduce(MAX), instead of writing the wrapped ghosts in-kernel.  The
+    result must equal the in-kernel path bit for bit."""
+    case = W.c2(small=True, variant=variant, passes=4)
+    a = S.Solver(case)
+    b = S.Solver(case, nccl_id=S.nccl_unique_id())
+    noise = W.perturbation(case, 9)
+    st = W.perturbed_state({f: a.get_field(f) for f in FIELDS}, noise, vscale=0.01)
+    for g in (a, b):
+        for f in ("p", "T", "u", "v"):
+            g.set_field(f, st[f])
+    _, sa = a.advance(3)
+    _, sb = b.advance(3)
+    for f in FIELDS:
+        assert np.array_equal(a.get_field(f), b.get_field(f)), f
+    assert sa["res"] == sb["res"]
+
+
 @pytest.mark.parametrize("seg", ["3", "5", "17"])
 def test_segments_bitwise(S, seg):
     """The y-march segmentation (warm-up rows) does not change a single bit."""
