@@ -121,6 +121,25 @@ typedef struct {
 
 typedef struct sts_ctx sts_ctx;
 
+/* Host-only decomposition plan of one rank (no CUDA call):
+ * the channel is cut into `world` slabs of near-equal width along x
+ * (remainder to the low ranks).  Rank `rank` owns global columns [i0, i1)
+ * and stores `pitch` local columns, local column l <-> global column
+ * i0 - ghost + l (periodic: mod nx).  After every pass it sends its first /
+ * last `ghost` owned columns to the left / right neighbour (-1: physical
+ * boundary) and receives the unwrapped global columns recv_left /
+ * recv_right into its ghost columns.  kinds (optional, 3 x (ny+1) x pitch
+ * bytes): cell kinds (0 fluid, 1 solid, 2 inlet ghost, 3 outlet ghost,
+ * 4 beyond a wall), u-face kinds, v-face kinds (0 active, 1 fixed 0,
+ * 2 inlet, 3 outlet, 4 wall, 5 none) of the stored columns. */
+typedef struct {
+    int32_t nx, ny, i0, i1, pitch, ghost, left, right;
+    int32_t send_left[2], send_right[2], recv_left[2], recv_right[2];
+} sts_plan_info;
+sts_status sts_plan(const sts_grid* grid, const sts_square* squares, int32_t n_squares,
+                    const sts_gas* gas, int32_t world, int32_t rank, sts_plan_info* out,
+                    uint8_t* kinds);
+
 /* Build the case: validates and snaps the geometry (integer cells), builds
  * the cell / u-face / v-face kind maps (DESIGN 3.5), derives the Eq. pl37
  * constants, allocates three device snapshots (n-1, old, new) of u, v, p, T

@@ -520,6 +520,94 @@ extern "C" sts_status sts_nccl_unique_id(void* out128)
     return STS_OK;
 }
 
+// Host-only planning, no CUDA call: geometry validation and snapping to
+// integer cells, the global solid map, the slab decomposition along x and the
+// local cell / u-face / v-face kind maps of this rank (DESIGN 3.5, 7).
+// Used by sts_create and by sts_plan (the CPU-testable decomposition).
+static sts_status plan_host(const sts_grid* grid, const sts_square* squares, int32_t n_squares, const sts_gas* gas,
+                            int world, int rank, sts_ctx* ctx)
+{
+    if (!(grid->spacing > 0) || !(grid->length_x > 0) || !(grid->length_y > 0)) return fail(nullptr, STS_E_CONFIG, "non-positive grid");
+    double fx = grid->length_x / grid->spacing, fy = grid->length_y / grid->spacing;
+    int nx = (int)llround(fx), ny = (int)llround(fy);
+    if (std::fabs(fx - nx) > 1e-9 || std::fabs(fy - ny) > 1e-9 || nx < 1 || ny < 1)
+        return fail(nullptr, STS_E_CONFIG, "channel lengths are not multiples of the spacing");
+    if (!(gas->Kn > 0)) return fail(nullptr, STS_E_CONFIG, "Kn must be > 0");
+    if (!(gas->pw_sign == 1.0 || gas->pw_sign == -1.0)) return fail(nullptr, STS_E_CONFIG, "pw_sign must be +1 or -1");
+    if (gas->xbc != STS_X_INFLOW_OUTFLOW && gas->xbc != STS_X_PERIODIC) return fail(nullptr, STS_E_ARG, "bad xbc");
+    if (!(gas->p_in > 0) || !(gas->T_in > 0)) return fail(nullptr, STS_E_CONFIG, "inflow state must be positive");
+    if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, STS_E_ARG, "bad rank/world");
+    std::vector<uint8_t> solid((size_t)nx * ny, 0);
+    for (int s = 0; s < n_squares; s++) {
+        const sts_square& q = squares[s];
+        if (q.ni < 1 || q.nj < 1 || q.i0 < 0 || q.j0 < 0 || q.i0 + q.ni > nx || q.j0 + q.nj > ny)
+            return fail(nullptr, STS_E_CONFIG, "square outside the channel");
+        if (gas->xbc == STS_X_INFLOW_OUTFLOW && (q.i0 < 1 || q.i0 + q.ni > nx - 1))
+            return fail(nullptr, STS_E_CONFIG, "square must leave a fluid column at the inlet and outlet");
+        for (int j = q.j0; j < q.j0 + q.nj; j++)
+            for (int i = q.i0; i < q.i0 + q.ni; i++) solid[(size_t)j * nx + i] = 1;
+    }
+    ctx->nx = nx; ctx->ny = ny; ctx->spacing = grid->spacing;
+    ctx->gas = *gas;
+    ctx->squares.assign(squares, squares + n_squares);
+    ctx->h_solid = solid;
+    ctx->rank = rank; ctx->world = world;
+    // slab decomposition along x: near-equal, remainder to the low ranks
+    ctx->col_start.resize(world + 1);
+    for (int r = 0, acc = 0; r <= world; r++) {
+        ctx->col_start[r] = acc;
+        if (r < world) acc += nx / world + (r < nx % world ? 1 : 0);
+    }
+    ctx->gi0 = ctx->col_start[rank];
+    ctx->nloc = ctx->col_start[rank + 1] - ctx->gi0;
+    if (world > 1 && ctx->nloc < OFF) return fail(nullptr, STS_E_CONFIG, "slab narrower than the halo");
+    ctx->pitch = ((ctx->nloc + 2 * OFF + 1) + 15) / 16 * 16;
+    // kind maps of the stored local columns [gi0-OFF, gi0-OFF+pitch)
+    const size_t nce = (size_t)ctx->pitch * ny, nve = (size_t)ctx->pitch * (ny + 1);
+    ctx->h_ck.assign(nce, CK_WALLY); ctx->h_uk.assign(nce, FK_NONE); ctx->h_vk.assign(nve, FK_NONE);
+    for (int j = 0; j < ny; j++)
+        for (int li = 0; li < ctx->pitch; li++) {
+            int gi = ctx->gi0 - OFF + li;
+            ctx->h_ck[(size_t)j * ctx->pitch + li] = cell_kind_g(ctx, gi, j, solid);
+            ctx->h_uk[(size_t)j * ctx->pitch + li] = u_kind_g(ctx, gi, j, solid);
+        }
+    for (int j = 0; j <= ny; j++)
+        for (int li = 0; li < ctx->pitch; li++)
+            ctx->h_vk[(size_t)j * ctx->pitch + li] = v_kind_g(ctx, ctx->gi0 - OFF + li, j, solid);
+    return STS_OK;
+}
+
+extern "C" sts_status sts_plan(const sts_grid* grid, const sts_square* squares, int32_t n_squares,
+                               const sts_gas* gas, int32_t world, int32_t rank, sts_plan_info* out,
+                               uint8_t* kinds)
+{
+    if (!grid || !gas || !out || (n_squares > 0 && !squares)) return fail(nullptr, STS_E_ARG, "null argument");
+    sts_ctx c;
+    sts_status st = plan_host(grid, squares, n_squares, gas, world, rank, &c);
+    if (st != STS_OK) return st;
+    const bool per = gas->xbc == STS_X_PERIODIC;
+    out->nx = c.nx; out->ny = c.ny;
+    out->i0 = c.gi0; out->i1 = c.gi0 + c.nloc;
+    out->pitch = c.pitch; out->ghost = OFF;
+    out->left = rank > 0 ? rank - 1 : (per && world > 1 ? world - 1 : -1);
+    out->right = rank < world - 1 ? rank + 1 : (per && world > 1 ? 0 : -1);
+    // first / last OFF owned columns go to the left / right neighbour; the ghost
+    // columns [i0-OFF, i0) and [i1, i1+OFF) (unwrapped) come from them
+    out->send_left[0] = out->i0; out->send_left[1] = out->i0 + OFF;
+    out->send_right[0] = out->i1 - OFF; out->send_right[1] = out->i1;
+    out->recv_left[0] = out->i0 - OFF; out->recv_left[1] = out->i0;
+    out->recv_right[0] = out->i1; out->recv_right[1] = out->i1 + OFF;
+    if (kinds) {
+        const size_t nve = (size_t)c.pitch * (c.ny + 1);
+        for (size_t e = 0; e < nve; e++) {
+            kinds[e] = e < c.h_ck.size() ? c.h_ck[e] : (uint8_t)CK_WALLY;
+            kinds[nve + e] = e < c.h_uk.size() ? c.h_uk[e] : (uint8_t)FK_NONE;
+            kinds[2 * nve + e] = c.h_vk[e];
+        }
+    }
+    return STS_OK;
+}
+
 extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares, int32_t n_squares,
                                  const sts_gas* gas, const sts_scheme* scheme, const sts_dist* dist,
                                  sts_ctx** out)
@@ -527,40 +615,20 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
     sts_ctx* ctx = nullptr;
     if (!grid || !gas || !scheme || !out || (n_squares > 0 && !squares)) return fail(ctx, STS_E_ARG, "null argument");
     *out = nullptr;
-    if (!(grid->spacing > 0) || !(grid->length_x > 0) || !(grid->length_y > 0)) return fail(ctx, STS_E_CONFIG, "non-positive grid");
-    double fx = grid->length_x / grid->spacing, fy = grid->length_y / grid->spacing;
-    int nx = (int)llround(fx), ny = (int)llround(fy);
-    if (std::fabs(fx - nx) > 1e-9 || std::fabs(fy - ny) > 1e-9 || nx < 1 || ny < 1)
-        return fail(ctx, STS_E_CONFIG, "channel lengths are not multiples of the spacing");
-    if (!(gas->Kn > 0)) return fail(ctx, STS_E_CONFIG, "Kn must be > 0");
-    if (!(gas->pw_sign == 1.0 || gas->pw_sign == -1.0)) return fail(ctx, STS_E_CONFIG, "pw_sign must be +1 or -1");
-    if (gas->xbc != STS_X_INFLOW_OUTFLOW && gas->xbc != STS_X_PERIODIC) return fail(ctx, STS_E_ARG, "bad xbc");
     if ((scheme->time != STS_EXPLICIT && scheme->time != STS_IMPLICIT) || (scheme->space != STS_UPWIND && scheme->space != STS_TVD_VANLEER))
         return fail(ctx, STS_E_ARG, "bad scheme enum");
     if (!(scheme->dt > 0) || scheme->max_passes < 1 || scheme->min_passes < 0) return fail(ctx, STS_E_CONFIG, "bad dt / passes");
-    if (!(gas->p_in > 0) || !(gas->T_in > 0)) return fail(ctx, STS_E_CONFIG, "inflow state must be positive");
-    int world = dist ? dist->world : 1, rank = dist ? dist->rank : 0;
-    if (world < 1 || rank < 0 || rank >= world) return fail(ctx, STS_E_ARG, "bad rank/world");
-
-    std::vector<uint8_t> solid((size_t)nx * ny, 0);
-    for (int s = 0; s < n_squares; s++) {
-        const sts_square& q = squares[s];
-        if (q.ni < 1 || q.nj < 1 || q.i0 < 0 || q.j0 < 0 || q.i0 + q.ni > nx || q.j0 + q.nj > ny)
-            return fail(ctx, STS_E_CONFIG, "square outside the channel");
-        if (gas->xbc == STS_X_INFLOW_OUTFLOW && (q.i0 < 1 || q.i0 + q.ni > nx - 1))
-            return fail(ctx, STS_E_CONFIG, "square must leave a fluid column at the inlet and outlet");
-        for (int j = q.j0; j < q.j0 + q.nj; j++)
-            for (int i = q.i0; i < q.i0 + q.ni; i++) solid[(size_t)j * nx + i] = 1;
+    const int world = dist ? dist->world : 1, rank = dist ? dist->rank : 0;
+    ctx = new sts_ctx();
+    {
+        sts_status st0 = plan_host(grid, squares, n_squares, gas, world, rank, ctx);
+        if (st0 != STS_OK) { delete ctx; return st0; }
     }
     int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return fail(ctx, STS_E_CUDA, "no CUDA device");
-
-    ctx = new sts_ctx();
-    ctx->nx = nx; ctx->ny = ny; ctx->spacing = grid->spacing;
-    ctx->gas = *gas; ctx->sch = *scheme;
-    ctx->squares.assign(squares, squares + n_squares);
-    ctx->h_solid = solid;
-    ctx->rank = rank; ctx->world = world;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) { delete ctx; return fail(nullptr, STS_E_CUDA, "no CUDA device"); }
+    const int nx = ctx->nx, ny = ctx->ny;
+    const std::vector<uint8_t>& solid = ctx->h_solid;
+    ctx->sch = *scheme;
     ctx->device = dist ? dist->device : 0;
     if (ctx->device < 0 || ctx->device >= ndev) { delete ctx; return fail(nullptr, STS_E_ARG, "bad device"); }
     if (cudaSetDevice(ctx->device) != cudaSuccess) { delete ctx; return fail(nullptr, STS_E_CUDA, "cudaSetDevice"); }
@@ -573,31 +641,10 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
     ctx->u_in = gas->mach * std::sqrt(gas->gamma / 2.0 * gas->T_in);
     ctx->u_wb = gas->particle_frame ? ctx->u_in : gas->u_wall_bottom;   // R14
     ctx->u_wt = gas->particle_frame ? ctx->u_in : gas->u_wall_top;
-    // slab decomposition along x: near-equal, remainder to the low ranks
-    ctx->col_start.resize(world + 1);
-    for (int r = 0, acc = 0; r <= world; r++) {
-        ctx->col_start[r] = acc;
-        if (r < world) acc += nx / world + (r < nx % world ? 1 : 0);
-    }
-    ctx->gi0 = ctx->col_start[rank];
-    ctx->nloc = ctx->col_start[rank + 1] - ctx->gi0;
-    if (world > 1 && ctx->nloc < OFF) { delete ctx; return fail(nullptr, STS_E_CONFIG, "slab narrower than the halo"); }
-    ctx->pitch = ((ctx->nloc + 2 * OFF + 1) + 15) / 16 * 16;
 
     sts_status st = set_smem_attrs(ctx);
     if (st != STS_OK) { sts_destroy(ctx); return st; }
-    // kind maps
     size_t nce = cell_elems(ctx), nve = v_elems(ctx);
-    ctx->h_ck.assign(nce, CK_WALLY); ctx->h_uk.assign(nce, FK_NONE); ctx->h_vk.assign(nve, FK_NONE);
-    for (int j = 0; j < ny; j++)
-        for (int li = 0; li < ctx->pitch; li++) {
-            int gi = ctx->gi0 - OFF + li;
-            ctx->h_ck[(size_t)j * ctx->pitch + li] = cell_kind_g(ctx, gi, j, solid);
-            ctx->h_uk[(size_t)j * ctx->pitch + li] = u_kind_g(ctx, gi, j, solid);
-        }
-    for (int j = 0; j <= ny; j++)
-        for (int li = 0; li < ctx->pitch; li++)
-            ctx->h_vk[(size_t)j * ctx->pitch + li] = v_kind_g(ctx, ctx->gi0 - OFF + li, j, solid);
 
     auto alloc = [&](double** p, size_t n) -> sts_status {
         CU(cudaMalloc(p, n * sizeof(double)));

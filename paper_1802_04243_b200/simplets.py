@@ -25,7 +25,8 @@ FIELDS = {"u": 0, "v": 1, "p": 2, "T": 3, "rho": 4, "uexp": 6, "vexp": 7, "Texp"
 
 EXPORTS = ["sts_create", "sts_destroy", "sts_last_error", "sts_set_stream", "sts_init_freestream",
            "sts_set_field", "sts_set_field_device", "sts_advance", "sts_advance_group", "sts_get_field", "sts_get_field_device",
-           "sts_get_map", "sts_shape", "sts_constants", "sts_profile", "sts_profile_read", "sts_nccl_unique_id"]
+           "sts_get_map", "sts_shape", "sts_constants", "sts_profile", "sts_profile_read", "sts_nccl_unique_id",
+           "sts_plan"]
 
 
 class StsError(RuntimeError):
@@ -59,6 +60,11 @@ class sts_scheme(ctypes.Structure):
 class sts_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("nccl_id", ctypes.c_void_p)]
+
+
+class sts_plan_info(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("nx", "ny", "i0", "i1", "pitch", "ghost", "left", "right")] + \
+               [(n, ctypes.c_int32 * 2) for n in ("send_left", "send_right", "recv_left", "recv_right")]
 
 
 class sts_stats(ctypes.Structure):
@@ -112,6 +118,10 @@ def lib():
         L.sts_profile_read.argtypes = [vp, dp, ctypes.c_int32]
         L.sts_nccl_unique_id.restype = st
         L.sts_nccl_unique_id.argtypes = [vp]
+        L.sts_plan.restype = st
+        L.sts_plan.argtypes = [ctypes.POINTER(sts_grid), ctypes.POINTER(sts_square), ctypes.c_int32,
+                               ctypes.POINTER(sts_gas), ctypes.c_int32, ctypes.c_int32,
+                               ctypes.POINTER(sts_plan_info), ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -129,6 +139,43 @@ def advance_group(solvers, n_steps):
     st = sts_stats()
     _check(lib().sts_advance_group(arr, n, int(n_steps), ctypes.byref(st)), solvers[0]._h)
     return {"steps_done": st.steps_done, "passes_done": st.passes_done, "res": list(st.res), "converged": st.converged}
+
+
+def _structs(case: dict):
+    sp = float(case["spacing"])
+    grid = sts_grid(case["nx"] * sp, case["ny"] * sp, sp)
+    sq = list(case.get("squares", []))
+    arr = (sts_square * max(1, len(sq)))(*[sts_square(*map(int, s)) for s in sq])
+    gas = sts_gas(case["Kn"], case["mach"], case["gamma"], case.get("p_in", 1.0), case.get("T_in", 1.0),
+                  case.get("u_wall_bottom", 0.0), case.get("u_wall_top", 0.0),
+                  case.get("T_wall", 1.0), case.get("T_square", 1.0),
+                  case.get("g_x", 0.0), case.get("g_y", 0.0), float(case["pw_sign"]),
+                  int(case.get("particle_frame", 0)), int(case.get("xbc", 0)))
+    return grid, arr, len(sq), gas
+
+
+def plan(case: dict, world: int, rank: int, with_kinds: bool = True):
+    """Host-only decomposition plan of `rank` (sts_plan): a dict of the plan
+    fields and, optionally, the (3, ny+1, pitch) uint8 kind maps of its stored
+    columns.  Needs no GPU."""
+    grid, arr, nsq, gas = _structs(case)
+    info = sts_plan_info()
+    kinds = None
+    ptr = None
+    if with_kinds:
+        pitch_guess = case["nx"] // world + 64
+        kinds = np.zeros((3, case["ny"] + 1, pitch_guess), dtype=np.uint8)
+    # first call for the pitch, second for the maps
+    _check(lib().sts_plan(ctypes.byref(grid), arr, nsq, ctypes.byref(gas), world, rank, ctypes.byref(info), None))
+    out = {n: getattr(info, n) for n in ("nx", "ny", "i0", "i1", "pitch", "ghost", "left", "right")}
+    for n in ("send_left", "send_right", "recv_left", "recv_right"):
+        out[n] = tuple(getattr(info, n))
+    if with_kinds:
+        kinds = np.zeros((3, out["ny"] + 1, out["pitch"]), dtype=np.uint8)
+        ptr = kinds.ctypes.data_as(ctypes.c_void_p)
+        _check(lib().sts_plan(ctypes.byref(grid), arr, nsq, ctypes.byref(gas), world, rank, ctypes.byref(info), ptr))
+        out["kinds"] = kinds
+    return out
 
 
 def nccl_unique_id() -> bytes:
