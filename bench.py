@@ -216,18 +216,22 @@ def run_ours(args):
     pass_ms = prof["pass_ms"] / max(prof["pass_launches"], 1)
     bytes_per_launch = BYTES_PER_FVU[kind] * nfv_rank
     achieved = bytes_per_launch / (pass_ms / 1e3) / 1e9
-    traffic = None
+    # ncu evidence for this kernel (profiles/traffic.json, one --set full capture):
+    # DRAM bytes per launch and the fp64-pipe activity (the co-bound)
+    traffic = fp64_active = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            tj = json.load(open(tpath))
-            traffic = tj.get(f"{case['name']}_{args.variant}", {}).get("bytes_per_launch")
+            tj = json.load(open(tpath)).get(f"{case['name']}_{args.variant}", {})
+            traffic = tj.get("bytes_per_launch")
+            fp64_active = tj.get("fp64_pipe_active")
         except Exception:
-            traffic = None
+            traffic = fp64_active = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_kind, "kernel": f"pass_kernel<{kind},{args.variant.split('_')[1]}>",
+                "traffic": traffic, "peak_source": peak_kind, "kernel": f"march_kernel<{kind},{args.variant.split('_')[1]}>",
                 "algorithmic_bytes_per_fvu": BYTES_PER_FVU[kind], "pass_ms_avg": pass_ms,
-                "pass_share_of_step": prof["pass_ms"] / ms if ms > 0 else None}
+                "pass_share_of_step": prof["pass_ms"] / ms if ms > 0 else None,
+                "fp64_pipe_active_ncu": fp64_active}
 
     # e2e: through the public API with host (pinned) buffers, every step:
     # H2D of the step's input state (u, v, p, T) + advance + D2H of the residual maxima
