@@ -20,6 +20,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <functional>
+#include <queue>
 #include <vector>
 
 using namespace sts;
@@ -371,18 +373,25 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
         std::stable_sort(ctas.begin(), ctas.end(), [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
             return a.first > b.first;
         });
-        std::vector<double> load(std::min<size_t>(slots, ctas.size()), 0.0);
+        // greedy list scheduling onto the least-loaded slot (min-heap)
+        std::priority_queue<double, std::vector<double>, std::greater<double>> load;
+        for (size_t q = 0; q < std::min<size_t>(slots, ctas.size()); q++) load.push(0.0);
+        double makespan = 0.0;
         for (auto& q : ctas) {
-            auto it = std::min_element(load.begin(), load.end());
-            *it += q.first;
+            double l = load.top() + q.first;
+            load.pop();
+            load.push(l);
+            makespan = std::max(makespan, l);
         }
         (void)keep;
-        return *std::max_element(load.begin(), load.end());
+        return makespan;
     };
     if (forced > 0) {
         best_seg = forced;
     } else {
-        for (int seg = std::max(1, std::min(ny, 32)); seg <= ny; seg += (seg < 256 ? 8 : 32)) {
+        // candidate heights 32, 40, ... growing ~6 % per step (about 60 candidates)
+        for (int seg = std::max(1, std::min(ny, 32)); seg <= ny;
+             seg = std::max(seg + 8, (int)(seg * 1.06)) ) {
             const double ms = schedule(seg, false);
             if (ms < best * (1.0 - 1e-3)) { best = ms; best_seg = seg; }
         }

