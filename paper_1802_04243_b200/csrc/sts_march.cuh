@@ -80,19 +80,19 @@ __device__ __forceinline__ double fsqrt(double x)
     return fma(0.5 * y, fma(-s, s, x), s);
 }
 // same TVD correction as psi_u, with the reciprocal instead of IEEE division
-// (A branch-free form that always forms the quotient measured 15 % slower on
-// implicit TVD: the reciprocal costs more than the divergence it removes.)
+// The two flow directions share one code path (the upstream difference is
+// selected); the early exits skip the reciprocal on flat / extremum stencils,
+// which dominate the free stream.  (A fully branch-free form that always forms
+// the quotient measured 15 % slower on implicit TVD.)
 __device__ __forceinline__ double psi_f(double f1, double f2, double f3, double f4, double w)
 {
-    double b = f3 - f2;
+    const double b = f3 - f2;
     if (fabs(b) <= 1e-12 * (1.0 + fabs(f2) + fabs(f3))) return 0.0;   // R37
-    if (w > 0.0) {
-        double a = f2 - f1;
-        return ((a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0)) ? fdiv(a, a + b) : 0.0;
-    } else {
-        double c = f4 - f3;
-        return ((c > 0.0 && b > 0.0) || (c < 0.0 && b < 0.0)) ? -fdiv(c, c + b) : 0.0;
-    }
+    const bool up = w > 0.0;
+    const double a = up ? f2 - f1 : f4 - f3;
+    if (!(a * b > 0.0)) return 0.0;                                    // r <= 0 (R6)
+    const double q = fdiv(a, a + b);
+    return up ? q : -q;
 }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem)

@@ -160,11 +160,6 @@ def plan(case: dict, world: int, rank: int, with_kinds: bool = True):
     columns.  Needs no GPU."""
     grid, arr, nsq, gas = _structs(case)
     info = sts_plan_info()
-    kinds = None
-    ptr = None
-    if with_kinds:
-        pitch_guess = case["nx"] // world + 64
-        kinds = np.zeros((3, case["ny"] + 1, pitch_guess), dtype=np.uint8)
     # first call for the pitch, second for the maps
     _check(lib().sts_plan(ctypes.byref(grid), arr, nsq, ctypes.byref(gas), world, rank, ctypes.byref(info), None))
     out = {n: getattr(info, n) for n in ("nx", "ny", "i0", "i1", "pitch", "ghost", "left", "right")}
