@@ -19,8 +19,7 @@ namespace sts {
 
 struct ConvSmem {
     RingRow ring[RS];
-    double RU[2][RW], RV[2][RW];     // face densities rows j (cur) / j+1 (nxt)
-    double FX[2][RW], FY[2][RW];
+    double FX[2][RW], FY[2][RW];     // fluxes rows j (cur) / j+1 (nxt)
     double TX[RW], UX[RW], VX[RW];
 };
 
@@ -49,7 +48,7 @@ __global__ void __launch_bounds__(MX, 3) conv_march_kernel(MarchParams m)
     for (int j = js - 1; j <= js + 2; j++) ring_issue(ms, mm, I0, j, slot(j));
     cp_wait_all();
     __syncthreads();
-    for (int j = js - 1; j <= js + 2; j++) ring_derive(ms, slot(j));
+    for (int j = js - 1; j <= js + 2; j++) ring_derive<false>(ms, slot(j));
     ring_issue(ms, mm, I0, js + 3, slot(js + 3));
     int sj = slot(js);
 
@@ -66,7 +65,7 @@ __global__ void __launch_bounds__(MX, 3) conv_march_kernel(MarchParams m)
         cp_wait_all();
         __syncthreads();                                  // B0
         ring_issue(ms, mm, I0, j + 4, sd);
-        ring_derive(ms, sc);
+        ring_derive<false>(ms, sc);
         const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
         // ---- stage A: fluxes of row j+1 (Eqs. pl8-pl11 at time level n-1)
         double Fx1 = 0.0, Fy1 = 0.0;

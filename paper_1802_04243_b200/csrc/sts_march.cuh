@@ -174,14 +174,16 @@ __device__ __forceinline__ void ring_issue(MarchSmem& s, const MarchParams& m, i
     }
     cp_commit();
 }
-// rho = p/T (Eq. pl5), Gamma = sqrt(T) (Eq. pl37) of ring row j
+// rho = p/T (Eq. pl5), Gamma = sqrt(T) (Eq. pl37) of ring row j (the explicit
+// planes need no Gamma)
+template <bool WITH_GAMMA = true>
 __device__ __forceinline__ void ring_derive(MarchSmem& s, int sl)
 {
     RingRow& r = s.ring[sl];
     for (int lc = threadIdx.x; lc < RW; lc += MX) {
         const double Tv = r.T[lc];
         r.R[lc] = fdiv(r.P[lc], Tv);
-        r.G[lc] = fsqrt(Tv);
+        if (WITH_GAMMA) r.G[lc] = fsqrt(Tv);
     }
 }
 
