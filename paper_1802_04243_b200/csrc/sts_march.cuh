@@ -126,6 +126,20 @@ struct MarchSmem {
     double XUW[RW], XVW[RW], XVF[RW];
     double UH[RW], DU[RW];
 };
+// Implicit variants (3 CTAs/SM) keep p_new in a row of its own, so the next
+// row step's stage A may overwrite XTW while a neighbour is still in stage E:
+// the row-start barrier disappears (the ring row lands before B3 instead).
+struct MarchSmemI : MarchSmem {
+    double PN[RW];
+};
+__host__ __device__ constexpr size_t march_smem_bytes(bool impl) { return impl ? sizeof(MarchSmemI) : sizeof(MarchSmem); }
+template <bool IMPL> __device__ __forceinline__ double* pn_row(MarchSmem& s)
+{
+    if constexpr (IMPL) return static_cast<MarchSmemI&>(s).PN;
+    else return s.XTW;
+}
+// max that ignores a NaN operand (NaN u / v are flagged separately, T / p by the bad-state test)
+__device__ __forceinline__ double dmax(double m, double x) { return x > m ? x : m; }
 
 __device__ __forceinline__ int slot(int j) { return (j + 4 * RS) % RS; }
 __device__ __forceinline__ uint8_t ckind(uint32_t w) { return (uint8_t)(w & 0xff); }
@@ -502,7 +516,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
 }
 
 // ================= stage D: p_{i,j} (Eqs. pl23-pl24) =================
-template <bool REG>
+template <bool IMPL, bool REG>
 __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
                                         const RingRow& R0, const RingRow& Ra, const FluxRow& Fc,
                                         const FluxRow& Fn, const Carry& c, StepVars& v)
@@ -544,13 +558,13 @@ __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int 
         pn = (sum * dt + bp) * rcp(a0);
     }
     v.pn = pn;
-    s.XTW[lc] = pn;                  // p_new row (the T-eq piece row is dead after stage C)
+    pn_row<IMPL>(s)[lc] = pn;        // p_new row (explicit: the T-eq piece row, dead after stage C)
 }
 
-struct Resid { double du, dv, dp, dT, vel, p, T; long long bad; int badf; };
+struct Resid { double du, dv, dp, dT, vel, p, T; long long bad; int badf; bool nanv; };
 
 // ================= stage E: corrections, writes, residuals =================
-template <bool REG>
+template <bool IMPL, bool REG>
 __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int lc, int gi, int j,
                                         const RingRow& R0, const Carry& c, const StepVars& v, Resid& rs)
 {
@@ -561,10 +575,10 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
     if (fluid) {
         k.T_w[id] = v.TN;
         k.p_w[id] = v.pn;
-        rs.dT = nmax(rs.dT, fabs(v.TN - R0.T[lc]));
-        rs.dp = nmax(rs.dp, fabs(v.pn - R0.P[lc]));
-        rs.T = nmax(rs.T, fabs(v.TN));
-        rs.p = nmax(rs.p, fabs(v.pn));
+        rs.dT = dmax(rs.dT, fabs(v.TN - R0.T[lc]));
+        rs.dp = dmax(rs.dp, fabs(v.pn - R0.P[lc]));
+        rs.T = dmax(rs.T, fabs(v.TN));
+        rs.p = dmax(rs.p, fabs(v.pn));
         if (!(v.TN > 0.0) || !(v.pn > 0.0) || !isfinite(v.TN) || !isfinite(v.pn)) {
             const long long flat = (long long)j * k.nx + gi;
             if (rs.bad < 0 || flat < rs.bad) { rs.bad = flat; rs.badf = (!(v.TN > 0.0) || !isfinite(v.TN)) ? 3 : 2; }
@@ -572,16 +586,18 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
     }
     double un = 0.0;
     if (uA<REG>(kw0)) {
-        un = v.uhat - v.du * (v.pn - s.XTW[lc - 1]);     // XTW holds p_new in stage E
-        rs.du = nmax(rs.du, fabs(un - R0.U[lc]));
-        rs.vel = nmax(rs.vel, fabs(un));
+        un = v.uhat - v.du * (v.pn - pn_row<IMPL>(s)[lc - 1]);
+        rs.du = dmax(rs.du, fabs(un - R0.U[lc]));
+        rs.vel = dmax(rs.vel, fabs(un));
+        rs.nanv |= un != un;
     } else if (ukind(kw0) == FK_INLET) un = k.u_in;
     k.u_w[id] = un;
     double vn = 0.0;
     if (vA<REG>(kw0)) {
         vn = c.vhatP - c.dvP * (v.pn - c.pnP);
-        rs.dv = nmax(rs.dv, fabs(vn - R0.V[lc]));
-        rs.vel = nmax(rs.vel, fabs(vn));
+        rs.dv = dmax(rs.dv, fabs(vn - R0.V[lc]));
+        rs.vel = dmax(rs.vel, fabs(vn));
+        rs.nanv |= vn != vn;
     }
     k.v_w[id] = vn;
     if (!REG && k.xbc == 0 && gi == k.nx - 1) {
@@ -622,11 +638,13 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
     const bool owner = t >= 2 && t < 2 + MW && gi < k.gi0 + k.nloc;
 
     // ---- prologue: ring rows js-1 .. js+2 (synchronous), issue js+3
+    // (implicit: js+3 lands here too -- there is no row-start barrier)
     for (int j = js - 1; j <= js + 2; j++) ring_issue(s, m, I0, j, slot(j));
+    if (IMPL) ring_issue(s, m, I0, js + 3, slot(js + 3));
     cp_wait_all();
     __syncthreads();
     for (int j = js - 1; j <= js + 2; j++) ring_derive(s, slot(j));
-    ring_issue(s, m, I0, js + 3, slot(js + 3));
+    if (!IMPL) ring_issue(s, m, I0, js + 3, slot(js + 3));
     int sj = slot(js);                                  // ring slot of row j (incremental)
 
     // ---- n-1 / plane register pipeline (loaded one row step ahead)
@@ -643,7 +661,7 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
     if (!IMPL) { nm.Tec = ld(k.Te, js); nm.uec = ld(k.ue, js); nm.ven = ldv(k.ve, js + 1); }
 
     Carry c{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 1.0};
-    Resid rs{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, -1, 0};
+    Resid rs{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, -1, 0, false};
     StepVars v;
 
     for (int j = js; j < J1; j++) {
@@ -664,8 +682,10 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
         double Ten = 0.0, uen = 0.0, vem = 0.0;
         if (!IMPL) { Ten = ld(k.Te, j + 1); uen = ld(k.ue, j + 1); vem = ldv(k.ve, j + 2); }
 
-        cp_wait_all();
-        __syncthreads();                                    // B0: ring row j+3 landed
+        if (!IMPL) {
+            cp_wait_all();
+            __syncthreads();                                // B0: ring row j+3 landed
+        }
         ring_issue(s, m, I0, j + 4, sd);
         ring_derive(s, sc);
         // per-point choice (a function of the cell alone, so any decomposition
@@ -678,12 +698,13 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
         if (reg) stage_C<IMPL, TVD, true>(s, m, lc, Rm, R0, Ra, Rb, Fc, Fn, nm, c, v);
         else stage_C<IMPL, TVD, false>(s, m, lc, Rm, R0, Ra, Rb, Fc, Fn, nm, c, v);
         __syncthreads();                                    // B2
-        if (reg) stage_D<true>(s, m, lc, Rm, R0, Ra, Fc, Fn, c, v);
-        else stage_D<false>(s, m, lc, Rm, R0, Ra, Fc, Fn, c, v);
+        if (reg) stage_D<IMPL, true>(s, m, lc, Rm, R0, Ra, Fc, Fn, c, v);
+        else stage_D<IMPL, false>(s, m, lc, Rm, R0, Ra, Fc, Fn, c, v);
+        if (IMPL) cp_wait_all();                            // ring row j+4 (read from step j+1 on)
         __syncthreads();                                    // B3
         if (j >= J0 && owner) {
-            if (reg) stage_E<true>(s, m, lc, gi, j, R0, c, v, rs);
-            else stage_E<false>(s, m, lc, gi, j, R0, c, v, rs);
+            if (reg) stage_E<IMPL, true>(s, m, lc, gi, j, R0, c, v, rs);
+            else stage_E<IMPL, false>(s, m, lc, gi, j, R0, c, v, rs);
         }
         s.R1[lc] = v.r1n;                                   // (p/T)^{n-1} of row j+1 for step j+1
         // ---- carry row j+1 quantities to the next step
@@ -697,7 +718,8 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
         sj = sa;
     }
     cp_wait_all();
-    double vals[7] = {rs.du, rs.dv, rs.dp, rs.dT, rs.vel, rs.p, rs.T};
+    const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+    double vals[7] = {rs.nanv ? qnan : rs.du, rs.nanv ? qnan : rs.dv, rs.dp, rs.dT, rs.vel, rs.p, rs.T};
     __syncthreads();
     __shared__ double part[MX / 32][8];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
