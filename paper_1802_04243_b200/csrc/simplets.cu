@@ -573,6 +573,8 @@ static sts_status plan_host(const sts_grid* grid, const sts_square* squares, int
     ctx->nloc = ctx->col_start[rank + 1] - ctx->gi0;
     if (world > 1 && ctx->nloc < OFF) return fail(nullptr, STS_E_CONFIG, "slab narrower than the halo");
     ctx->pitch = ((ctx->nloc + 2 * OFF + 1) + 15) / 16 * 16;
+    if ((int64_t)ctx->pitch * (ny + 1) >= (int64_t)INT32_MAX)
+        return fail(nullptr, STS_E_CONFIG, "slab too large for 32-bit element indices (use more ranks)");
     // kind maps of the stored local columns [gi0-OFF, gi0-OFF+pitch)
     const size_t nce = (size_t)ctx->pitch * ny, nve = (size_t)ctx->pitch * (ny + 1);
     ctx->h_ck.assign(nce, CK_WALLY); ctx->h_uk.assign(nce, FK_NONE); ctx->h_vk.assign(nve, FK_NONE);

@@ -87,7 +87,14 @@ __device__ __forceinline__ double psi_u(double f1, double f2, double f3, double 
         return ((c > 0.0 && b > 0.0) || (c < 0.0 && b < 0.0)) ? -c / (c + b) : 0.0;
     }
 }
-__device__ __forceinline__ double max0(double a) { return a > 0.0 ? a : 0.0; }
+// max(0, a) exactly (also for -0 and NaN inputs of either sign' magnitude): clear
+// both words when the sign bit is set -- three integer ops, no fp64 compare/select
+__device__ __forceinline__ double max0(double a)
+{
+    const int hi = __double2hiint(a), lo = __double2loint(a);
+    const int keep = ~(hi >> 31);
+    return __hiloint2double(hi & keep, lo & keep);
+}
 __device__ __forceinline__ bool flux_face(uint8_t k) { return k == FK_ACTIVE || k == FK_INLET || k == FK_OUTLET; }
 __device__ __forceinline__ bool wallish(uint8_t k) { return k == CK_SOLID || k == CK_WALLY; }
 

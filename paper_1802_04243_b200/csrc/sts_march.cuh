@@ -156,23 +156,23 @@ template <bool REG> __device__ __forceinline__ bool vA(uint32_t w) { return REG 
 // Issue the loads of ring row j (global columns I0-4 .. I0-4+RW).  Rows outside
 // [0, ny] and unstored columns are filled directly: kind WALLY / NONE, u = wall
 // velocity beyond the walls (BC spec 8), p = T = 1, v = 0.
-__device__ __forceinline__ void ring_issue(MarchSmem& s, const MarchParams& m, int I0, int j, int sl)
+__device__ __forceinline__ void ring_issue(RingRow& r, const MarchParams& m, int I0, int j)
 {
     const Params& k = m.k;
-    RingRow& r = s.ring[sl];
-    const long long ro = (long long)j * k.pitch;
+    const int ro = j * k.pitch;                          // 32-bit element indices (checked on the host)
+    const int li0 = I0 - 4 - k.gi0 + OFF;
+    const bool row_ok = j >= 0 && j < k.ny;
     for (int lc = threadIdx.x; lc < RW; lc += MX) {
-        const int li = I0 - 4 + lc - k.gi0 + OFF;        // stored local column
+        const int li = li0 + lc;                         // stored local column
         const bool col_ok = li >= 0 && li < k.pitch;
-        if (j >= 0 && j < k.ny && col_ok) {
-            const long long id = ro + li;
+        const int id = ro + li;
+        if (row_ok && col_ok) {
             cp_async8(&r.U[lc], k.u_o + id);
             cp_async8(&r.V[lc], k.v_o + id);
             cp_async8(&r.P[lc], k.p_o + id);
             cp_async8(&r.T[lc], k.T_o + id);
             cp_async4(&r.KK[lc], m.kind + id);
         } else if (j == k.ny && col_ok) {          // top wall row: v = 0 (WALL), no cells
-            const long long id = ro + li;
             r.U[lc] = k.u_wt;
             cp_async8(&r.V[lc], k.v_o + id);
             r.P[lc] = 1.0;
@@ -188,17 +188,25 @@ __device__ __forceinline__ void ring_issue(MarchSmem& s, const MarchParams& m, i
     }
     cp_commit();
 }
+__device__ __forceinline__ void ring_issue(MarchSmem& s, const MarchParams& m, int I0, int j, int sl)
+{
+    ring_issue(s.ring[sl], m, I0, j);
+}
 // rho = p/T (Eq. pl5), Gamma = sqrt(T) (Eq. pl37) of ring row j (the explicit
 // planes need no Gamma)
 template <bool WITH_GAMMA = true>
-__device__ __forceinline__ void ring_derive(MarchSmem& s, int sl)
+__device__ __forceinline__ void ring_derive(RingRow& r)
 {
-    RingRow& r = s.ring[sl];
     for (int lc = threadIdx.x; lc < RW; lc += MX) {
         const double Tv = r.T[lc];
         r.R[lc] = fdiv(r.P[lc], Tv);
         if (WITH_GAMMA) r.G[lc] = fsqrt(Tv);
     }
+}
+template <bool WITH_GAMMA = true>
+__device__ __forceinline__ void ring_derive(MarchSmem& s, int sl)
+{
+    ring_derive<WITH_GAMMA>(s.ring[sl]);
 }
 
 // Quantities carried from row step j-1 to row step j (register rotation).
@@ -569,7 +577,7 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
                                         const RingRow& R0, const Carry& c, const StepVars& v, Resid& rs)
 {
     const Params& k = m.k;
-    const long long id = gidx(k, gi, j);
+    const int id = j * k.pitch + (gi - k.gi0 + OFF);
     const uint32_t kw0 = R0.KK[lc];
     const bool fluid = cF<REG>(kw0);
     if (fluid) {
@@ -611,7 +619,7 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
         if (gi < OFF) tgt = gi + k.nx;
         else if (gi >= k.nx - OFF) tgt = gi - k.nx;
         if (tgt > -1000) {
-            const long long tt = gidx(k, tgt, j);
+            const int tt = j * k.pitch + (tgt - k.gi0 + OFF);
             if (fluid) { k.p_w[tt] = v.pn; k.T_w[tt] = v.TN; }
             k.u_w[tt] = un;
             k.v_w[tt] = vn;
@@ -639,20 +647,28 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
 
     // ---- prologue: ring rows js-1 .. js+2 (synchronous), issue js+3
     // (implicit: js+3 lands here too -- there is no row-start barrier)
-    for (int j = js - 1; j <= js + 2; j++) ring_issue(s, m, I0, j, slot(j));
-    if (IMPL) ring_issue(s, m, I0, js + 3, slot(js + 3));
+    // ring slots of rows j-1 .. j+4, rotated by one per row step
+    RingRow *pm = &s.ring[0], *p0 = &s.ring[1], *pa = &s.ring[2], *pb = &s.ring[3], *pc = &s.ring[4], *pd = &s.ring[5];
+    ring_issue(*pm, m, I0, js - 1);
+    ring_issue(*p0, m, I0, js);
+    ring_issue(*pa, m, I0, js + 1);
+    ring_issue(*pb, m, I0, js + 2);
+    if (IMPL) ring_issue(*pc, m, I0, js + 3);
     cp_wait_all();
     __syncthreads();
-    for (int j = js - 1; j <= js + 2; j++) ring_derive(s, slot(j));
-    if (!IMPL) ring_issue(s, m, I0, js + 3, slot(js + 3));
-    int sj = slot(js);                                  // ring slot of row j (incremental)
+    ring_derive(*pm);
+    ring_derive(*p0);
+    ring_derive(*pa);
+    ring_derive(*pb);
+    if (!IMPL) ring_issue(*pc, m, I0, js + 3);
 
     // ---- n-1 / plane register pipeline (loaded one row step ahead)
+    const int col = gi - k.gi0 + OFF;                   // stored local column of this thread
     auto ld = [&](const double* a, int j) -> double {
-        return (col_stored && j >= 0 && j < k.ny) ? __ldg(a + gidx(k, gi, j)) : 0.0;
+        return (col_stored && j >= 0 && j < k.ny) ? __ldg(a + (j * k.pitch + col)) : 0.0;
     };
     auto ldv = [&](const double* a, int j) -> double {
-        return (col_stored && j >= 0 && j <= k.ny) ? __ldg(a + gidx(k, gi, j)) : 0.0;
+        return (col_stored && j >= 0 && j <= k.ny) ? __ldg(a + (j * k.pitch + col)) : 0.0;
     };
     NM1 nm;
     nm.p1n = ld(k.p_1, js + 1); nm.T1n = ld(k.T_1, js + 1);
@@ -665,14 +681,11 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
     StepVars v;
 
     for (int j = js; j < J1; j++) {
-        const int sa = sj + 1 == RS ? 0 : sj + 1, sb = sa + 1 == RS ? 0 : sa + 1;
-        const int sc = sb + 1 == RS ? 0 : sb + 1, sd = sc + 1 == RS ? 0 : sc + 1;
-        const int sm = sj == 0 ? RS - 1 : sj - 1;
-        RingRow& Rm = s.ring[sm];
-        RingRow& R0 = s.ring[sj];
-        RingRow& Ra = s.ring[sa];
-        RingRow& Rb = s.ring[sb];
-        RingRow& Rc = s.ring[sc];
+        RingRow& Rm = *pm;
+        RingRow& R0 = *p0;
+        RingRow& Ra = *pa;
+        RingRow& Rb = *pb;
+        RingRow& Rc = *pc;
         FluxRow& Fc = s.fr[j & 1];
         FluxRow& Fn = s.fr[(j + 1) & 1];
 
@@ -686,8 +699,8 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
             cp_wait_all();
             __syncthreads();                                // B0: ring row j+3 landed
         }
-        ring_issue(s, m, I0, j + 4, sd);
-        ring_derive(s, sc);
+        ring_issue(*pd, m, I0, j + 4);
+        ring_derive(Rc);
         // per-point choice (a function of the cell alone, so any decomposition
         // gives bit-identical results); warps mixing both kinds run both
         // instances -- such CTAs are scheduled first (host longest-first order)
@@ -715,7 +728,8 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
         c.pnP = v.pn; c.gcP = v.gcN;
         nm.p1n = p1nn; nm.T1c = nm.T1n; nm.T1n = T1nn; nm.u1c = u1n; nm.v1n = v1nn;
         if (!IMPL) { nm.Tec = Ten; nm.uec = uen; nm.ven = vem; }
-        sj = sa;
+        RingRow* const pf = pm;
+        pm = p0; p0 = pa; pa = pb; pb = pc; pc = pd; pd = pf;
     }
     cp_wait_all();
     const double qnan = __longlong_as_double(0x7ff8000000000000LL);
