@@ -276,9 +276,8 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
     pass_fn fns[6] = {pass_table(0, 0), pass_table(0, 1), pass_table(1, 0), pass_table(1, 1), conv_table(0), conv_table(1)};
     for (pass_fn f : fns) CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     march_fn mfs[4] = {march_table(0, 0), march_table(0, 1), march_table(1, 0), march_table(1, 1)};
-    for (int q = 0; q < 4; q++)
-        CU(cudaFuncSetAttribute((const void*)mfs[q], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)march_smem_bytes(q >= 2)));
+    for (march_fn f : mfs)
+        CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));
     for (int tvd = 0; tvd < 2; tvd++)
         CU(cudaFuncSetAttribute((const void*)conv_march_table(tvd), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(ConvSmem)));
@@ -333,8 +332,7 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
     int nb = 0;
     const void* fn = (const void*)march_table(c->sch.time == STS_IMPLICIT, c->sch.space == STS_TVD_VANLEER);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, MX, march_smem_bytes(c->sch.time == STS_IMPLICIT)) ==
-            cudaSuccess && nb > 0)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, MX, sizeof(MarchSmem)) == cudaSuccess && nb > 0)
         per_sm = nb;
     const int strips = (c->nloc + MW - 1) / MW;
     const int slots = dev_sms * per_sm;
@@ -1091,7 +1089,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                     pass<<<grid, NT, smem, st>>>(k);
                 } else {
                     const dim3 mgrid(c->march_nstrips * c->march_nseg);
-                    march<<<mgrid, MX, march_smem_bytes(impl), st>>>(make_march(c, k));
+                    march<<<mgrid, MX, sizeof(MarchSmem), st>>>(make_march(c, k));
                 }
                 prof_end(c);
                 c->launches++;

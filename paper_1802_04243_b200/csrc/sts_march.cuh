@@ -113,31 +113,23 @@ struct RingRow {                 // one old-iterate row (slot-major: one base ad
     uint32_t KK[RW];
 };
 struct FluxRow {                 // face densities / fluxes of one row
-    double RU[RW], FX[RW], RV[RW], FY[RW];
+    double RU[RW], FX[RW], FY[RW];   // (rho^v stays in registers: only the own column reads it)
 };
-// 56.8 KB: four CTAs (16 warps) per SM.  Pieces a neighbour can recompute with
+// 54.7 KB: four CTAs (16 warps) per SM.  Pieces a neighbour can recompute with
 // the same operations (E-side coefficients = W-side - F, F-bar^x, corner Gamma)
-// are not stored; p_new reuses the T-eq piece row (dead after stage C).
+// are not stored.
 struct MarchSmem {
     RingRow ring[RS];
     FluxRow fr[2];
     double R1[RW];               // (p/T)^{n-1} of row j (row j+1 is written in stage E)
-    double XTW[RW];              // T-eq W coefficient of face i (stage C); p_new (stages D-E)
+    double XTW[RW];              // T-eq W coefficient of face i (stage C)
     double XUW[RW], XVW[RW], XVF[RW];
     double UH[RW], DU[RW];
+    double PN[RW];               // p_new of row j (stages D-E): a row of its own, so no row-start barrier
 };
-// Implicit variants (3 CTAs/SM) keep p_new in a row of its own, so the next
-// row step's stage A may overwrite XTW while a neighbour is still in stage E:
-// the row-start barrier disappears (the ring row lands before B3 instead).
-struct MarchSmemI : MarchSmem {
-    double PN[RW];
-};
-__host__ __device__ constexpr size_t march_smem_bytes(bool impl) { return impl ? sizeof(MarchSmemI) : sizeof(MarchSmem); }
-template <bool IMPL> __device__ __forceinline__ double* pn_row(MarchSmem& s)
-{
-    if constexpr (IMPL) return static_cast<MarchSmemI&>(s).PN;
-    else return s.XTW;
-}
+// resident CTAs per SM: 4 (128 registers, 16 warps) except implicit TVD, whose
+// limiter work needs more registers (3 CTAs; measured: 4 CTAs spill and lose 4 %)
+__host__ __device__ constexpr int march_ctas(bool impl, bool tvd) { return impl && tvd ? 3 : 4; }
 // max that ignores a NaN operand (NaN u / v are flagged separately, T / p by the bad-state test)
 __device__ __forceinline__ double dmax(double m, double x) { return x > m ? x : m; }
 
@@ -217,6 +209,7 @@ struct Carry {
     double vhatP, dvP;    // v-hat, d^v at v-face (i, j)
     double pnP;           // p_new(i, j-1)
     double gcP;           // corner Gamma (i, j)
+    double rvS;           // rho^v at v-face (i, j)
 };
 // Values passed between the stages of one row step.
 struct StepVars {
@@ -228,6 +221,7 @@ struct StepVars {
     double xvW, FwSum;            // v-eq tangential W piece / flux sum at x^f_i, v-row j+1
     double xe, Fb;                // u-eq E coefficient of face i / F-bar^x of cell (i, j)
     double r1n;                   // (p/T)^{n-1} (i, j+1)
+    double rv1;                   // rho^v at v-face (i, j+1)
     double TN, uhat, du, utSn, FsSumN, vhatN, dvN, pn;
 };
 struct NM1 {                      // n-1 state / explicit planes at this thread's points
@@ -271,7 +265,7 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
                 rv += psi_f(Rm.R[lc], r1, r2, Rb.R[lc], w) * (r2 - r1);
             F = rv * w * dx;
         }
-        Fn.RV[lc] = rv;
+        v.rv1 = rv;
         Fn.FY[lc] = F;
         v.Fy1 = F;
     }
@@ -524,7 +518,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
 }
 
 // ================= stage D: p_{i,j} (Eqs. pl23-pl24) =================
-template <bool IMPL, bool REG>
+template <bool IMPL, bool TVD, bool REG>
 __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
                                         const RingRow& R0, const RingRow& Ra, const FluxRow& Fc,
                                         const FluxRow& Fn, const Carry& c, StepVars& v)
@@ -536,7 +530,7 @@ __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int 
     if (cF<REG>(kw0)) {
         double apW = 0.0, apE = 0.0, apS = 0.0, apN = 0.0, bpW = 0.0, bpE = 0.0, bpS = 0.0, bpN = 0.0, sum = 0.0;
         if (REG) {
-            const double rw = Fc.RU[lc], re = Fc.RU[lc + 1], rs = Fc.RV[lc], rn = Fn.RV[lc];
+            const double rw = Fc.RU[lc], re = Fc.RU[lc + 1], rs = c.rvS, rn = v.rv1;
             apW = rw * v.du * dy; bpW = rw * v.uhat * dy;
             apE = re * s.DU[lc + 1] * dy; bpE = re * s.UH[lc + 1] * dy;
             apS = rs * c.dvP * dx; bpS = rs * c.vhatP * dx;
@@ -553,11 +547,11 @@ __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int 
                 apE = r * s.DU[lc + 1] * dy; bpE = r * s.UH[lc + 1] * dy; sum += apE * R0.P[lc + 1];
             } else if (kef == FK_OUTLET) bpE = Fc.RU[lc + 1] * R0.U[lc] * dy;
             if (vkind(kw0) == FK_ACTIVE) {
-                const double r = Fc.RV[lc];
+                const double r = c.rvS;
                 apS = r * c.dvP * dx; bpS = r * c.vhatP * dx; sum += apS * Rm.P[lc];
             }
             if (vkind(Ra.KK[lc]) == FK_ACTIVE) {
-                const double r = Fn.RV[lc];
+                const double r = v.rv1;
                 apN = r * v.dvN * dx; bpN = r * v.vhatN * dx; sum += apN * Ra.P[lc];
             }
         }
@@ -566,13 +560,13 @@ __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int 
         pn = (sum * dt + bp) * rcp(a0);
     }
     v.pn = pn;
-    pn_row<IMPL>(s)[lc] = pn;        // p_new row (explicit: the T-eq piece row, dead after stage C)
+    s.PN[lc] = pn;
 }
 
 struct Resid { double du, dv, dp, dT, vel, p, T; long long bad; int badf; bool nanv; };
 
 // ================= stage E: corrections, writes, residuals =================
-template <bool IMPL, bool REG>
+template <bool IMPL, bool TVD, bool REG>
 __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int lc, int gi, int j,
                                         const RingRow& R0, const Carry& c, const StepVars& v, Resid& rs)
 {
@@ -594,7 +588,7 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
     }
     double un = 0.0;
     if (uA<REG>(kw0)) {
-        un = v.uhat - v.du * (v.pn - pn_row<IMPL>(s)[lc - 1]);
+        un = v.uhat - v.du * (v.pn - s.PN[lc - 1]);
         rs.du = dmax(rs.du, fabs(un - R0.U[lc]));
         rs.vel = dmax(rs.vel, fabs(un));
         rs.nanv |= un != un;
@@ -628,7 +622,7 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
 }
 
 template <bool IMPL, bool TVD>
-__global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
+__global__ void __launch_bounds__(MX, march_ctas(IMPL, TVD)) march_kernel(MarchParams m)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MarchSmem& s = *reinterpret_cast<MarchSmem*>(smem_raw);
@@ -645,22 +639,21 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
     const bool col_stored = stored_col(k, gi);
     const bool owner = t >= 2 && t < 2 + MW && gi < k.gi0 + k.nloc;
 
-    // ---- prologue: ring rows js-1 .. js+2 (synchronous), issue js+3
-    // (implicit: js+3 lands here too -- there is no row-start barrier)
+    // ---- prologue: ring rows js-1 .. js+3 land (there is no row-start barrier: from
+    // here on, row j+4 is issued at the start of step j and lands before its B3);
     // ring slots of rows j-1 .. j+4, rotated by one per row step
     RingRow *pm = &s.ring[0], *p0 = &s.ring[1], *pa = &s.ring[2], *pb = &s.ring[3], *pc = &s.ring[4], *pd = &s.ring[5];
     ring_issue(*pm, m, I0, js - 1);
     ring_issue(*p0, m, I0, js);
     ring_issue(*pa, m, I0, js + 1);
     ring_issue(*pb, m, I0, js + 2);
-    if (IMPL) ring_issue(*pc, m, I0, js + 3);
+    ring_issue(*pc, m, I0, js + 3);
     cp_wait_all();
     __syncthreads();
     ring_derive(*pm);
     ring_derive(*p0);
     ring_derive(*pa);
     ring_derive(*pb);
-    if (!IMPL) ring_issue(*pc, m, I0, js + 3);
 
     // ---- n-1 / plane register pipeline (loaded one row step ahead)
     const int col = gi - k.gi0 + OFF;                   // stored local column of this thread
@@ -676,7 +669,7 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
     nm.Tec = nm.uec = nm.ven = 0.0;
     if (!IMPL) { nm.Tec = ld(k.Te, js); nm.uec = ld(k.ue, js); nm.ven = ldv(k.ve, js + 1); }
 
-    Carry c{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 1.0};
+    Carry c{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 1.0, 0.0};
     Resid rs{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, -1, 0, false};
     StepVars v;
 
@@ -695,10 +688,6 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
         double Ten = 0.0, uen = 0.0, vem = 0.0;
         if (!IMPL) { Ten = ld(k.Te, j + 1); uen = ld(k.ue, j + 1); vem = ldv(k.ve, j + 2); }
 
-        if (!IMPL) {
-            cp_wait_all();
-            __syncthreads();                                // B0: ring row j+3 landed
-        }
         ring_issue(*pd, m, I0, j + 4);
         ring_derive(Rc);
         // per-point choice (a function of the cell alone, so any decomposition
@@ -711,13 +700,13 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
         if (reg) stage_C<IMPL, TVD, true>(s, m, lc, Rm, R0, Ra, Rb, Fc, Fn, nm, c, v);
         else stage_C<IMPL, TVD, false>(s, m, lc, Rm, R0, Ra, Rb, Fc, Fn, nm, c, v);
         __syncthreads();                                    // B2
-        if (reg) stage_D<IMPL, true>(s, m, lc, Rm, R0, Ra, Fc, Fn, c, v);
-        else stage_D<IMPL, false>(s, m, lc, Rm, R0, Ra, Fc, Fn, c, v);
-        if (IMPL) cp_wait_all();                            // ring row j+4 (read from step j+1 on)
+        if (reg) stage_D<IMPL, TVD, true>(s, m, lc, Rm, R0, Ra, Fc, Fn, c, v);
+        else stage_D<IMPL, TVD, false>(s, m, lc, Rm, R0, Ra, Fc, Fn, c, v);
+        cp_wait_all();                                      // ring row j+4 (read from step j+1 on)
         __syncthreads();                                    // B3
         if (j >= J0 && owner) {
-            if (reg) stage_E<IMPL, true>(s, m, lc, gi, j, R0, c, v, rs);
-            else stage_E<IMPL, false>(s, m, lc, gi, j, R0, c, v, rs);
+            if (reg) stage_E<IMPL, TVD, true>(s, m, lc, gi, j, R0, c, v, rs);
+            else stage_E<IMPL, TVD, false>(s, m, lc, gi, j, R0, c, v, rs);
         }
         s.R1[lc] = v.r1n;                                   // (p/T)^{n-1} of row j+1 for step j+1
         // ---- carry row j+1 quantities to the next step
@@ -725,7 +714,7 @@ __global__ void __launch_bounds__(MX, IMPL ? 3 : 4) march_kernel(MarchParams m)
         c.utS = v.utSn; c.FsSum = v.FsSumN;
         c.vcS = v.vcSn; c.FbS = v.FbN;
         c.vhatP = v.vhatN; c.dvP = v.dvN;
-        c.pnP = v.pn; c.gcP = v.gcN;
+        c.pnP = v.pn; c.gcP = v.gcN; c.rvS = v.rv1;
         nm.p1n = p1nn; nm.T1c = nm.T1n; nm.T1n = T1nn; nm.u1c = u1n; nm.v1n = v1nn;
         if (!IMPL) { nm.Tec = Ten; nm.uec = uen; nm.ven = vem; }
         RingRow* const pf = pm;
