@@ -54,27 +54,35 @@ class ClockSampler:
         self.samples = []          # (sm_mhz, sm_max_mhz, {reason names})
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._h = None
+        try:                       # NVML set up before the timed region starts
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            try:                   # the CUDA device's PCI address (NVML ignores CUDA_VISIBLE_DEVICES)
+                import torch
+                pr = torch.cuda.get_device_properties(index)
+                self._h = pynvml.nvmlDeviceGetHandleByPciBusId(
+                    f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+            except Exception:
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._bits = {"hw_slowdown": pynvml.nvmlClocksThrottleReasonHwSlowdown,
+                          "hw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
+                          "sw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonSwThermalSlowdown,
+                          "sw_power_cap": pynvml.nvmlClocksThrottleReasonSwPowerCap}
+            self._max = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self._h = None
+
+    def _sample_nvml(self):
+        nv = self._nv
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        self.samples.append((float(sm), self._max, {n for n, b in self._bits.items() if r & b}))
 
     def _nvml(self):
-        import pynvml
-        pynvml.nvmlInit()
-        h = None
-        try:                       # the CUDA device's PCI address (NVML ignores CUDA_VISIBLE_DEVICES)
-            import torch
-            pr = torch.cuda.get_device_properties(self.index)
-            h = pynvml.nvmlDeviceGetHandleByPciBusId(
-                f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
-        except Exception:
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-        bits = {"hw_slowdown": pynvml.nvmlClocksThrottleReasonHwSlowdown,
-                "hw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
-                "sw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonSwThermalSlowdown,
-                "sw_power_cap": pynvml.nvmlClocksThrottleReasonSwPowerCap}
-        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         while not self._stop.is_set():
-            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-            r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-            self.samples.append((float(sm), float(mx), {n for n, b in bits.items() if r & b}))
+            self._sample_nvml()
             self._stop.wait(0.005)
 
     def _smi(self):
@@ -93,10 +101,12 @@ class ClockSampler:
             self._stop.wait(0.02)
 
     def _run(self):
-        try:
-            self._nvml()
-        except Exception:
-            self._smi()
+        if self._h is not None:
+            try:
+                return self._nvml()
+            except Exception:
+                pass
+        self._smi()
 
     def __enter__(self):
         self._t.start()
@@ -105,6 +115,11 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if not self.samples and self._h is not None:
+            try:                   # a timed region shorter than one sampling interval
+                self._sample_nvml()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.samples:
