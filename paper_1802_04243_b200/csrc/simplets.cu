@@ -99,6 +99,14 @@ struct sts_ctx {
     bool use_tile = false;                 // STS_KERNEL=tile: v1 2-D tile kernel
     int march_seg = 0, march_nseg = 0, march_nstrips = 0;
     int* cta_order = nullptr;              // launch order of the march CTAs (longest first)
+    int* cta_split = nullptr;              // the same CTAs, edge strips (0, last) first, then the interior
+    int n_edge = 0;                        // CTAs in the edge strips
+    int edge_seg = 0;                      // their (shorter) segment height
+    int n_split = 0;                       // entries of cta_split
+    // halo overlap (multi-GPU): edge strips + pack/NCCL/unpack on a high-priority
+    // stream while the interior strips of the next pass run on the pass stream
+    cudaStream_t hstream = nullptr;
+    cudaEvent_t ev_a[2] = {nullptr, nullptr}, ev_b = nullptr, ev_s = nullptr, ev_h = nullptr;
     unsigned long long* red = nullptr;     // [max_passes][9]
     unsigned long long* h_red = nullptr;   // pinned, 9 entries
     double* stage = nullptr;               // device staging (global-shape field)
@@ -406,6 +414,32 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     c->cta_order = nullptr;
     cudaMalloc(&c->cta_order, order.size() * sizeof(int));
     cudaMemcpy(c->cta_order, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice);
+    // Split order for the multi-GPU halo overlap: the CTAs of the edge strips
+    // (strip st, local first column I0 = st MW, reads local columns I0-4 ..
+    // I0+127 and writes I0 .. I0+124: an edge strip reads a ghost column or
+    // writes one of the 4 columns sent to a neighbour), then the interior ones
+    // in the longest-first order.  The edge strips get ~15 % shorter segments,
+    // so that they finish early enough for the halo exchange to hide behind the
+    // interior strips of the next pass (the height never changes a bit).
+    auto edge = [&](int st) { const int I0 = st * MW; return I0 < OFF || I0 + MX >= c->nloc; };
+    c->edge_seg = std::max(8, std::min(best_seg, (int)(best_seg * 0.85)));
+    const int nseg_e = (ny + c->edge_seg - 1) / c->edge_seg;
+    std::vector<std::pair<double, int>> ectas;
+    for (int g = 0; g < nseg_e; g++)
+        for (int st = 0; st < strips; st++)
+            if (edge(st)) ectas.push_back({seg_cost(st, g * c->edge_seg, std::min(ny, (g + 1) * c->edge_seg)), st + strips * g});
+    std::stable_sort(ectas.begin(), ectas.end(), [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
+        return a.first > b.first;
+    });
+    std::vector<int> split;
+    for (auto& q : ectas) split.push_back(q.second);
+    c->n_edge = (int)split.size();
+    for (int o : order) if (!edge(o % strips)) split.push_back(o);
+    c->n_split = (int)split.size();
+    cudaFree(c->cta_split);
+    c->cta_split = nullptr;
+    cudaMalloc(&c->cta_split, split.size() * sizeof(int));
+    cudaMemcpy(c->cta_split, split.data(), split.size() * sizeof(int), cudaMemcpyHostToDevice);
 }
 
 // ------------------------------------------------------------- profiling
@@ -468,7 +502,7 @@ static sts_status halo_unpack(sts_ctx* ctx, const Snapshot& s, cudaStream_t st)
     return STS_OK;
 }
 // NCCL transport: grouped send/recv with both neighbours on the context stream.
-static sts_status halo_nccl(sts_ctx* ctx)
+static sts_status halo_nccl(sts_ctx* ctx, cudaStream_t st)
 {
     const int per = halo_per(ctx);
     const int left = left_of(ctx), right = right_of(ctx);
@@ -478,13 +512,13 @@ static sts_status halo_nccl(sts_ctx* ctx)
     // strip first and receive into its LEFT ghosts first: a rank's left ghosts
     // take its left neighbour's right strip.
     if (g_nccl.GroupStart()) return fail(ctx, STS_E_COMM, "ncclGroupStart");
-    if (right >= 0 && g_nccl.Send(ctx->halo + per, per, NCCL_FLOAT64, right, ctx->comm, ctx->stream))
+    if (right >= 0 && g_nccl.Send(ctx->halo + per, per, NCCL_FLOAT64, right, ctx->comm, st))
         return fail(ctx, STS_E_COMM, "ncclSend");
-    if (left >= 0 && g_nccl.Send(ctx->halo, per, NCCL_FLOAT64, left, ctx->comm, ctx->stream))
+    if (left >= 0 && g_nccl.Send(ctx->halo, per, NCCL_FLOAT64, left, ctx->comm, st))
         return fail(ctx, STS_E_COMM, "ncclSend");
-    if (left >= 0 && g_nccl.Recv(ctx->halo + 2 * per, per, NCCL_FLOAT64, left, ctx->comm, ctx->stream))
+    if (left >= 0 && g_nccl.Recv(ctx->halo + 2 * per, per, NCCL_FLOAT64, left, ctx->comm, st))
         return fail(ctx, STS_E_COMM, "ncclRecv");
-    if (right >= 0 && g_nccl.Recv(ctx->halo + 3 * per, per, NCCL_FLOAT64, right, ctx->comm, ctx->stream))
+    if (right >= 0 && g_nccl.Recv(ctx->halo + 3 * per, per, NCCL_FLOAT64, right, ctx->comm, st))
         return fail(ctx, STS_E_COMM, "ncclRecv");
     if (g_nccl.GroupEnd()) return fail(ctx, STS_E_COMM, "ncclGroupEnd");
     return STS_OK;
@@ -502,7 +536,7 @@ static sts_status exchange_group(sts_ctx** cs, int n, const int* which, cudaStre
     if (cs[0]->world == 1 && !cs[0]->comm) return STS_OK;
     for (int r = 0; r < n; r++) { sts_status e = halo_pack(cs[r], pick(cs[r], which[r]), st); if (e) return e; }
     if (n == 1) {
-        sts_status e = halo_nccl(cs[0]);
+        sts_status e = halo_nccl(cs[0], st);
         if (e) return e;
     } else {
         for (int r = 0; r < n; r++) {
@@ -741,9 +775,11 @@ extern "C" void sts_destroy(sts_ctx* ctx)
     cudaDeviceSynchronize();
     for (int k = 0; k < 3; k++) { cudaFree(ctx->snap[k].u); cudaFree(ctx->snap[k].v); cudaFree(ctx->snap[k].p); cudaFree(ctx->snap[k].T); }
     cudaFree(ctx->ue); cudaFree(ctx->ve); cudaFree(ctx->Te); cudaFree(ctx->stage); cudaFree(ctx->halo);
-    cudaFree(ctx->ck); cudaFree(ctx->uk); cudaFree(ctx->vk); cudaFree(ctx->kind32); cudaFree(ctx->cta_order); cudaFree(ctx->red);
+    cudaFree(ctx->ck); cudaFree(ctx->uk); cudaFree(ctx->vk); cudaFree(ctx->kind32); cudaFree(ctx->cta_order); cudaFree(ctx->cta_split); cudaFree(ctx->red);
     if (ctx->h_red) cudaFreeHost(ctx->h_red);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : {ctx->ev_a[0], ctx->ev_a[1], ctx->ev_b, ctx->ev_s, ctx->ev_h}) if (e) cudaEventDestroy(e);
+    if (ctx->hstream) cudaStreamDestroy(ctx->hstream);
     if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
     delete ctx;
 }
@@ -1076,6 +1112,26 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
         }
         int passes = 0;
         bool conv = false;
+        // Halo overlap (one rank per process, a halo to exchange, >= 3 strips):
+        // pass p runs its edge strips on the high-priority halo stream, followed
+        // there by pack -> NCCL send/recv -> unpack; the interior strips run on the
+        // pass stream and need only pass p-1 (edge + interior), never the halo, so
+        // the exchange of pass p overlaps the interior of pass p+1.  In-process
+        // slab groups launch the same two CTA sets one after the other.
+        const bool split = !ctx->use_tile && (ctx->world > 1 || ctx->comm) && ctx->n_edge > 0 &&
+                           ctx->n_edge < ctx->n_split && !getenv("STS_NO_SPLIT");
+        const bool overlap = split && n == 1 && ctx->comm;
+        if (overlap) {
+            if (!ctx->hstream) {
+                int lo = 0, hi = 0;
+                CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+                CU(cudaStreamCreateWithPriority(&ctx->hstream, cudaStreamNonBlocking, hi));
+                for (cudaEvent_t* e : {&ctx->ev_a[0], &ctx->ev_a[1], &ctx->ev_b, &ctx->ev_s, &ctx->ev_h})
+                    CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+            }
+            CU(cudaEventRecord(ctx->ev_s, st));                   // red reset, explicit planes, last step
+            CU(cudaStreamWaitEvent(ctx->hstream, ctx->ev_s, 0));
+        }
         for (int it = 0; it < ctx->sch.max_passes; it++) {
             for (int r = 0; r < n; r++) {
                 sts_ctx* c = cs[r];
@@ -1083,26 +1139,58 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 k.u_o = c->snap[old[r]].u; k.v_o = c->snap[old[r]].v; k.p_o = c->snap[old[r]].p; k.T_o = c->snap[old[r]].T;
                 k.u_w = c->snap[nw[r]].u; k.v_w = c->snap[nw[r]].v; k.p_w = c->snap[nw[r]].p; k.T_w = c->snap[nw[r]].T;
                 k.red = c->red + (size_t)it * 9;
-                prof_begin(c, 0);
                 if (c->use_tile) {
+                    prof_begin(c, 0);
                     const dim3 grid((c->nloc + TX - 1) / TX, (c->ny + TY - 1) / TY);
                     pass<<<grid, NT, smem, st>>>(k);
+                    prof_end(c);
+                    c->launches++;
+                } else if (split) {
+                    MarchParams ma = make_march(c, k), mb = ma;
+                    ma.order = c->cta_split;
+                    ma.seg = c->edge_seg;
+                    mb.order = c->cta_split + c->n_edge;
+                    cudaStream_t as = overlap ? c->hstream : st;
+                    if (overlap && it > 0) CU(cudaStreamWaitEvent(as, c->ev_b, 0));   // pass it-1 complete
+                    prof_begin(c, 0);
+                    march<<<c->n_edge, MX, sizeof(MarchSmem), as>>>(ma);
+                    if (overlap) CU(cudaEventRecord(c->ev_a[it & 1], as));
+                    march<<<c->n_split - c->n_edge, MX, sizeof(MarchSmem), st>>>(mb);
+                    if (overlap) {
+                        CU(cudaStreamWaitEvent(st, c->ev_a[it & 1], 0));   // the pass ends with both sets
+                        prof_end(c);
+                        CU(cudaEventRecord(c->ev_b, st));
+                        sts_status e = halo_pack(c, c->snap[nw[r]], as);
+                        if (!e) e = halo_nccl(c, as);
+                        if (!e) e = halo_unpack(c, c->snap[nw[r]], as);
+                        if (e) return e;
+                    } else {
+                        prof_end(c);
+                    }
+                    c->launches += 2;
                 } else {
+                    prof_begin(c, 0);
                     const dim3 mgrid(c->march_nstrips * c->march_nseg);
                     march<<<mgrid, MX, sizeof(MarchSmem), st>>>(make_march(c, k));
+                    prof_end(c);
+                    c->launches++;
                 }
-                prof_end(c);
-                c->launches++;
                 CU(cudaGetLastError());
                 which[r] = nw[r];
             }
-            sts_status e = exchange_group(cs, n, which.data(), st);
-            if (e) return e;
+            if (!overlap) {
+                sts_status e = exchange_group(cs, n, which.data(), st);
+                if (e) return e;
+            }
             passes++;
             last_it = it;
             for (int r = 0; r < n; r++) { old[r] = nw[r]; nw[r] = (nw[r] == a[r]) ? b[r] : a[r]; }
             if (tolmode && passes >= ctx->sch.min_passes) {
-                e = gather_red(cs, n, it, red, st);
+                if (overlap) {                                    // the halo of this pass too
+                    CU(cudaEventRecord(ctx->ev_h, ctx->hstream));
+                    CU(cudaStreamWaitEvent(st, ctx->ev_h, 0));
+                }
+                sts_status e = gather_red(cs, n, it, red, st);
                 if (e) return e;
                 for (int r = 0; r < n; r++) cs[r]->cur = old[r];
                 e = finish_residuals(ctx, red);
@@ -1111,6 +1199,10 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 const double* rs = ctx->stats.res;
                 if (rs[0] < ctx->sch.tol && rs[1] < ctx->sch.tol && rs[2] < ctx->sch.tol && rs[3] < ctx->sch.tol) { conv = true; break; }
             }
+        }
+        if (overlap) {                                            // join the halo stream
+            CU(cudaEventRecord(ctx->ev_h, ctx->hstream));
+            CU(cudaStreamWaitEvent(st, ctx->ev_h, 0));
         }
         for (int r = 0; r < n; r++) {
             sts_ctx* c = cs[r];

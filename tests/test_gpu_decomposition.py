@@ -60,6 +60,47 @@ def test_slabs_bitwise(S, variant, k):
         assert np.array_equal(a, got[f]), (f, np.abs(a - got[f]).max())
 
 
+@pytest.mark.parametrize("variant", ["implicit_upwind", "explicit_tvd"])
+@pytest.mark.parametrize("nx", [754, 1002])
+def test_slabs_split_launch_bitwise(S, variant, nx):
+    """Slabs wide enough for >= 3 strips of 125 columns: each pass launches the
+    edge-strip CTAs and the interior CTAs separately (the multi-GPU overlap
+    split).  nx = 754 gives slabs of 377 = 3 x 125 + 2 columns, whose last strip
+    owns 2 columns, so the strip before it also reads ghost columns and must be
+    an edge strip.  Still bit-identical to one slab."""
+    case = W.channel(nx, 24, spacing=0.25, variant=variant, passes=3,
+                     squares=[(5, 8, 4, 4), (370, 10, 6, 5), (nx - 9, 2, 4, 4)])
+    ref, got, _ = _slabs(S, case, 2, steps=2)
+    for f in FIELDS:
+        assert np.array_equal(ref.get_field(f), got[f]), f
+
+
+@pytest.mark.parametrize("variant", list(W.VARIANTS))
+@pytest.mark.parametrize("nx", [377, 500])
+def test_nccl_self_ring_overlap_bitwise(S, variant, nx):
+    """Periodic single rank with an NCCL communicator and >= 3 strips: the edge
+    strips and the halo (pack -> ncclSend/Recv -> unpack) run on the high-
+    priority halo stream while the interior strips of the next pass run on the
+    pass stream.  Bit-identical to the in-kernel wrap, in fixed-pass and in
+    tolerance mode (which joins the halo stream before every residual check)."""
+    case = W.periodic_box(nx, 20, 0.1, variant=variant, passes=4, dt=0.02, Kn=0.02,
+                          squares=[(3, 6, 4, 4), (nx - 6, 9, 4, 5)])
+    for tol in (0.0, 1e-3):
+        case = dict(case, tol=tol, min_passes=2)
+        a = S.Solver(case)
+        b = S.Solver(case, nccl_id=S.nccl_unique_id())
+        noise = W.perturbation(case, 11)
+        st = W.perturbed_state({f: a.get_field(f) for f in FIELDS}, noise, vscale=0.2)
+        for g in (a, b):
+            for f in ("p", "T", "u", "v"):
+                g.set_field(f, st[f])
+        sa = a.advance(3, check=False)[1]
+        sb = b.advance(3, check=False)[1]
+        for f in FIELDS:
+            assert np.array_equal(a.get_field(f), b.get_field(f)), (tol, f)
+        assert sa["res"] == sb["res"] and sa["passes_done"] == sb["passes_done"]
+
+
 def test_slabs_periodic_bitwise(S):
     """Periodic x with slabs: ring neighbours (rank 0 <-> rank k-1)."""
     case = W.c2(small=True, variant="implicit_tvd", passes=4)
