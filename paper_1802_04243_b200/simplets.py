@@ -14,6 +14,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsimplets.so")
+if os.environ.get("STS_LIB"):          # kernel A/B experiments (tools/ab.sh): another in-tree build
+    LIB_PATH = os.path.abspath(os.environ["STS_LIB"])
 
 STS_OK, STS_E_ARG, STS_E_CONFIG, STS_E_NONCONVERGED, STS_E_STATE, STS_E_CUDA, STS_E_COMM, STS_E_OOM = range(8)
 STATUS_NAMES = {0: "STS_OK", 1: "STS_E_ARG", 2: "STS_E_CONFIG", 3: "STS_E_NONCONVERGED", 4: "STS_E_STATE",
