@@ -108,6 +108,12 @@ struct sts_ctx {
     cudaStream_t hstream = nullptr;
     cudaEvent_t ev_a[2] = {nullptr, nullptr}, ev_b = nullptr, ev_s = nullptr, ev_h = nullptr;
     unsigned long long* red = nullptr;     // [max_passes][9]
+    // graph-driven loop 2 (tolerance mode, one context without NCCL): one CUDA
+    // graph per snapshot rotation, loop 2 as a conditional WHILE node
+    cudaGraphExec_t tol_exec[3] = {nullptr, nullptr, nullptr};
+    unsigned long long* red2 = nullptr;    // [2][9] residual slots (even / odd passes)
+    struct LoopState* d_ls = nullptr;      // device loop state
+    struct LoopState* h_ls = nullptr;      // pinned copy
     unsigned long long* h_red = nullptr;   // pinned, 9 entries
     double* stage = nullptr;               // device staging (global-shape field)
     size_t stage_elems = 0;
@@ -274,6 +280,11 @@ static march_fn march_table(int impl, int tvd)
     if (impl) return tvd ? march_kernel<true, true> : march_kernel<true, false>;
     return tvd ? march_kernel<false, true> : march_kernel<false, false>;
 }
+static march_fn march_graph_table(int impl, int tvd)
+{
+    if (impl) return tvd ? march_kernel<true, true, true> : march_kernel<true, false, true>;
+    return tvd ? march_kernel<false, true, true> : march_kernel<false, false, true>;
+}
 static march_fn conv_march_table(int tvd) { return tvd ? conv_march_kernel<true> : conv_march_kernel<false>; }
 
 static sts_status set_smem_attrs(sts_ctx* ctx)
@@ -283,7 +294,8 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
     const int bytes = (int)sizeof(Smem);
     pass_fn fns[6] = {pass_table(0, 0), pass_table(0, 1), pass_table(1, 0), pass_table(1, 1), conv_table(0), conv_table(1)};
     for (pass_fn f : fns) CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    march_fn mfs[4] = {march_table(0, 0), march_table(0, 1), march_table(1, 0), march_table(1, 1)};
+    march_fn mfs[8] = {march_table(0, 0), march_table(0, 1), march_table(1, 0), march_table(1, 1),
+                       march_graph_table(0, 0), march_graph_table(0, 1), march_graph_table(1, 0), march_graph_table(1, 1)};
     for (march_fn f : mfs)
         CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));
     for (int tvd = 0; tvd < 2; tvd++)
@@ -397,9 +409,11 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     if (forced > 0) {
         best_seg = forced;
     } else {
-        // candidate heights 32, 40, ... growing ~6 % per step (about 60 candidates)
-        for (int seg = std::max(1, std::min(ny, 32)); seg <= ny;
-             seg = std::max(seg + 8, (int)(seg * 1.06)) ) {
+        // candidate heights 8, 10, ..., 32, 40, ... growing ~6 % per step (about
+        // 70 candidates); short segments fill the SMs on the paper's small meshes
+        // (4032 x 200: 33 strips) at the price of 4 warm-up rows each
+        for (int seg = std::max(1, std::min(ny, 8)); seg <= ny;
+             seg = seg < 32 ? seg + 2 : std::max(seg + 8, (int)(seg * 1.06))) {
             const double ms = schedule(seg, false);
             if (ms < best * (1.0 - 1e-3)) { best = ms; best_seg = seg; }
         }
@@ -777,6 +791,9 @@ extern "C" void sts_destroy(sts_ctx* ctx)
     cudaFree(ctx->ue); cudaFree(ctx->ve); cudaFree(ctx->Te); cudaFree(ctx->stage); cudaFree(ctx->halo);
     cudaFree(ctx->ck); cudaFree(ctx->uk); cudaFree(ctx->vk); cudaFree(ctx->kind32); cudaFree(ctx->cta_order); cudaFree(ctx->cta_split); cudaFree(ctx->red);
     if (ctx->h_red) cudaFreeHost(ctx->h_red);
+    for (cudaGraphExec_t& g : ctx->tol_exec) if (g) cudaGraphExecDestroy(g);
+    cudaFree(ctx->red2); cudaFree(ctx->d_ls);
+    if (ctx->h_ls) cudaFreeHost(ctx->h_ls);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : {ctx->ev_a[0], ctx->ev_a[1], ctx->ev_b, ctx->ev_s, ctx->ev_h}) if (e) cudaEventDestroy(e);
     if (ctx->hstream) cudaStreamDestroy(ctx->hstream);
@@ -1059,6 +1076,166 @@ static sts_status gather_red(sts_ctx** cs, int n, int it, unsigned long long* ou
     return STS_OK;
 }
 
+// ------------------------------------------------------------- graph-driven loop 2
+// Tolerance mode on one context without NCCL: the loop-2 convergence test runs
+// on the device, so a whole time step is one CUDA graph launch and one 100-byte
+// read-back, instead of a host round trip per pass (the paper reads the maximum
+// residuals back after every pass).  Graph of snapshot rotation n1
+// (a = n1+1, b = n1+2 mod 3):
+//   zero slots + loop state; [explicit planes]; pass(n1 -> a); check;
+//   WHILE(cond) { pass(a -> b); check; pass(b -> a); check }
+// A pass that finds the loop finished returns at once (MarchParams.done), so the
+// second pass of a body iteration is a no-op when the first one converged.  The
+// check applies exactly the host's test (finish_residuals + the tol comparison,
+// same fp64 operations), so both drivers take identical pass counts.
+struct LoopState {
+    int passes, done, conv, checked;
+    unsigned long long red[9];   // residual slots of the last checked pass
+};
+
+__global__ void loop_check_kernel(unsigned long long* slot, LoopState* ls, cudaGraphConditionalHandle h,
+                                  int min_passes, int max_passes, double tol)
+{
+    if (threadIdx.x != 0) return;
+    if (ls->done) { cudaGraphSetConditional(h, 0); return; }
+    const int passes = ls->passes + 1;
+    ls->passes = passes;
+    bool done = passes >= max_passes;
+    if (passes >= min_passes) {
+        double v[7];
+        bool bad = slot[7] != 0;
+        for (int q = 0; q < 7; q++) {
+            v[q] = __longlong_as_double((long long)slot[q]);
+            if (!(v[q] == v[q]) || isinf(v[q])) bad = true;
+        }
+        for (int q = 0; q < 9; q++) ls->red[q] = slot[q];
+        ls->checked = 1;
+        const double vel = v[4], pm = v[5], Tm = v[6];
+        const double r0 = vel > 0 ? v[0] / vel : v[0], r1 = vel > 0 ? v[1] / vel : v[1];
+        const double r2 = pm > 0 ? v[2] / pm : v[2], r3 = Tm > 0 ? v[3] / Tm : v[3];
+        if (bad) done = true;
+        else if (r0 < tol && r1 < tol && r2 < tol && r3 < tol) { ls->conv = 1; done = true; }
+    }
+    for (int q = 0; q < 9; q++) slot[q] = 0;   // re-armed for the pass two later
+    ls->done = done ? 1 : 0;
+    cudaGraphSetConditional(h, done ? 0u : 1u);
+}
+
+static bool tol_graph_ok(const sts_ctx* c)
+{
+    return c->sch.tol > 0 && c->world == 1 && !c->comm && !c->use_tile && !c->profiling && !getenv("STS_NO_GRAPH");
+}
+
+#define CG(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
+    if (cap) { cudaGraph_t g_ = nullptr; cudaStreamEndCapture(cap, &g_); if (g_) cudaGraphDestroy(g_); cudaStreamDestroy(cap); } \
+    if (cap2) { cudaGraph_t g_ = nullptr; cudaStreamEndCapture(cap2, &g_); cudaStreamDestroy(cap2); } \
+    return fail(c, STS_E_CUDA, std::string("graph build: ") + cudaGetErrorString(e_)); } } while (0)
+
+static sts_status build_tol_graph(sts_ctx* c, int n1)
+{
+    cudaStream_t cap = nullptr, cap2 = nullptr;
+    const int impl = c->sch.time == STS_IMPLICIT, tvd = c->sch.space == STS_TVD_VANLEER;
+    const int a = (n1 + 1) % 3, b = (n1 + 2) % 3;
+    if (!c->red2) {
+        CG(cudaMalloc(&c->red2, 18 * sizeof(unsigned long long)));
+        CG(cudaMalloc(&c->d_ls, sizeof(LoopState)));
+        CG(cudaMallocHost(&c->h_ls, sizeof(LoopState)));
+    }
+    CG(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    CG(cudaStreamCreateWithFlags(&cap2, cudaStreamNonBlocking));
+    Params k = make_params(c);
+    k.u_1 = c->snap[n1].u; k.v_1 = c->snap[n1].v; k.p_1 = c->snap[n1].p; k.T_1 = c->snap[n1].T;
+    k.ue = c->ue; k.ve = c->ve; k.Te = c->Te;
+    march_fn march = march_graph_table(impl, tvd);
+    const dim3 mgrid(c->march_nstrips * c->march_nseg);
+    auto pass = [&](int o, int w, int sl, cudaStream_t s) {
+        Params q = k;
+        q.u_o = c->snap[o].u; q.v_o = c->snap[o].v; q.p_o = c->snap[o].p; q.T_o = c->snap[o].T;
+        q.u_w = c->snap[w].u; q.v_w = c->snap[w].v; q.p_w = c->snap[w].p; q.T_w = c->snap[w].T;
+        q.red = c->red2 + sl * 9;
+        MarchParams m = make_march(c, q);
+        m.done = &c->d_ls->done;
+        march<<<mgrid, MX, sizeof(MarchSmem), s>>>(m);
+    };
+    const int mn = c->sch.min_passes, mx = c->sch.max_passes;
+    const double tol = c->sch.tol;
+
+    CG(cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed));
+    cudaStreamCaptureStatus cst;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CG(cudaStreamGetCaptureInfo(cap, &cst, nullptr, &cg, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    CG(cudaGraphConditionalHandleCreate(&h, cg, 1, cudaGraphCondAssignDefault));
+    CG(cudaMemsetAsync(c->red2, 0, 18 * sizeof(unsigned long long), cap));
+    CG(cudaMemsetAsync(c->d_ls, 0, sizeof(LoopState), cap));
+    if (!impl) {                                  // a1: explicit planes of this step
+        Params q = k;
+        q.ue_w = c->ue; q.ve_w = c->ve; q.Te_w = c->Te;
+        conv_march_table(tvd)<<<mgrid, MX, sizeof(ConvSmem), cap>>>(make_march(c, q));
+    }
+    pass(n1, a, 0, cap);
+    loop_check_kernel<<<1, 32, 0, cap>>>(c->red2, c->d_ls, h, mn, mx, tol);
+    CG(cudaGetLastError());
+    CG(cudaStreamGetCaptureInfo(cap, &cst, nullptr, &cg, &deps, &nd));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn;
+    CG(cudaGraphAddNode(&cn, cg, deps, nd, &cp));
+    CG(cudaStreamUpdateCaptureDependencies(cap, &cn, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CG(cudaStreamBeginCaptureToGraph(cap2, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    pass(a, b, 1, cap2);
+    loop_check_kernel<<<1, 32, 0, cap2>>>(c->red2 + 9, c->d_ls, h, mn, mx, tol);
+    pass(b, a, 0, cap2);
+    loop_check_kernel<<<1, 32, 0, cap2>>>(c->red2, c->d_ls, h, mn, mx, tol);
+    CG(cudaGetLastError());
+    cudaGraph_t bo = nullptr;
+    CG(cudaStreamEndCapture(cap2, &bo));
+    cudaGraph_t g = nullptr;
+    CG(cudaStreamEndCapture(cap, &g));
+    cudaStream_t keep = cap;
+    cap = nullptr;                                // capture ended: CG must not end it again
+    cudaError_t e = cudaGraphInstantiate(&c->tol_exec[n1], g, 0);
+    cudaGraphDestroy(g);
+    cudaStreamDestroy(keep);
+    cudaStreamDestroy(cap2);
+    cap2 = nullptr;
+    if (e != cudaSuccess) return fail(c, STS_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    return STS_OK;
+}
+#undef CG
+
+// One time step of loop 1 through the graph of the current rotation.
+static sts_status graph_step(sts_ctx* ctx, bool* conv)
+{
+    sts_ctx* const c = ctx;
+    const int n1 = c->cur, a = (n1 + 1) % 3, b = (n1 + 2) % 3;
+    if (!c->tol_exec[n1]) {
+        sts_status e = build_tol_graph(c, n1);
+        if (e) return e;
+    }
+    CU(cudaGraphLaunch(c->tol_exec[n1], c->stream));
+    CU(cudaMemcpyAsync(c->h_ls, c->d_ls, sizeof(LoopState), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    const LoopState ls = *c->h_ls;
+    c->launches += 2 * ls.passes + (c->sch.time == STS_EXPLICIT ? 1 : 0);
+    c->cur = (ls.passes & 1) ? a : b;             // pass 1 writes a, pass 2 b, ...
+    *conv = ls.conv != 0;
+    if (ls.checked) {
+        sts_status e = finish_residuals(c, ls.red);
+        if (e) return e;
+    }
+    c->stats.steps_done++;
+    c->stats.passes_done += ls.passes;
+    c->stats.converged = ls.conv ? 1 : 0;
+    return STS_OK;
+}
+
 // Loop 1 x loop 2 for a group of slab contexts advanced in lockstep (n == 1
 // for the usual one-context-per-process case).
 static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
@@ -1075,6 +1252,17 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
     int last_it = -1;
     std::vector<int> n1(n), a(n), b(n), old(n), nw(n), which(n);
     unsigned long long red[9];
+    if (n == 1 && tol_graph_ok(ctx)) {
+        for (int step = 0; step < n_steps; step++) {
+            bool conv = false;
+            sts_status e = graph_step(ctx, &conv);
+            if (e) { if (out) *out = ctx->stats; return e; }
+            if (!conv) status = STS_E_NONCONVERGED;
+        }
+        if (out) *out = ctx->stats;
+        if (status == STS_E_NONCONVERGED) return fail(ctx, status, "loop 2 reached max_passes without convergence");
+        return STS_OK;
+    }
     for (int step = 0; step < n_steps; step++) {
         for (int r = 0; r < n; r++) {
             sts_ctx* c = cs[r];

@@ -48,6 +48,7 @@ struct MarchParams {
     int nstrips;                 // strips per row of CTAs
     const int* order;            // CTA schedule (longest first); blockIdx.x -> strip + nstrips * segment
     double inv_dx, inv_dy, CT1_dydx, CT1_dxdy, B_dydx, B_dxdy, c_t, dV, A_dy, A_dx, half_dV;
+    const int* done;             // graph-driven loop 2 (tolerance mode): loop finished -> the pass is a no-op
 };
 
 // fp64 reciprocal: MUFU.RCP64H seed + 2 Newton steps (~1 ulp), no slow path.
@@ -621,12 +622,13 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
     }
 }
 
-template <bool IMPL, bool TVD>
+template <bool IMPL, bool TVD, bool GRAPH = false>
 __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MarchSmem& s = *reinterpret_cast<MarchSmem*>(smem_raw);
     const Params& k = m.k;
+    if (GRAPH && *m.done) return;                       // converged earlier in this graph launch
     const int t = threadIdx.x;
     const int lc = t + 2;                               // ring column of this thread's column
     const int cta = m.order[blockIdx.x];

@@ -1,0 +1,115 @@
+"""Graph-driven loop 2 (tolerance mode): one CUDA graph per time
+step with loop 2 as a conditional WHILE node and the convergence test on the
+device, against the host-driven loop (STS_NO_GRAPH=1, one residual read-back
+per pass as the paper does) and against the CPU oracle.
+
+Both drivers run the same pass kernels and apply the same test (finish_residuals
++ `res < tol`, reading R35), so pass counts, residuals and fields must agree bit
+for bit; the oracle's pass count must agree too (fixed by the tolerance, which
+is chosen well away from the residual of any pass)."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_1802_04243_b200 import workloads as W
+from tests.parity_util import FIELDS, rel_errors, seeded_pair
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    import torch
+    assert torch.cuda.is_available()
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1802_04243_b200 import simplets
+    return simplets
+
+
+def _run(S, case, steps, graph, seed=3):
+    old = os.environ.pop("STS_NO_GRAPH", None)
+    if not graph:
+        os.environ["STS_NO_GRAPH"] = "1"
+    try:
+        g = S.Solver(case)
+        base = {k: g.get_field(k) for k in ("u", "v", "p", "T")}
+        st_in = W.perturbed_state(base, W.perturbation(case, seed=seed), vscale=0.05)
+        for k in ("p", "T", "u", "v"):
+            g.set_field(k, st_in[k])
+        out = []
+        for _ in range(steps):                 # one call per step: per-step pass counts
+            st, stats = g.advance(1, check=False)
+            out.append((st, stats["passes_done"], tuple(stats["res"]), stats["converged"]))
+        return out, {k: g.get_field(k) for k in FIELDS}
+    finally:
+        os.environ.pop("STS_NO_GRAPH", None)
+        if old is not None:
+            os.environ["STS_NO_GRAPH"] = old
+
+
+def _same(a, b):
+    (sa, fa), (sb, fb) = a, b
+    assert sa == sb, (sa, sb)
+    for k in FIELDS:
+        assert np.array_equal(fa[k], fb[k]), k
+
+
+@pytest.mark.parametrize("variant", list(W.VARIANTS))
+def test_graph_loop_matches_host_loop(S, variant):
+    """Converging steps (pass counts of both parities) -- bitwise equal."""
+    case = W.c1_small(variant, passes=80)
+    case["tol"] = 1e-6
+    a = _run(S, case, 3, graph=True)
+    b = _run(S, case, 3, graph=False)
+    _same(a, b)
+    assert all(c == 1 for _, _, _, c in a[0]), a[0]
+    assert a[0][0][1] > 1
+
+
+def test_graph_loop_nonconverged_and_min_passes(S):
+    """max_passes reached (STS_E_NONCONVERGED) and min_passes > 1, both drivers."""
+    case = W.c1_small("implicit_tvd", passes=5)
+    case["tol"] = 1e-30
+    a = _run(S, case, 2, graph=True)
+    b = _run(S, case, 2, graph=False)
+    _same(a, b)
+    assert all(st == S.STS_E_NONCONVERGED and c == 0 for st, _, _, c in a[0])
+    assert [p for _, p, _, _ in a[0]] == [5, 10]
+    case = W.c1_small("explicit_upwind", passes=9)
+    case["tol"] = 1.0                         # converged at the first check
+    case["min_passes"] = 4
+    a = _run(S, case, 2, graph=True)
+    b = _run(S, case, 2, graph=False)
+    _same(a, b)
+    assert [p for _, p, _, _ in a[0]] == [4, 8]
+
+
+def test_graph_loop_vs_oracle(S, oracle_mod):
+    """Same pass count as the oracle's loop 2 and fields within the parity bar."""
+    case = W.c1_small("implicit_upwind", passes=200)
+    case["tol"] = 1e-9
+    g, o = seeded_pair(S, oracle_mod, case, seed=4)
+    done = 0
+    for _ in range(2):                         # the oracle reports the passes of its last step
+        st, stats = g.advance(1)
+        ost, ores, opasses = o.advance(1)
+        assert st == 0 and ost == 0 and stats["converged"] == 1
+        assert stats["passes_done"] - done == opasses, (stats["passes_done"] - done, opasses)
+        done = stats["passes_done"]
+    err = rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), o.get_map(0) == 0)
+    assert max(err.values()) <= 1e-8, err
+
+
+def test_graph_loop_bad_state(S):
+    """A non-positive temperature stops the graph loop with STS_E_STATE."""
+    case = W.c1_small("implicit_upwind", passes=20)
+    case["tol"] = 1e-12
+    g = S.Solver(case)
+    T = g.get_field("T")
+    T[5, 3] = -1.0
+    g.set_field("T", T)
+    st, stats = g.advance(1, check=False)
+    assert st == S.STS_E_STATE
+    assert stats["bad_cell"] >= 0
