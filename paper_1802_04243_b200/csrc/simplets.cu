@@ -341,7 +341,7 @@ static MarchParams make_march(const sts_ctx* c, const Params& k)
 // CTA (it advances at the pace of its slowest warp, barriers every stage): a
 // warp whose 32 points are all regular costs 1, an all-general warp 1.35, a
 // mixed warp 2.35 (both instances).  For each candidate segment count the
-// CTAs (+4 warm-up rows each) are list-scheduled longest-first onto the
+// CTAs (+WARM = 3 warm-up rows each) are list-scheduled longest-first onto the
 // resident slots (148 SMs x CTAs/SM from the occupancy API); the count with
 // the smallest makespan wins, and the same longest-first order is the launch
 // order (blockIdx.x -> CTA), so the boundary CTAs (inlet, squares, walls)
@@ -411,7 +411,7 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     } else {
         // candidate heights 8, 10, ..., 32, 40, ... growing ~6 % per step (about
         // 70 candidates); short segments fill the SMs on the paper's small meshes
-        // (4032 x 200: 33 strips) at the price of 4 warm-up rows each
+        // (4032 x 200: 33 strips) at the price of 3 warm-up rows each
         for (int seg = std::max(1, std::min(ny, 8)); seg <= ny;
              seg = seg < 32 ? seg + 2 : std::max(seg + 8, (int)(seg * 1.06))) {
             const double ms = schedule(seg, false);

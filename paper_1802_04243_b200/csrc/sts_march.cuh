@@ -26,7 +26,7 @@
 //    the cell alone (decomposition-invariant);
 //  - divisions become MUFU reciprocals + Newton steps; the mesh constants
 //    (dy/dx, dx dy/(2 dt), ...) are precomputed on the host.
-// A segment starts 4 rows early (warm-up) so that every carried quantity is
+// A segment starts 3 rows early (warm-up) so that every carried quantity is
 // exact when its first output row is reached.
 #pragma once
 
@@ -38,7 +38,9 @@ constexpr int MX = 128;          // threads per CTA = columns handled per strip
 constexpr int MW = MX - 3;       // owned columns per strip
 constexpr int RW = MX + 4;       // ring row width (global columns I0-4 .. I0-4+RW)
 constexpr int RS = 6;            // ring slots
-constexpr int WARM = 4;          // warm-up rows per segment
+constexpr int WARM = 3;          // warm-up rows per segment: the longest carried chain is
+                                 // E(J0) <- D(J0-1) <- C(J0-2) <- A(J0-3); 2 rows fail the bitwise
+                                 // segmentation tests, 3 pass them for every variant down to 1-row segments
 constexpr uint32_t REG_BIT = 1u << 24;   // kind-word bit: the +-3 window is all fluid
 
 struct MarchParams {

@@ -134,10 +134,11 @@ def test_nccl_transport_self_ring(S, variant):
     assert sa["res"] == sb["res"]
 
 
-@pytest.mark.parametrize("seg", ["3", "5", "17"])
-def test_segments_bitwise(S, seg):
+@pytest.mark.parametrize("variant", list(W.VARIANTS))
+@pytest.mark.parametrize("seg", ["1", "3", "5", "17"])
+def test_segments_bitwise(S, seg, variant):
     """The y-march segmentation (warm-up rows) does not change a single bit."""
-    case = W.c1("implicit_tvd", passes=4)
+    case = W.c1(variant, passes=4)
     base = S.Solver(case)
     base.advance(3)
     ref = {f: base.get_field(f) for f in FIELDS}
