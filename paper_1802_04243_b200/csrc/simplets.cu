@@ -334,6 +334,8 @@ static MarchParams make_march(const sts_ctx* c, const Params& k)
     m.B_dydx = c->B * dy / dx; m.B_dxdy = c->B * dx / dy;
     m.c_t = dx * dy / (2.0 * dt); m.dV = dx * dy; m.half_dV = 0.5 * dx * dy;
     m.A_dy = c->A * dy; m.A_dx = c->A * dx;
+    m.B43_dydx = 4.0 / 3.0 * m.B_dydx; m.B43_dxdy = 4.0 / 3.0 * m.B_dxdy;
+    m.q_dx = 0.25 / dx; m.q_dy = 0.25 / dy;
     return m;
 }
 

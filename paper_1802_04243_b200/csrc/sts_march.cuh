@@ -50,6 +50,8 @@ struct MarchParams {
     int nstrips;                 // strips per row of CTAs
     const int* order;            // CTA schedule (longest first); blockIdx.x -> strip + nstrips * segment
     double inv_dx, inv_dy, CT1_dydx, CT1_dxdy, B_dydx, B_dxdy, c_t, dV, A_dy, A_dx, half_dV;
+    double B43_dydx, B43_dxdy;   // 4/3 B dy/dx, 4/3 B dx/dy (normal viscous links)
+    double q_dx, q_dy;           // 1/(4 dx), 1/(4 dy) (bilinear differences in S^T_c)
     const int* done;             // graph-driven loop 2 (tolerance mode): loop finished -> the pass is a no-op
 };
 
@@ -187,15 +189,31 @@ __device__ __forceinline__ void ring_issue(MarchSmem& s, const MarchParams& m, i
 {
     ring_issue(s.ring[sl], m, I0, j);
 }
-// rho = p/T (Eq. pl5), Gamma = sqrt(T) (Eq. pl37) of ring row j (the explicit
-// planes need no Gamma)
+// 1/sqrt(x), x > 0: MUFU seed + 2 Newton steps (~1 ulp)
+__device__ __forceinline__ double frsqrt(double x)
+{
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    y = y * fma(-hx * y, y, 1.5);
+    y = y * fma(-hx * y, y, 1.5);
+    return y;
+}
+// rho = p/T (Eq. pl5), Gamma = sqrt(T) (Eq. pl37) of ring row j from one
+// reciprocal square root y = T^(-1/2): Gamma = T y, rho = p y^2 (~2 ulp; the
+// explicit planes need no Gamma)
 template <bool WITH_GAMMA = true>
 __device__ __forceinline__ void ring_derive(RingRow& r)
 {
     for (int lc = threadIdx.x; lc < RW; lc += MX) {
         const double Tv = r.T[lc];
-        r.R[lc] = fdiv(r.P[lc], Tv);
-        if (WITH_GAMMA) r.G[lc] = fsqrt(Tv);
+        if (WITH_GAMMA) {
+            const double y = frsqrt(Tv);
+            r.R[lc] = r.P[lc] * (y * y);
+            r.G[lc] = Tv * y;
+        } else {
+            r.R[lc] = fdiv(r.P[lc], Tv);
+        }
     }
 }
 template <bool WITH_GAMMA = true>
@@ -307,7 +325,7 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         if (cF<REG>(kw0)) {
             const double ub = 0.5 * (R0.U[lc] + R0.U[lc + 1]);
             Fb = R0.R[lc] * ub * dy;
-            const double D = 4.0 / 3.0 * m.B_dydx * R0.G[lc];
+            const double D = m.B43_dydx * R0.G[lc];
             double ps = 0.0;
             if (IMPL && TVD && uA<REG>(R0.KK[lc - 1]) && uA<REG>(kw0) && uA<REG>(R0.KK[lc + 1]) &&
                 uA<REG>(R0.KK[lc + 2]))
@@ -334,7 +352,7 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
     if (cF<REG>(kw1)) {
         const double vb = 0.5 * (Ra.V[lc] + Rb.V[lc]);
         v.FbN = Ra.R[lc] * vb * dx;
-        const double D = 4.0 / 3.0 * m.B_dxdy * Ra.G[lc];
+        const double D = m.B43_dxdy * Ra.G[lc];
         double ps = 0.0;
         if (IMPL && TVD && vA<REG>(kw0) && vA<REG>(kw1) && vA<REG>(Rb.KK[lc]) && vA<REG>(Rc.KK[lc]))
             ps = psi_f(R0.V[lc], Ra.V[lc], Rb.V[lc], Rc.V[lc], vb);
@@ -413,11 +431,10 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         // S^T_c, Eq. pl29 (R4 bilinear = 4-point mean; R9 sign)
         const double dudx = (R0.U[lc + 1] - R0.U[lc]) * m.inv_dx;
         const double dvdy = (Ra.V[lc] - R0.V[lc]) * m.inv_dy;
-        const double vE = 0.25 * (R0.V[lc] + R0.V[lc + 1] + Ra.V[lc] + Ra.V[lc + 1]);
-        const double vW = 0.25 * (R0.V[lc - 1] + R0.V[lc] + Ra.V[lc - 1] + Ra.V[lc]);
-        const double uN = 0.25 * (R0.U[lc] + R0.U[lc + 1] + Ra.U[lc] + Ra.U[lc + 1]);
-        const double uS = 0.25 * (Rm.U[lc] + Rm.U[lc + 1] + R0.U[lc] + R0.U[lc + 1]);
-        const double shear = (vE - vW) * m.inv_dx + (uN - uS) * m.inv_dy;
+        // dv/dx + du/dy from the bilinear face values (R4): v_E - v_W and u_N - u_S
+        // as one difference each (the shared corner values cancel)
+        const double shear = ((R0.V[lc + 1] + Ra.V[lc + 1]) - (R0.V[lc - 1] + Ra.V[lc - 1])) * m.q_dx
+                           + ((Ra.U[lc] + Ra.U[lc + 1]) - (Rm.U[lc] + Rm.U[lc + 1])) * m.q_dy;
         const double div = dudx + dvdy;
         const double Sc = (k.CT2 * gP * (2.0 * (dudx * dudx + dvdy * dvdy) + shear * shear - 2.0 / 3.0 * div * div)
                            + k.pw_sign * k.CT3 * R0.P[lc] * div) * m.dV;
