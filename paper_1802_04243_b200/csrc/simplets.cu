@@ -1247,7 +1247,15 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
     cudaStream_t st = ctx->stream;
     const int impl = ctx->sch.time == STS_IMPLICIT, tvd = ctx->sch.space == STS_TVD_VANLEER;
     pass_fn pass = pass_table(impl, tvd);
-    march_fn march = march_table(impl, tvd);
+    // test hook: the graph instances (early exit on a zero `done` flag) launched from the stream
+    const bool gk = getenv("STS_GRAPH_KERNEL") != nullptr && !ctx->use_tile;
+    march_fn march = gk ? march_graph_table(impl, tvd) : march_table(impl, tvd);
+    if (gk && !ctx->red2) {
+        CU(cudaMalloc(&ctx->red2, 18 * sizeof(unsigned long long)));
+        CU(cudaMalloc(&ctx->d_ls, sizeof(LoopState)));
+        CU(cudaMallocHost(&ctx->h_ls, sizeof(LoopState)));
+        CU(cudaMemset(ctx->d_ls, 0, sizeof(LoopState)));
+    }
     const size_t smem = sizeof(Smem);
     const bool tolmode = ctx->sch.tol > 0;
     sts_status status = STS_OK;
@@ -1361,7 +1369,9 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 } else {
                     prof_begin(c, 0);
                     const dim3 mgrid(c->march_nstrips * c->march_nseg);
-                    march<<<mgrid, MX, sizeof(MarchSmem), st>>>(make_march(c, k));
+                    MarchParams mk = make_march(c, k);
+                    if (gk) mk.done = &c->d_ls->done;
+                    march<<<mgrid, MX, sizeof(MarchSmem), st>>>(mk);
                     prof_end(c);
                     c->launches++;
                 }

@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MarchSmem& s = *reinterpret_cast<MarchSmem*>(smem_raw);
     const Params& k = m.k;
-    if (GRAPH && *m.done) return;                       // converged earlier in this graph launch
+    if (GRAPH && *(volatile const int*)m.done) return;  // converged earlier in this graph launch (CTA-uniform)
     const int t = threadIdx.x;
     const int lc = t + 2;                               // ring column of this thread's column
     const int cta = m.order[blockIdx.x];
@@ -675,6 +675,7 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     ring_derive(*p0);
     ring_derive(*pa);
     ring_derive(*pb);
+    __syncthreads();        // rho, Gamma of rows js-1 .. js+2 before step js reads neighbours' elements
 
     // ---- n-1 / explicit-plane values of this thread's column.  Upwind variants
     // prefetch them one row step ahead through registers; the TVD variants
