@@ -219,7 +219,11 @@ def run_ours(args):
 
     case = bench_case(args, world)
     stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize(dev)
+    free0 = torch.cuda.mem_get_info(dev)[0]
     g = S.Solver(case, rank=rank, world=world, device=local, nccl_id=nccl_id, stream=stream.cuda_stream)
+    torch.cuda.synchronize(dev)
+    lib_bytes = free0 - torch.cuda.mem_get_info(dev)[0]      # device memory the library holds for this rank
     nfv_rank = g.shape("p")[2] * case["ny"]
     passes = case["max_passes"]
     kind = "implicit" if case["time"] == W.IMPLICIT else "explicit"
@@ -318,6 +322,9 @@ def run_ours(args):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(prof["launches"]), "clocks": clk.summary(),
             "hbm_gbs_algorithmic_step": value / world * BYTES_PER_FVU[kind] / 1e9,
+            # resident device memory per FV (the paper: 5.9 M FVs per GB, P:708 = 169 B/FV)
+            "memory": {"device_bytes_per_gpu": int(lib_bytes), "bytes_per_fv": lib_bytes / nfv_rank,
+                       "paper_bytes_per_fv": 1e9 / 5.9e6},
         }
         print(json.dumps(line), flush=True)
     g.close()
