@@ -281,21 +281,40 @@ def run_ours(args):
                 "fp64_pipe_active_ncu": fp64_active}
 
     # e2e: through the public API with host (pinned) buffers, every step:
-    # H2D of the step's input state (u, v, p, T) + advance + D2H of the residual maxima
+    # H2D of the step's input state (u, v, p, T) + advance + D2H of the residual maxima.
+    # The inputs are double-buffered: the H2D copy of step s+1 runs on a copy
+    # stream while step s computes (the copy of step 0 is inside the timed region too).
     e2e = None
     if not args.no_e2e:
         names = ("u", "v", "p", "T")
         host = {k: torch.from_numpy(g.get_field(k)).pin_memory() for k in names}
-        devb = {k: torch.empty_like(host[k], device=dev) for k in names}
+        devb = [{k: torch.empty_like(host[k], device=dev) for k in names} for _ in range(2)]
         h2d = sum(h.numel() * 8 for h in host.values())
-        e_steps = max(1, min(args.steps, 5))
+        e_steps = max(2, min(args.steps, 6))
+        cstream = torch.cuda.Stream(dev)
+        copied = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
+
+        def h2d_copy(b):
+            with torch.cuda.stream(cstream):
+                for k in names:
+                    devb[b][k].copy_(host[k], non_blocking=True)
+                copied[b].record(cstream)
+
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(e_steps):
+        cstream.wait_event(e0)
+        h2d_copy(0)
+        for s in range(e_steps):
+            b = s % 2
+            stream.wait_event(copied[b])
             for k in names:
-                devb[k].copy_(host[k], non_blocking=True)
-                g.set_field_device(k, devb[k].data_ptr(), devb[k].numel())
+                g.set_field_device(k, devb[b][k].data_ptr(), devb[b][k].numel())
+            consumed[b].record(stream)
+            if s + 1 < e_steps:
+                cstream.wait_event(consumed[1 - b]) if s >= 1 else None
+                h2d_copy(1 - b)
             g.advance(1)          # reads back the 9 residual slots (72 B) to the host
         e1.record(stream)
         barrier()
@@ -304,7 +323,8 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": nfv_rank * world * passes * e_steps / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": 72 * world, "steps": e_steps}
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": 72 * world, "steps": e_steps,
+               "inputs": "pinned host state copied every step, double-buffered (copy of step s+1 overlaps step s)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
