@@ -36,7 +36,7 @@ namespace sts {
 
 constexpr int MX = 128;          // threads per CTA = columns handled per strip
 constexpr int MW = MX - 3;       // owned columns per strip
-constexpr int RW = MX + 4;       // ring row width (global columns I0-4 .. I0-4+RW)
+constexpr int RW = MX + 6;       // ring row width: columns I0-4-shift .. (TMA rows: 16-byte aligned, shift in {0,1})
 constexpr int RS = 6;            // ring slots
 constexpr int WARM = 3;          // warm-up rows per segment: the longest carried chain is
                                  // E(J0) <- D(J0-1) <- C(J0-2) <- A(J0-3); 2 rows fail the bitwise
@@ -113,10 +113,37 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem)
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+// ---- TMA (bulk async copy) rows with mbarrier completion
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, int parity)
+{
+    asm volatile("{\n\t.reg .pred P1;\n"
+                 "WAIT:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                 "\t@!P1 bra WAIT;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_row(void* dst, const void* src, unsigned bytes, unsigned long long* b)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
+
 struct RingRow {                 // one old-iterate row (slot-major: one base address per row)
     double U[RW], V[RW], P[RW], T[RW], R[RW], G[RW];
-    uint32_t KK[RW];
+    uint32_t KK[(RW + 3) / 4 * 4];   // padded: every slot (TMA destination) starts 16-byte aligned
 };
+static_assert(sizeof(RingRow) % 16 == 0 && (RW * 8) % 16 == 0, "TMA rows need 16-byte alignment");
 struct FluxRow {                 // face densities / fluxes of one row
     double RU[RW], FX[RW], FY[RW];   // (rho^v stays in registers: only the own column reads it)
 };
@@ -131,6 +158,7 @@ struct MarchSmem {
     double XUW[RW], XVW[RW], XVF[RW];
     double UH[RW], DU[RW];
     double PN[RW];               // p_new of row j (stages D-E): a row of its own, so no row-start barrier
+    unsigned long long mbar[RS]; // TMA completion barrier of each ring slot (u, v, p, T rows)
 };
 // resident CTAs per SM: 4 (128 registers, 16 warps) for every variant (implicit TVD
 // spills 12 B at 128 registers and is still 4 % faster than at 3 CTAs / 154 registers)
@@ -250,6 +278,62 @@ struct NM1 {                      // n-1 state / explicit planes at this thread'
     double T1c, u1c, v1n;         // T^{n-1}(i, j), u^{n-1}(i, j), v^{n-1}(i, j+1)
     double Tec, uec, ven;         // T^exp(i, j), u^exp(i, j), v^exp(i, j+1)
 };
+
+// Ring row r into slot sl (march kernel).  c0 = stored column of ring column 0,
+// even, so every row starts 16-byte aligned; `tma` = the CTA's window
+// [c0, c0 + RW) lies inside the stored columns.  Rows inside the channel are
+// four TMA bulk copies of RW doubles (u, v, p, T) issued by one thread and
+// completing on the slot's mbarrier, plus one 4-byte cp.async per element for
+// the packed kinds.  Every other row (beyond a channel wall, or a window that
+// leaves the stored columns) is filled by the threads exactly as ring_issue
+// does, and the issuing thread arrives on the mbarrier without bytes, so the
+// slot's phase advances either way.
+__device__ __forceinline__ void ring_issue_tma(MarchSmem& s, int sl, const MarchParams& m, int c0, bool tma, int r)
+{
+    const Params& k = m.k;
+    RingRow& R = s.ring[sl];
+    const int t = threadIdx.x;
+    const bool row_in = (unsigned)r < (unsigned)k.ny;
+    if (tma && row_in) {
+        const int base = r * k.pitch + c0;
+        if (t == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // earlier generic writes of the slot
+            mbar_expect_tx(&s.mbar[sl], 4u * RW * 8u);
+            tma_row(R.U, k.u_o + base, RW * 8, &s.mbar[sl]);
+            tma_row(R.V, k.v_o + base, RW * 8, &s.mbar[sl]);
+            tma_row(R.P, k.p_o + base, RW * 8, &s.mbar[sl]);
+            tma_row(R.T, k.T_o + base, RW * 8, &s.mbar[sl]);
+        }
+        for (int c = t; c < RW; c += MX) cp_async4(&R.KK[c], m.kind + base + c);
+    } else {
+        for (int c = t; c < RW; c += MX) {
+            const int li = c0 + c;
+            const bool col_ok = li >= 0 && li < k.pitch;
+            const int id = r * k.pitch + li;
+            if (row_in && col_ok) {
+                cp_async8(&R.U[c], k.u_o + id);
+                cp_async8(&R.V[c], k.v_o + id);
+                cp_async8(&R.P[c], k.p_o + id);
+                cp_async8(&R.T[c], k.T_o + id);
+                cp_async4(&R.KK[c], m.kind + id);
+            } else if (r == k.ny && col_ok) {          // top wall row: v = 0 (WALL), no cells
+                R.U[c] = k.u_wt;
+                cp_async8(&R.V[c], k.v_o + id);
+                R.P[c] = 1.0;
+                R.T[c] = 1.0;
+                cp_async4(&R.KK[c], m.kind + id);
+            } else {
+                R.U[c] = r < 0 ? k.u_wb : (r >= k.ny ? k.u_wt : 0.0);
+                R.V[c] = 0.0;
+                R.P[c] = 1.0;
+                R.T[c] = 1.0;
+                R.KK[c] = (uint32_t)CK_WALLY | ((uint32_t)FK_NONE << 8) | ((uint32_t)FK_NONE << 16);
+            }
+        }
+        if (t == 0) mbar_arrive(&s.mbar[sl]);
+    }
+    cp_commit();
+}
 
 // ================= stage A: row j+1 fluxes, link pieces =================
 template <bool IMPL, bool TVD, bool REG>
@@ -649,10 +733,21 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     const Params& k = m.k;
     if (GRAPH && *(volatile const int*)m.done) return;  // converged earlier in this graph launch (CTA-uniform)
     const int t = threadIdx.x;
-    const int lc = t + 2;                               // ring column of this thread's column
     const int cta = m.order[blockIdx.x];
     const int strip = cta % m.nstrips, segi = cta / m.nstrips;
     const int I0 = k.gi0 + strip * MW;                  // first owned column of the strip
+    // ring column 0 = stored column c0 (even: 16-byte aligned TMA rows); this
+    // thread's column sits at ring column lc
+    const int wbase = I0 - 4 - k.gi0 + OFF;
+    const int shift = wbase & 1;
+    const int c0 = wbase - shift;
+    const bool tma = c0 + RW <= k.pitch;
+    const int lc = t + 2 + shift;
+    if (t == 0) {
+        for (int q = 0; q < RS; q++) mbar_init(&s.mbar[q], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
     const int gi = I0 - 2 + t;                          // this thread's global column
     const int J0 = segi * m.seg;
     const int J1 = min(J0 + m.seg, k.ny);
@@ -664,13 +759,10 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     // here on, row j+4 is issued at the start of step j and lands before its B3);
     // ring slots of rows j-1 .. j+4, rotated by one per row step
     RingRow *pm = &s.ring[0], *p0 = &s.ring[1], *pa = &s.ring[2], *pb = &s.ring[3], *pc = &s.ring[4], *pd = &s.ring[5];
-    ring_issue(*pm, m, I0, js - 1);
-    ring_issue(*p0, m, I0, js);
-    ring_issue(*pa, m, I0, js + 1);
-    ring_issue(*pb, m, I0, js + 2);
-    ring_issue(*pc, m, I0, js + 3);
+    for (int q = 0; q < 5; q++) ring_issue_tma(s, q, m, c0, tma, js - 1 + q);   // row js-1+q -> slot q
     cp_wait_all();
     __syncthreads();
+    for (int q = 0; q < 4; q++) mbar_wait(&s.mbar[q], 0);
     ring_derive(*pm);
     ring_derive(*p0);
     ring_derive(*pa);
@@ -731,7 +823,11 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
             }
         }
 
-        ring_issue(*pd, m, I0, j + 4);
+        {   // row j+4 -> slot (j+5-js) mod RS (= pd); row j+3 (slot of pc) must have landed
+            const int q = j + 4 - js;
+            ring_issue_tma(s, (q + 1) % RS, m, c0, tma, j + 4);
+            mbar_wait(&s.mbar[q % RS], (q / RS) & 1);
+        }
         ring_derive(Rc);
         // per-point choice (a function of the cell alone, so any decomposition
         // gives bit-identical results); warps mixing both kinds run both
