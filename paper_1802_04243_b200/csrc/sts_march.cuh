@@ -36,7 +36,7 @@ namespace sts {
 
 constexpr int MX = 128;          // threads per CTA = columns handled per strip
 constexpr int MW = MX - 3;       // owned columns per strip
-constexpr int RW = MX + 6;       // ring row width: columns I0-4-shift .. (TMA rows: 16-byte aligned, shift in {0,1})
+constexpr int RW = MX + 8;       // ring row width: columns I0-4-shift .. (TMA rows 16-byte aligned, shift in 0..3)
 constexpr int RS = 6;            // ring slots
 constexpr int WARM = 3;          // warm-up rows per segment: the longest carried chain is
                                  // E(J0) <- D(J0-1) <- C(J0-2) <- A(J0-3); 2 rows fail the bitwise
@@ -141,9 +141,9 @@ __device__ __forceinline__ void tma_row(void* dst, const void* src, unsigned byt
 
 struct RingRow {                 // one old-iterate row (slot-major: one base address per row)
     double U[RW], V[RW], P[RW], T[RW], R[RW], G[RW];
-    uint32_t KK[(RW + 3) / 4 * 4];   // padded: every slot (TMA destination) starts 16-byte aligned
+    uint32_t KK[RW];
 };
-static_assert(sizeof(RingRow) % 16 == 0 && (RW * 8) % 16 == 0, "TMA rows need 16-byte alignment");
+static_assert(sizeof(RingRow) % 16 == 0 && (RW * 4) % 16 == 0, "TMA rows need 16-byte alignment");
 struct FluxRow {                 // face densities / fluxes of one row
     double RU[RW], FX[RW], FY[RW];   // (rho^v stays in registers: only the own column reads it)
 };
@@ -155,7 +155,7 @@ struct MarchSmem {
     FluxRow fr[2];
     double R1[RW];               // (p/T)^{n-1} of row j (row j+1 is written in stage E)
     double XTW[RW];              // T-eq W coefficient of face i (stage C)
-    double XUW[RW], XVW[RW], XVF[RW];
+    double XUW[RW], XVW[RW];     // (the flux sum F^x(j) + F^x(j+1) of a face is re-read from the flux rows)
     double UH[RW], DU[RW];
     double PN[RW];               // p_new of row j (stages D-E): a row of its own, so no row-start barrier
     unsigned long long mbar[RS]; // TMA completion barrier of each ring slot (u, v, p, T rows)
@@ -280,11 +280,10 @@ struct NM1 {                      // n-1 state / explicit planes at this thread'
 };
 
 // Ring row r into slot sl (march kernel).  c0 = stored column of ring column 0,
-// even, so every row starts 16-byte aligned; `tma` = the CTA's window
+// a multiple of 4, so every double and kind row starts 16-byte aligned; `tma` = the CTA's window
 // [c0, c0 + RW) lies inside the stored columns.  Rows inside the channel are
-// four TMA bulk copies of RW doubles (u, v, p, T) issued by one thread and
-// completing on the slot's mbarrier, plus one 4-byte cp.async per element for
-// the packed kinds.  Every other row (beyond a channel wall, or a window that
+// five TMA bulk copies (RW doubles of u, v, p, T; RW packed kind words) issued
+// by one thread and completing on the slot's mbarrier.  Every other row (beyond a channel wall, or a window that
 // leaves the stored columns) is filled by the threads exactly as ring_issue
 // does, and the issuing thread arrives on the mbarrier without bytes, so the
 // slot's phase advances either way.
@@ -298,13 +297,13 @@ __device__ __forceinline__ void ring_issue_tma(MarchSmem& s, int sl, const March
         const int base = r * k.pitch + c0;
         if (t == 0) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // earlier generic writes of the slot
-            mbar_expect_tx(&s.mbar[sl], 4u * RW * 8u);
+            mbar_expect_tx(&s.mbar[sl], 4u * RW * 8u + RW * 4u);
             tma_row(R.U, k.u_o + base, RW * 8, &s.mbar[sl]);
             tma_row(R.V, k.v_o + base, RW * 8, &s.mbar[sl]);
             tma_row(R.P, k.p_o + base, RW * 8, &s.mbar[sl]);
             tma_row(R.T, k.T_o + base, RW * 8, &s.mbar[sl]);
+            tma_row(R.KK, m.kind + base, RW * 4, &s.mbar[sl]);
         }
-        for (int c = t; c < RW; c += MX) cp_async4(&R.KK[c], m.kind + base + c);
     } else {
         for (int c = t; c < RW; c += MX) {
             const int li = c0 + c;
@@ -469,8 +468,7 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         const double D = m.B_dydx * v.gcN;
         v.FwSum = F1 + F2;
         v.xvW = (IMPL ? 0.5 * (max0(F1) - F1 * p1 + max0(F2) - F2 * p2) : 0.0) + D;
-        s.XVW[lc] = v.xvW;           // the E side of v-face (i-1, j+1) is XVW - XVF/2
-        s.XVF[lc] = v.FwSum;
+        s.XVW[lc] = v.xvW;           // the E side of v-face (i-1, j+1) is XVW - (F^x(j) + F^x(j+1))/2
     }
 }
 
@@ -581,7 +579,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         double a1, a2, vW, vE, FwS, FeS;
         if (REG) {
             a1 = v.xvW; FwS = v.FwSum; vW = Ra.V[lc - 1];
-            FeS = s.XVF[lc + 1]; a2 = IMPL ? s.XVW[lc + 1] - 0.5 * FeS : s.XVW[lc + 1]; vE = Ra.V[lc + 1];
+            FeS = Fn.FX[lc + 1] + Fc.FX[lc + 1]; a2 = IMPL ? s.XVW[lc + 1] - 0.5 * FeS : s.XVW[lc + 1]; vE = Ra.V[lc + 1];
         } else {
             FwS = FeS = 0.0;
             const double gadj = 0.5 * (gB + gT);
@@ -591,7 +589,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
             } else { a1 = v.xvW; FwS = v.FwSum; vW = Ra.V[lc - 1]; }
             if (ckind(R0.KK[lc + 1]) == CK_SOLID && ckind(Ra.KK[lc + 1]) == CK_SOLID) {
                 a2 = k.B * gadj * dy * rcp(0.5 * dx + zeta); vE = 0.0;
-            } else { FeS = s.XVF[lc + 1]; a2 = IMPL ? s.XVW[lc + 1] - 0.5 * FeS : s.XVW[lc + 1]; vE = Ra.V[lc + 1]; }
+            } else { FeS = Fn.FX[lc + 1] + Fc.FX[lc + 1]; a2 = IMPL ? s.XVW[lc + 1] - 0.5 * FeS : s.XVW[lc + 1]; vE = Ra.V[lc + 1]; }
         }
         // corner Gamma (i+1, j+1), recomputed with the same operations as its owner
         double gcE;
@@ -736,10 +734,10 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     const int cta = m.order[blockIdx.x];
     const int strip = cta % m.nstrips, segi = cta / m.nstrips;
     const int I0 = k.gi0 + strip * MW;                  // first owned column of the strip
-    // ring column 0 = stored column c0 (even: 16-byte aligned TMA rows); this
+    // ring column 0 = stored column c0 (a multiple of 4: 16-byte aligned TMA rows); this
     // thread's column sits at ring column lc
     const int wbase = I0 - 4 - k.gi0 + OFF;
-    const int shift = wbase & 1;
+    const int shift = wbase & 3;                        // c0 % 4 == 0: double and 4-byte kind rows aligned
     const int c0 = wbase - shift;
     const bool tma = c0 + RW <= k.pitch;
     const int lc = t + 2 + shift;
