@@ -21,6 +21,7 @@ struct ConvSmem {
     RingRow ring[RS];
     double FX[2][RW], FY[2][RW];     // fluxes rows j (cur) / j+1 (nxt)
     double TX[RW], UX[RW], VX[RW];
+    unsigned long long mbar[RS];     // TMA completion barrier of each ring slot
 };
 
 template <bool TVD>
@@ -31,10 +32,20 @@ __global__ void __launch_bounds__(MX, 3) conv_march_kernel(MarchParams m)
     MarchSmem& ms = *reinterpret_cast<MarchSmem*>(smem_raw);   // ring accessors share the layout prefix
     const Params& k = m.k;
     const int t = threadIdx.x;
-    const int lc = t + 2;
     const int cta = m.order[blockIdx.x];
     const int strip = cta % m.nstrips, segi = cta / m.nstrips;
     const int I0 = k.gi0 + strip * MW;
+    // ring rows by TMA as in march_kernel: ring column 0 = stored column c0 (a multiple of 4)
+    const int wbase = I0 - 4 - k.gi0 + OFF;
+    const int shift = wbase & 3;
+    const int c0 = wbase - shift;
+    const bool tma = c0 + RW <= k.pitch;
+    const int lc = t + 2 + shift;
+    if (t == 0) {
+        for (int q = 0; q < RS; q++) mbar_init(&s.mbar[q], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
     const int gi = I0 - 2 + t;
     const int J0 = segi * m.seg;
     const int J1 = min(J0 + m.seg, k.ny);
@@ -45,11 +56,13 @@ __global__ void __launch_bounds__(MX, 3) conv_march_kernel(MarchParams m)
     MarchParams mm = m;
     mm.k.u_o = k.u_1; mm.k.v_o = k.v_1; mm.k.p_o = k.p_1; mm.k.T_o = k.T_1;
 
-    for (int j = js - 1; j <= js + 2; j++) ring_issue(ms, mm, I0, j, slot(j));
+    // row r goes to slot(r); its use of that slot is the ((r - js + 1) / RS)-th
+    for (int j = js - 1; j <= js + 2; j++) ring_issue_tma(s, slot(j), mm, c0, tma, j);
     cp_wait_all();
     __syncthreads();
+    for (int j = js - 1; j <= js + 2; j++) mbar_wait(&s.mbar[slot(j)], 0);
     for (int j = js - 1; j <= js + 2; j++) ring_derive<false>(ms, slot(j));
-    ring_issue(ms, mm, I0, js + 3, slot(js + 3));
+    ring_issue_tma(s, slot(js + 3), mm, c0, tma, js + 3);
     int sj = slot(js);
 
     double TYc = 0.0, uYc = 0.0, vYc = 0.0;          // carried: TY(i,j), uY(i,y^f_j), vY(cell (i,j-1)) for v-face (i,j)
@@ -64,7 +77,8 @@ __global__ void __launch_bounds__(MX, 3) conv_march_kernel(MarchParams m)
         const int cb = j & 1, nb = (j + 1) & 1;
         cp_wait_all();
         __syncthreads();                                  // B0
-        ring_issue(ms, mm, I0, j + 4, sd);
+        ring_issue_tma(s, sd, mm, c0, tma, j + 4);
+        mbar_wait(&s.mbar[sc], ((j + 4 - js) / RS) & 1);   // row j+3
         ring_derive<false>(ms, sc);
         const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
         // ---- stage A: fluxes of row j+1 (Eqs. pl8-pl11 at time level n-1)

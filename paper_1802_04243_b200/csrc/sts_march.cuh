@@ -178,45 +178,6 @@ template <bool REG> __device__ __forceinline__ bool uA(uint32_t w) { return REG 
 template <bool REG> __device__ __forceinline__ bool uFl(uint32_t w) { return REG || flux_face(ukind(w)); }
 template <bool REG> __device__ __forceinline__ bool vA(uint32_t w) { return REG || vkind(w) == FK_ACTIVE; }
 
-// Issue the loads of ring row j (global columns I0-4 .. I0-4+RW).  Rows outside
-// [0, ny] and unstored columns are filled directly: kind WALLY / NONE, u = wall
-// velocity beyond the walls (BC spec 8), p = T = 1, v = 0.
-__device__ __forceinline__ void ring_issue(RingRow& r, const MarchParams& m, int I0, int j)
-{
-    const Params& k = m.k;
-    const int ro = j * k.pitch;                          // 32-bit element indices (checked on the host)
-    const int li0 = I0 - 4 - k.gi0 + OFF;
-    const bool row_ok = j >= 0 && j < k.ny;
-    for (int lc = threadIdx.x; lc < RW; lc += MX) {
-        const int li = li0 + lc;                         // stored local column
-        const bool col_ok = li >= 0 && li < k.pitch;
-        const int id = ro + li;
-        if (row_ok && col_ok) {
-            cp_async8(&r.U[lc], k.u_o + id);
-            cp_async8(&r.V[lc], k.v_o + id);
-            cp_async8(&r.P[lc], k.p_o + id);
-            cp_async8(&r.T[lc], k.T_o + id);
-            cp_async4(&r.KK[lc], m.kind + id);
-        } else if (j == k.ny && col_ok) {          // top wall row: v = 0 (WALL), no cells
-            r.U[lc] = k.u_wt;
-            cp_async8(&r.V[lc], k.v_o + id);
-            r.P[lc] = 1.0;
-            r.T[lc] = 1.0;
-            cp_async4(&r.KK[lc], m.kind + id);
-        } else {
-            r.U[lc] = j < 0 ? k.u_wb : (j >= k.ny ? k.u_wt : 0.0);
-            r.V[lc] = 0.0;
-            r.P[lc] = 1.0;
-            r.T[lc] = 1.0;
-            r.KK[lc] = (uint32_t)CK_WALLY | ((uint32_t)FK_NONE << 8) | ((uint32_t)FK_NONE << 16);
-        }
-    }
-    cp_commit();
-}
-__device__ __forceinline__ void ring_issue(MarchSmem& s, const MarchParams& m, int I0, int j, int sl)
-{
-    ring_issue(s.ring[sl], m, I0, j);
-}
 // 1/sqrt(x), x > 0: MUFU seed + 2 Newton steps (~1 ulp)
 __device__ __forceinline__ double frsqrt(double x)
 {
@@ -287,7 +248,8 @@ struct NM1 {                      // n-1 state / explicit planes at this thread'
 // leaves the stored columns) is filled by the threads exactly as ring_issue
 // does, and the issuing thread arrives on the mbarrier without bytes, so the
 // slot's phase advances either way.
-__device__ __forceinline__ void ring_issue_tma(MarchSmem& s, int sl, const MarchParams& m, int c0, bool tma, int r)
+template <class SM>   // MarchSmem or ConvSmem (both hold ring[RS] and mbar[RS])
+__device__ __forceinline__ void ring_issue_tma(SM& s, int sl, const MarchParams& m, int c0, bool tma, int r)
 {
     const Params& k = m.k;
     RingRow& R = s.ring[sl];
