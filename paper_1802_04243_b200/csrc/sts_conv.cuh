@@ -17,19 +17,24 @@
 
 namespace sts {
 
+struct RingRowC {                // n-1 row of the conv kernel: no Gamma (the planes need none)
+    double U[RW], V[RW], P[RW], T[RW], R[RW];
+    uint32_t KK[RW];
+};
+static_assert(sizeof(RingRowC) % 16 == 0, "TMA rows need 16-byte alignment");
+// 43.6 KB: five CTAs (20 warps) per SM
 struct ConvSmem {
-    RingRow ring[RS];
+    RingRowC ring[RS];
     double FX[2][RW], FY[2][RW];     // fluxes rows j (cur) / j+1 (nxt)
     double TX[RW], UX[RW], VX[RW];
     unsigned long long mbar[RS];     // TMA completion barrier of each ring slot
 };
 
 template <bool TVD>
-__global__ void __launch_bounds__(MX, 3) conv_march_kernel(MarchParams m)
+__global__ void __launch_bounds__(MX, 5) conv_march_kernel(MarchParams m)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ConvSmem& s = *reinterpret_cast<ConvSmem*>(smem_raw);
-    MarchSmem& ms = *reinterpret_cast<MarchSmem*>(smem_raw);   // ring accessors share the layout prefix
     const Params& k = m.k;
     const int t = threadIdx.x;
     const int cta = m.order[blockIdx.x];
@@ -61,7 +66,7 @@ __global__ void __launch_bounds__(MX, 3) conv_march_kernel(MarchParams m)
     cp_wait_all();
     __syncthreads();
     for (int j = js - 1; j <= js + 2; j++) mbar_wait(&s.mbar[slot(j)], 0);
-    for (int j = js - 1; j <= js + 2; j++) ring_derive<false>(ms, slot(j));
+    for (int j = js - 1; j <= js + 2; j++) ring_derive<false>(s.ring[slot(j)]);
     ring_issue_tma(s, slot(js + 3), mm, c0, tma, js + 3);
     int sj = slot(js);
 
@@ -70,16 +75,16 @@ __global__ void __launch_bounds__(MX, 3) conv_march_kernel(MarchParams m)
         const int sa = sj + 1 == RS ? 0 : sj + 1, sb = sa + 1 == RS ? 0 : sa + 1;
         const int sc = sb + 1 == RS ? 0 : sb + 1, sd = sc + 1 == RS ? 0 : sc + 1;
         const int sm = sj == 0 ? RS - 1 : sj - 1;
-        const RingRow& Rm = s.ring[sm];
-        const RingRow& R0 = s.ring[sj];
-        const RingRow& Ra = s.ring[sa];
-        const RingRow& Rb = s.ring[sb];
+        const RingRowC& Rm = s.ring[sm];
+        const RingRowC& R0 = s.ring[sj];
+        const RingRowC& Ra = s.ring[sa];
+        const RingRowC& Rb = s.ring[sb];
         const int cb = j & 1, nb = (j + 1) & 1;
         cp_wait_all();
         __syncthreads();                                  // B0
         ring_issue_tma(s, sd, mm, c0, tma, j + 4);
         mbar_wait(&s.mbar[sc], ((j + 4 - js) / RS) & 1);   // row j+3
-        ring_derive<false>(ms, sc);
+        ring_derive<false>(s.ring[sc]);
         const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
         // ---- stage A: fluxes of row j+1 (Eqs. pl8-pl11 at time level n-1)
         double Fx1 = 0.0, Fy1 = 0.0;

@@ -191,15 +191,15 @@ __device__ __forceinline__ double frsqrt(double x)
 // rho = p/T (Eq. pl5), Gamma = sqrt(T) (Eq. pl37) of ring row j from one
 // reciprocal square root y = T^(-1/2): Gamma = T y, rho = p y^2 (~2 ulp; the
 // explicit planes need no Gamma)
-template <bool WITH_GAMMA = true>
-__device__ __forceinline__ void ring_derive(RingRow& r)
+template <bool WITH_GAMMA = true, class ROW = RingRow>
+__device__ __forceinline__ void ring_derive(ROW& r)
 {
     for (int lc = threadIdx.x; lc < RW; lc += MX) {
         const double Tv = r.T[lc];
-        if (WITH_GAMMA) {
+        if constexpr (WITH_GAMMA) {
             const double y = frsqrt(Tv);
             r.R[lc] = r.P[lc] * (y * y);
-            r.G[lc] = Tv * y;
+            if constexpr (WITH_GAMMA) r.G[lc] = Tv * y;
         } else {
             r.R[lc] = fdiv(r.P[lc], Tv);
         }
@@ -252,7 +252,7 @@ template <class SM>   // MarchSmem or ConvSmem (both hold ring[RS] and mbar[RS])
 __device__ __forceinline__ void ring_issue_tma(SM& s, int sl, const MarchParams& m, int c0, bool tma, int r)
 {
     const Params& k = m.k;
-    RingRow& R = s.ring[sl];
+    auto& R = s.ring[sl];
     const int t = threadIdx.x;
     const bool row_in = (unsigned)r < (unsigned)k.ny;
     if (tma && row_in) {
