@@ -752,6 +752,7 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     Carry c{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 1.0, 0.0};
     Resid rs{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, -1, 0, false};
     StepVars v;
+    int oj = js * k.pitch + col;                        // element offset of (row j, own column), + pitch per step (upwind prefetch)
 
     for (int j = js; j < J1; j++) {
         RingRow& Rm = *pm;
@@ -764,10 +765,19 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
 
         double p1nn = 0.0, T1nn = 0.0, u1n = 0.0, v1nn = 0.0, Ten = 0.0, uen = 0.0, vem = 0.0;
         if (PREF) {                                         // consumed one row step later
-            p1nn = ld(k.p_1, j + 2); T1nn = ld(k.T_1, j + 2); u1n = ld(k.u_1, j + 1); v1nn = ldv(k.v_1, j + 2);
-            if (!IMPL) { Ten = ld(k.Te, j + 1); uen = ld(k.ue, j + 1); vem = ldv(k.ve, j + 2); }
+            const unsigned o1 = (unsigned)(oj + k.pitch), o2 = o1 + (unsigned)k.pitch;
+            const bool ok1 = col_stored && (unsigned)(j + 1) < (unsigned)k.ny;
+            const bool ok2 = col_stored && (unsigned)(j + 2) < (unsigned)k.ny;
+            const bool ok2v = col_stored && (unsigned)(j + 2) <= (unsigned)k.ny;
+            if (ok2) { p1nn = __ldg(k.p_1 + o2); T1nn = __ldg(k.T_1 + o2); }
+            if (ok1) u1n = __ldg(k.u_1 + o1);
+            if (ok2v) v1nn = __ldg(k.v_1 + o2);
+            if (!IMPL) {
+                if (ok1) { Ten = __ldg(k.Te + o1); uen = __ldg(k.ue + o1); }
+                if (ok2v) vem = __ldg(k.ve + o2);
+            }
         } else {
-            const unsigned rj = (unsigned)(j * k.pitch + col), rn = rj + (unsigned)k.pitch;
+            const unsigned rj = (unsigned)(j * k.pitch + col), rn = rj + (unsigned)k.pitch;   // (offset form measured 0.4 % slower here)
             const bool okj = col_stored && j >= 0 && j < k.ny;
             const bool okn = col_stored && j + 1 >= 0 && j + 1 < k.ny;
             const bool okv = col_stored && j + 1 >= 0 && j + 1 <= k.ny;
@@ -820,6 +830,7 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
         }
         RingRow* const pf = pm;
         pm = p0; p0 = pa; pa = pb; pb = pc; pc = pd; pd = pf;
+        oj += k.pitch;
     }
     cp_wait_all();
     const double qnan = __longlong_as_double(0x7ff8000000000000LL);
