@@ -113,7 +113,12 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem)
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-// ---- TMA (bulk async copy) rows with mbarrier completion
+// ---- TMA (bulk async copy) rows with mbarrier completion.  Work beyond one
+// element per thread is spread over different warps (a CTA advances at the
+// pace of its slowest warp): warp 1 derives the ring columns beyond MX, the
+// first lane of warp 2 issues the row copies.
+constexpr int TMA_THREAD = 64;
+constexpr int DERIVE_EXTRA_WARP = 1;
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, int count)
 {
@@ -194,7 +199,10 @@ __device__ __forceinline__ double frsqrt(double x)
 template <bool WITH_GAMMA = true, class ROW = RingRow>
 __device__ __forceinline__ void ring_derive(ROW& r)
 {
-    for (int lc = threadIdx.x; lc < RW; lc += MX) {
+    const int t = threadIdx.x, xl = t - 32 * DERIVE_EXTRA_WARP;
+    const int n = (xl >= 0 && xl < RW - MX) ? 2 : 1;
+    for (int q = 0; q < n; q++) {
+        const int lc = q == 0 ? t : MX + xl;
         const double Tv = r.T[lc];
         if constexpr (WITH_GAMMA) {
             const double y = frsqrt(Tv);
@@ -257,7 +265,7 @@ __device__ __forceinline__ void ring_issue_tma(SM& s, int sl, const MarchParams&
     const bool row_in = (unsigned)r < (unsigned)k.ny;
     if (tma && row_in) {
         const int base = r * k.pitch + c0;
-        if (t == 0) {
+        if (t == TMA_THREAD) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // earlier generic writes of the slot
             mbar_expect_tx(&s.mbar[sl], 4u * RW * 8u + RW * 4u);
             tma_row(R.U, k.u_o + base, RW * 8, &s.mbar[sl]);
@@ -291,7 +299,7 @@ __device__ __forceinline__ void ring_issue_tma(SM& s, int sl, const MarchParams&
                 R.KK[c] = (uint32_t)CK_WALLY | ((uint32_t)FK_NONE << 8) | ((uint32_t)FK_NONE << 16);
             }
         }
-        if (t == 0) mbar_arrive(&s.mbar[sl]);
+        if (t == TMA_THREAD) mbar_arrive(&s.mbar[sl]);
     }
     cp_commit();
 }
