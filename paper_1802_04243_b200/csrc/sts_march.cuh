@@ -626,9 +626,10 @@ __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int 
                 apN = r * v.dvN * dx; bpN = r * v.vhatN * dx; sum += apN * Ra.P[lc];
             }
         }
-        const double a0 = m.dV * rcp(v.TN) + (apW + apE + apS + apN) * dt;
+        // a^p_0 = dV / T_new + dt sum a^p (Eq. pl24, R28); multiplied through by T_new
+        // so one reciprocal serves: p = T_new (dt sum + b^p) / (dV + T_new dt sum a^p)
         const double bp = s.R1[lc] * m.dV - (bpE - bpW + bpN - bpS) * dt;
-        pn = (sum * dt + bp) * rcp(a0);
+        pn = v.TN * (sum * dt + bp) * rcp(fma(v.TN * dt, apW + apE + apS + apN, m.dV));
     }
     v.pn = pn;
     s.PN[lc] = pn;
