@@ -737,11 +737,11 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     ring_derive(*pb);
     __syncthreads();        // rho, Gamma of rows js-1 .. js+2 before step js reads neighbours' elements
 
-    // ---- n-1 / explicit-plane values of this thread's column.  Upwind variants
-    // prefetch them one row step ahead through registers; the TVD variants
-    // (no registers to spare at 4 CTAs/SM) load them at the start of the row
-    // step that uses them (measured: 7 % faster for TVD, 2 % slower for upwind)
-    constexpr bool PREF = !TVD;
+    // ---- n-1 / explicit-plane values of this thread's column.  Prefetched one
+    // row step ahead through registers, except in implicit TVD (no registers to
+    // spare at 4 CTAs/SM: 16 B of spills and +14 %), which loads them at the start
+    // of the row step that uses them
+    constexpr bool PREF = !(IMPL && TVD);
     const int col = gi - k.gi0 + OFF;                   // stored local column of this thread
     auto ld = [&](const double* a, int j) -> double {
         return (col_stored && j >= 0 && j < k.ny) ? __ldg(a + (j * k.pitch + col)) : 0.0;
