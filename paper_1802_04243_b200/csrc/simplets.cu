@@ -424,8 +424,29 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     c->march_seg = best_seg;
     c->march_nseg = (ny + best_seg - 1) / best_seg;
     c->march_nstrips = strips;
+    // bit 30 of a launch-order entry: every point of the CTA's rows (warm-up rows
+    // included) and columns is regular, so the kernel runs the loop body compiled
+    // with the regular stage instances only (no per-point dispatch); a regular
+    // point runs the same instance either way
+    auto allreg = [&](int id, int seg) {
+        const int st = id % strips, g = id / strips;
+        const int J0 = g * seg, J1 = std::min(ny, J0 + seg);
+        if (J0 - WARM < 0) return false;
+        for (int j = J0 - WARM; j < J1; j++)
+            for (int t = 0; t < MX; t++) {
+                const int li = st * MW - 2 + t + OFF;
+                if (li < 0 || li >= c->pitch || !(packed[(size_t)j * c->pitch + li] & REG_BIT)) return false;
+            }
+        return true;
+    };
     std::vector<int> order(ctas.size());
-    for (size_t q = 0; q < ctas.size(); q++) order[q] = ctas[q].second;
+    int n_allreg = 0;
+    for (size_t q = 0; q < ctas.size(); q++) {
+        const bool ar = allreg(ctas[q].second, best_seg);
+        n_allreg += ar;
+        order[q] = ctas[q].second | (ar ? ALLREG_BIT : 0);
+    }
+    if (getenv("STS_VERBOSE")) fprintf(stderr, "sts: seg %d, %zu CTAs, %d all-regular\n", best_seg, ctas.size(), n_allreg);
     cudaFree(c->cta_order);
     c->cta_order = nullptr;
     cudaMalloc(&c->cta_order, order.size() * sizeof(int));
@@ -448,9 +469,9 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
         return a.first > b.first;
     });
     std::vector<int> split;
-    for (auto& q : ectas) split.push_back(q.second);
+    for (auto& q : ectas) split.push_back(q.second | (allreg(q.second, c->edge_seg) ? ALLREG_BIT : 0));
     c->n_edge = (int)split.size();
-    for (int o : order) if (!edge(o % strips)) split.push_back(o);
+    for (int o : order) if (!edge((o & (ALLREG_BIT - 1)) % strips)) split.push_back(o);
     c->n_split = (int)split.size();
     cudaFree(c->cta_split);
     c->cta_split = nullptr;

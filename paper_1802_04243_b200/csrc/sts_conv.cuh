@@ -39,7 +39,9 @@ __global__ void __launch_bounds__(MX, 5) conv_march_kernel(MarchParams m)
     ConvSmem& s = *reinterpret_cast<ConvSmem*>(smem_raw);
     const Params& k = m.k;
     const int t = threadIdx.x;
-    const int cta = m.order[blockIdx.x];
+    const int ow = m.order[blockIdx.x];
+    const int cta = ow & (ALLREG_BIT - 1);
+    const bool allreg = (ow & ALLREG_BIT) != 0;
     const int strip = cta % m.nstrips, segi = cta / m.nstrips;
     const int I0 = k.gi0 + strip * MW;
     // ring rows by TMA as in march_kernel: ring column 0 = stored column c0 (a multiple of 4)
@@ -90,7 +92,7 @@ __global__ void __launch_bounds__(MX, 5) conv_march_kernel(MarchParams m)
         const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
         // per-point instance (REG: the +-3 window of the point is all fluid, so
         // every kind test folds away; same operations as the general instance)
-        const bool reg = (kw0 & REG_BIT) != 0u;
+        const bool reg = allreg || (kw0 & REG_BIT) != 0u;
         double Fx1 = 0.0, Fy1 = 0.0, TYn = 0.0, vYn = 0.0, uYn = 0.0;
         auto stageA = [&](auto regc) {
             constexpr bool REG = decltype(regc)::value;
