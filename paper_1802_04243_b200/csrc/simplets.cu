@@ -359,6 +359,8 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     const int strips = (c->nloc + MW - 1) / MW;
     const int slots = dev_sms * per_sm;
     const int ny = c->ny;
+    double w_gen = 1.35, w_mix = 2.35;                  // warp costs relative to an all-regular warp
+    if (const char* cv = getenv("STS_COST")) sscanf(cv, "%lf,%lf", &w_gen, &w_mix);   // tuning hook
     // row cost of every (strip, row), prefix-summed over rows
     std::vector<double> pre((size_t)strips * (ny + 1), 0.0);
     for (int st = 0; st < strips; st++) {
@@ -371,7 +373,7 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
                     const int li = I0 - 2 + 32 * w + l - c->gi0 + OFF;
                     if (li >= 0 && li < c->pitch && (packed[(size_t)j * c->pitch + li] & REG_BIT)) nreg++;
                 }
-                const double wc = nreg == 32 ? 1.0 : (nreg == 0 ? 1.35 : 2.35);
+                const double wc = nreg == 32 ? 1.0 : (nreg == 0 ? w_gen : w_mix);
                 rc = std::max(rc, wc);
             }
             pre[(size_t)st * (ny + 1) + j + 1] = pre[(size_t)st * (ny + 1) + j] + rc;
