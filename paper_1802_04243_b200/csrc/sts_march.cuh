@@ -706,9 +706,7 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     const int t = threadIdx.x;
     const int ow = m.order[blockIdx.x];
     const int cta = ow & (ALLREG_BIT - 1);
-    // (bit 30, every point of the CTA regular, is used by the conv kernel only: a
-    // second copy of this row loop with the regular instances alone measured
-    // -1.2 % in implicit upwind but +40 % in the explicit variants)
+    const bool allreg = (ow & ALLREG_BIT) != 0;          // every point of the CTA is regular (host)
     const int strip = cta % m.nstrips, segi = cta / m.nstrips;
     const int I0 = k.gi0 + strip * MW;                  // first owned column of the strip
     // ring column 0 = stored column c0 (a multiple of 4: 16-byte aligned TMA rows); this
@@ -769,83 +767,20 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     StepVars v;
     int oj = js * k.pitch + col;                        // element offset of (row j, own column), + pitch per step (upwind prefetch)
 
-    for (int j = js; j < J1; j++) {
-        RingRow& Rm = *pm;
-        RingRow& R0 = *p0;
-        RingRow& Ra = *pa;
-        RingRow& Rb = *pb;
-        RingRow& Rc = *pc;
-        FluxRow& Fc = s.fr[j & 1];
-        FluxRow& Fn = s.fr[(j + 1) & 1];
-
-        double p1nn = 0.0, T1nn = 0.0, u1n = 0.0, v1nn = 0.0, Ten = 0.0, uen = 0.0, vem = 0.0;
-        if (PREF) {                                         // consumed one row step later
-            const unsigned o1 = (unsigned)(oj + k.pitch), o2 = o1 + (unsigned)k.pitch;
-            const bool ok1 = col_stored && (unsigned)(j + 1) < (unsigned)k.ny;
-            const bool ok2 = col_stored && (unsigned)(j + 2) < (unsigned)k.ny;
-            const bool ok2v = col_stored && (unsigned)(j + 2) <= (unsigned)k.ny;
-            if (ok2) { p1nn = __ldg(k.p_1 + o2); T1nn = __ldg(k.T_1 + o2); }
-            if (ok1) u1n = __ldg(k.u_1 + o1);
-            if (ok2v) v1nn = __ldg(k.v_1 + o2);
-            if (!IMPL) {
-                if (ok1) { Ten = __ldg(k.Te + o1); uen = __ldg(k.ue + o1); }
-                if (ok2v) vem = __ldg(k.ve + o2);
-            }
+    // The row loop.  Implicit upwind compiles it twice, once with the regular
+    // stage instances only for all-regular CTAs (measured -1.2 %); in the other
+    // variants a second copy costs more (explicit +40 %: instruction cache).
+    if constexpr (IMPL && !TVD) {
+        if (allreg) {
+            constexpr bool ALLREG = true;
+#include "sts_march_loop.inc"
         } else {
-            const unsigned rj = (unsigned)(j * k.pitch + col), rn = rj + (unsigned)k.pitch;   // (offset form measured 0.4 % slower here)
-            const bool okj = col_stored && j >= 0 && j < k.ny;
-            const bool okn = col_stored && j + 1 >= 0 && j + 1 < k.ny;
-            const bool okv = col_stored && j + 1 >= 0 && j + 1 <= k.ny;
-            nm.p1n = okn ? __ldg(k.p_1 + rn) : 0.0;
-            nm.T1n = okn ? __ldg(k.T_1 + rn) : 0.0;
-            nm.T1c = okj ? __ldg(k.T_1 + rj) : 0.0;
-            nm.u1c = okj ? __ldg(k.u_1 + rj) : 0.0;
-            nm.v1n = okv ? __ldg(k.v_1 + rn) : 0.0;
-            if (!IMPL) {
-                nm.Tec = okj ? __ldg(k.Te + rj) : 0.0;
-                nm.uec = okj ? __ldg(k.ue + rj) : 0.0;
-                nm.ven = okv ? __ldg(k.ve + rn) : 0.0;
-            }
+            constexpr bool ALLREG = false;
+#include "sts_march_loop.inc"
         }
-
-        {   // row j+4 -> slot (j+5-js) mod RS (= pd); row j+3 (slot of pc) must have landed
-            const int q = j + 4 - js;
-            ring_issue_tma(s, (q + 1) % RS, m, c0, tma, j + 4);
-            mbar_wait(&s.mbar[q % RS], (q / RS) & 1);
-        }
-        ring_derive(Rc);
-        // per-point choice (a function of the cell alone, so any decomposition
-        // gives bit-identical results); warps mixing both kinds run both
-        // instances -- such CTAs are scheduled first (host longest-first order)
-        const bool reg = (R0.KK[lc] & REG_BIT) != 0u;
-        if (reg) stage_A<IMPL, TVD, true>(s, m, lc, Rm, R0, Ra, Rb, Rc, Fc, Fn, nm, v);
-        else stage_A<IMPL, TVD, false>(s, m, lc, Rm, R0, Ra, Rb, Rc, Fc, Fn, nm, v);
-        __syncthreads();                                    // B1
-        if (reg) stage_C<IMPL, TVD, true>(s, m, lc, Rm, R0, Ra, Rb, Fc, Fn, nm, c, v);
-        else stage_C<IMPL, TVD, false>(s, m, lc, Rm, R0, Ra, Rb, Fc, Fn, nm, c, v);
-        __syncthreads();                                    // B2
-        if (reg) stage_D<IMPL, TVD, true>(s, m, lc, Rm, R0, Ra, Fc, Fn, c, v);
-        else stage_D<IMPL, TVD, false>(s, m, lc, Rm, R0, Ra, Fc, Fn, c, v);
-        cp_wait_all();                                      // ring row j+4 (read from step j+1 on)
-        __syncthreads();                                    // B3
-        if (j >= J0 && owner) {
-            if (reg) stage_E<IMPL, TVD, true>(s, m, lc, gi, j, R0, c, v, rs);
-            else stage_E<IMPL, TVD, false>(s, m, lc, gi, j, R0, c, v, rs);
-        }
-        s.R1[lc] = v.r1n;                                   // (p/T)^{n-1} of row j+1 for step j+1
-        // ---- carry row j+1 quantities to the next step
-        c.ytS = v.ytSn; c.FS = v.Fy1;
-        c.utS = v.utSn; c.FsSum = v.FsSumN;
-        c.vcS = v.vcSn; c.FbS = v.FbN;
-        c.vhatP = v.vhatN; c.dvP = v.dvN;
-        c.pnP = v.pn; c.gcP = v.gcN; c.rvS = v.rv1;
-        if (PREF) {
-            nm.p1n = p1nn; nm.T1c = nm.T1n; nm.T1n = T1nn; nm.u1c = u1n; nm.v1n = v1nn;
-            if (!IMPL) { nm.Tec = Ten; nm.uec = uen; nm.ven = vem; }
-        }
-        RingRow* const pf = pm;
-        pm = p0; p0 = pa; pa = pb; pb = pc; pc = pd; pd = pf;
-        oj += k.pitch;
+    } else {
+        constexpr bool ALLREG = false;
+#include "sts_march_loop.inc"
     }
     cp_wait_all();
     const double qnan = __longlong_as_double(0x7ff8000000000000LL);
