@@ -743,10 +743,9 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     __syncthreads();        // rho, Gamma of rows js-1 .. js+2 before step js reads neighbours' elements
 
     // ---- n-1 / explicit-plane values of this thread's column.  Prefetched one
-    // row step ahead through registers, except in implicit TVD (no registers to
-    // spare at 4 CTAs/SM: 16 B of spills and +14 %), which loads them at the start
-    // of the row step that uses them
-    constexpr bool PREF = !(IMPL && TVD);
+    // row step ahead through registers (PREF_L), except in implicit TVD (no
+    // registers to spare at 4 CTAs/SM: 16 B of spills and +14 %), which loads them
+    // at the start of the row step that uses them
     const int col = gi - k.gi0 + OFF;                   // stored local column of this thread
     auto ld = [&](const double* a, int j) -> double {
         return (col_stored && j >= 0 && j < k.ny) ? __ldg(a + (j * k.pitch + col)) : 0.0;
@@ -756,11 +755,11 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     };
     NM1 nm;
     nm.Tec = nm.uec = nm.ven = 0.0;
-    if (PREF) {
+    auto nm_prefetch_init = [&]() {
         nm.p1n = ld(k.p_1, js + 1); nm.T1n = ld(k.T_1, js + 1);
         nm.T1c = ld(k.T_1, js); nm.u1c = ld(k.u_1, js); nm.v1n = ldv(k.v_1, js + 1);
         if (!IMPL) { nm.Tec = ld(k.Te, js); nm.uec = ld(k.ue, js); nm.ven = ldv(k.ve, js + 1); }
-    }
+    };
 
     Carry c{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 1.0, 0.0};
     Resid rs{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, -1, 0, false};
@@ -771,17 +770,37 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     // for all-regular CTAs (no per-point dispatch).  Measured: implicit upwind
     // -3.2 %, explicit upwind -2.8 %, explicit TVD -2 %; implicit TVD +0.2 %, so
     // it keeps one copy.
-    if constexpr (!(IMPL && TVD)) {
+    // Measured per variant (profiles/r01_v8_summary.md): implicit TVD keeps one
+    // copy without the n-1 prefetch (no registers to spare); implicit upwind is
+    // fastest with the prefetch set-up inside each copy, the explicit variants
+    // with it ahead of the branch.
+    if constexpr (IMPL && TVD) {
+        constexpr bool ALLREG = false;
+        constexpr bool PREF_L = false;
+#include "sts_march_loop.inc"
+    } else if constexpr (IMPL) {
         if (allreg) {
             constexpr bool ALLREG = true;
+            constexpr bool PREF_L = true;
+            nm_prefetch_init();
 #include "sts_march_loop.inc"
         } else {
             constexpr bool ALLREG = false;
+            constexpr bool PREF_L = true;
+            nm_prefetch_init();
 #include "sts_march_loop.inc"
         }
     } else {
-        constexpr bool ALLREG = false;
+        nm_prefetch_init();
+        if (allreg) {
+            constexpr bool ALLREG = true;
+            constexpr bool PREF_L = true;
 #include "sts_march_loop.inc"
+        } else {
+            constexpr bool ALLREG = false;
+            constexpr bool PREF_L = true;
+#include "sts_march_loop.inc"
+        }
     }
     cp_wait_all();
     const double qnan = __longlong_as_double(0x7ff8000000000000LL);
