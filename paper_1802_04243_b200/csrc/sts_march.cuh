@@ -259,7 +259,8 @@ struct NM1 {                      // n-1 state / explicit planes at this thread'
 // does, and the issuing thread arrives on the mbarrier without bytes, so the
 // slot's phase advances either way.
 template <class SM>   // MarchSmem or ConvSmem (both hold ring[RS] and mbar[RS])
-__device__ __forceinline__ void ring_issue_tma(SM& s, int sl, const MarchParams& m, int c0, bool tma, int r)
+__device__ __forceinline__ void ring_issue_tma(SM& s, int sl, const MarchParams& m, int c0, bool tma, int r,
+                                               bool kinds = true)   // false: an all-regular CTA reads no kinds
 {
     const Params& k = m.k;
     auto& R = s.ring[sl];
@@ -269,12 +270,12 @@ __device__ __forceinline__ void ring_issue_tma(SM& s, int sl, const MarchParams&
         const int base = r * k.pitch + c0;
         if (t == TMA_THREAD) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // earlier generic writes of the slot
-            mbar_expect_tx(&s.mbar[sl], 4u * RW * 8u + RW * 4u);
+            mbar_expect_tx(&s.mbar[sl], 4u * RW * 8u + (kinds ? RW * 4u : 0u));
             tma_row(R.U, k.u_o + base, RW * 8, &s.mbar[sl]);
             tma_row(R.V, k.v_o + base, RW * 8, &s.mbar[sl]);
             tma_row(R.P, k.p_o + base, RW * 8, &s.mbar[sl]);
             tma_row(R.T, k.T_o + base, RW * 8, &s.mbar[sl]);
-            tma_row(R.KK, m.kind + base, RW * 4, &s.mbar[sl]);
+            if (kinds) tma_row(R.KK, m.kind + base, RW * 4, &s.mbar[sl]);
         }
     } else {
         for (int c = t; c < RW; c += MX) {
@@ -732,7 +733,8 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     // here on, row j+4 is issued at the start of step j and lands before its B3);
     // ring slots of rows j-1 .. j+4, rotated by one per row step
     RingRow *pm = &s.ring[0], *p0 = &s.ring[1], *pa = &s.ring[2], *pb = &s.ring[3], *pc = &s.ring[4], *pd = &s.ring[5];
-    for (int q = 0; q < 5; q++) ring_issue_tma(s, q, m, c0, tma, js - 1 + q);   // row js-1+q -> slot q
+    const bool kinds = !(allreg && !(IMPL && TVD));      // the all-regular loop copies read no kinds
+    for (int q = 0; q < 5; q++) ring_issue_tma(s, q, m, c0, tma, js - 1 + q, kinds);   // row js-1+q -> slot q
     cp_wait_all();
     __syncthreads();
     for (int q = 0; q < 4; q++) mbar_wait(&s.mbar[q], 0);
