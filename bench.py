@@ -130,7 +130,15 @@ class ClockSampler:
 
 
 def bench_case(args, world):
+    """Default: C3 H = 200 (the paper's largest mesh) at N = 1, and the same slab
+    per GPU laid end to end at N > 1 (weak scaling).  --workload C4 (100.8 M FVs,
+    strong scaling: one channel split over the N GPUs) and C5 (150 M FVs per GPU,
+    weak scaling) are BASELINE.json's configs[3] and configs[4]."""
     from paper_1802_04243_b200 import workloads as W
+    if args.workload == "C4":
+        return W.c4(args.variant, passes=args.passes)
+    if args.workload == "C5":
+        return W.c5(world, args.variant, passes=args.passes)
     if world == 1:
         return W.c3(200, args.variant, passes=args.passes)
     return W.c3_long(world, args.variant, passes=args.passes)
@@ -333,7 +341,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if args.workload == "C4" else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: the paper's geometry (P:686, P:719), free-stream IC; no datasets",
             "config": {"workload": f"{case['name']}_{args.variant}", "nx": case["nx"], "ny": case["ny"],
                        "fv_per_gpu": nfv_rank, "passes_per_step": passes, "dt": case["dt"],
@@ -362,6 +370,7 @@ def main():
     ap.add_argument("--variant", default="implicit_upwind",
                     choices=["implicit_upwind", "implicit_tvd", "explicit_upwind", "explicit_tvd"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C3", choices=["C3", "C4", "C5"])
     ap.add_argument("--ref-passes", type=int, default=1)
     ap.add_argument("--ref-warmup", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
