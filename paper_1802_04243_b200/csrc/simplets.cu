@@ -430,7 +430,9 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     // included) and columns is regular, so the kernel runs the loop body compiled
     // with the regular stage instances only (no per-point dispatch); a regular
     // point runs the same instance either way
+    const bool no_allreg = getenv("STS_NO_ALLREG") != nullptr;   // test hook: every CTA takes the general loop
     auto allreg = [&](int id, int seg) {
+        if (no_allreg) return false;
         const int st = id % strips, g = id / strips;
         const int J0 = g * seg, J1 = std::min(ny, J0 + seg);
         if (J0 - WARM < 0) return false;

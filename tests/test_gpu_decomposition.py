@@ -173,3 +173,34 @@ def test_tile_kernel_agrees(S, oracle_mod, variant):
     for f in FIELDS:
         x, y = a.get_field(f), b.get_field(f)
         assert np.abs(x - y).max() <= 1e-10 * max(1.0, np.abs(y).max()), f
+
+
+@pytest.mark.parametrize("variant", list(W.VARIANTS))
+def test_allreg_loop_bitwise(S, variant):
+    """CTAs whose every point is regular run the regular-only copy of the row
+    loop (launch-order bit 30) and skip the kind rows; forcing every CTA onto the
+    general loop (STS_NO_ALLREG) must not change a single bit.  A 520 x 96
+    channel with one square and 16-row segments has many all-regular CTAs."""
+    case = W.channel(520, 96, spacing=0.25, variant=variant, passes=4, squares=[(200, 40, 10, 10)])
+    out = []
+    for env in ({"STS_SEG": "16"}, {"STS_SEG": "16", "STS_NO_ALLREG": "1"}, {"STS_SEG": "40"}):
+        old = {k: os.environ.get(k) for k in ("STS_SEG", "STS_NO_ALLREG")}
+        os.environ.pop("STS_NO_ALLREG", None)
+        os.environ.update(env)
+        try:
+            g = S.Solver(case)
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        base = {k: g.get_field(k) for k in ("u", "v", "p", "T")}
+        st = W.perturbed_state(base, W.perturbation(case, seed=9), vscale=0.05)
+        for k in ("p", "T", "u", "v"):
+            g.set_field(k, st[k])
+        g.advance(3)
+        out.append({f: g.get_field(f) for f in FIELDS})
+    for f in FIELDS:
+        assert np.array_equal(out[0][f], out[1][f]), f
+        assert np.array_equal(out[0][f], out[2][f]), f
