@@ -200,9 +200,26 @@ def test_c4_100m_properties(S):
     assert np.abs(f["v"]).max() > 1e-3            # the squares do deflect the flow
 
 
+@pytest.mark.parametrize("variant", list(W.VARIANTS))
 @pytest.mark.parametrize("H", [10])
-def test_parity_paper_mesh(S, oracle_mod, H):
-    """The paper's 4032 x 200 mesh (C3, H = 10), implicit upwind, 1 step x 3 passes
-    in the bench's launch configuration: every element compared."""
-    case = W.c3(H, "implicit_upwind", passes=3)
-    _run_compare(S, oracle_mod, case, 1, seed=5)
+def test_parity_paper_mesh(S, oracle_mod, H, variant):
+    """The paper's 4032 x 200 mesh (C3, H = 10), every variant, 1 step x 3 passes
+    in the bench's launch configuration (TMA rows, all-regular loop copies,
+    longest-first CTA order): every element compared."""
+    case = W.c3(H, variant, passes=3)
+    extra = ("uexp", "vexp", "Texp") if variant.startswith("explicit") else ()
+    _run_compare(S, oracle_mod, case, 1, seed=5, extra=extra)
+
+
+def test_parity_paper_mesh_tolerance_mode(S, oracle_mod):
+    """Tolerance mode on the paper's 4032 x 200 mesh, implicit TVD: the graph-
+    driven loop 2 takes the oracle's pass count and matches its fields."""
+    case = W.c3(10, "implicit_tvd", passes=200)
+    case["tol"] = 1e-4                         # ~20 passes: the oracle finishes in seconds
+    g, o = seeded_pair(S, oracle_mod, case, seed=12)
+    st, stats = g.advance(1, check=False)
+    ost, ores, opasses = o.advance(1)
+    assert st == 0 and ost == 0 and stats["converged"] == 1
+    assert stats["passes_done"] == opasses, (stats["passes_done"], opasses)
+    err = rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), o.get_map(0) == 0)
+    assert max(err.values()) <= 1e-8, err
