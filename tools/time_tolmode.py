@@ -19,7 +19,7 @@ def run(case, graph, steps):
     if not graph:
         os.environ["STS_NO_GRAPH"] = "1"
     g = S.Solver(case)
-    g.advance(2, check=False)                       # warm-up (graph build)
+    g.advance(3, check=False)                       # warm-up: builds the graphs of all 3 snapshot rotations
     torch.cuda.synchronize()
     p0 = g.advance(0)[1]["passes_done"]
     t = time.perf_counter()
