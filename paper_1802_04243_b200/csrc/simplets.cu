@@ -1242,10 +1242,11 @@ static sts_status graph_step(sts_ctx* ctx, bool* conv)
 {
     sts_ctx* const c = ctx;
     const int n1 = c->cur, a = (n1 + 1) % 3, b = (n1 + 2) % 3;
-    if (!c->tol_exec[n1]) {
-        sts_status e = build_tol_graph(c, n1);
-        if (e) return e;
-    }
+    for (int r = 0; r < 3; r++)                   // all three rotations at once: no build inside later steps
+        if (!c->tol_exec[r]) {
+            sts_status e = build_tol_graph(c, r);
+            if (e) return e;
+        }
     CU(cudaGraphLaunch(c->tol_exec[n1], c->stream));
     CU(cudaMemcpyAsync(c->h_ls, c->d_ls, sizeof(LoopState), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
