@@ -75,161 +75,12 @@ __global__ void __launch_bounds__(MX, 5) conv_march_kernel(MarchParams m)
     int sj = slot(js);
 
     double TYc = 0.0, uYc = 0.0, vYc = 0.0;          // carried: TY(i,j), uY(i,y^f_j), vY(cell (i,j-1)) for v-face (i,j)
-    for (int j = js; j < J1; j++) {
-        const int sa = sj + 1 == RS ? 0 : sj + 1, sb = sa + 1 == RS ? 0 : sa + 1;
-        const int sc = sb + 1 == RS ? 0 : sb + 1, sd = sc + 1 == RS ? 0 : sc + 1;
-        const int sm = sj == 0 ? RS - 1 : sj - 1;
-        const RingRowC& Rm = s.ring[sm];
-        const RingRowC& R0 = s.ring[sj];
-        const RingRowC& Ra = s.ring[sa];
-        const RingRowC& Rb = s.ring[sb];
-        const int cb = j & 1, nb = (j + 1) & 1;
-        cp_wait_all();
-        __syncthreads();                                  // B0
-        ring_issue_tma(s, sd, mm, c0, tma, j + 4);
-        mbar_wait(&s.mbar[sc], ((j + 4 - js) / RS) & 1);   // row j+3
-        ring_derive<false>(s.ring[sc]);
-        const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
-        // per-point instance (REG: the +-3 window of the point is all fluid, so
-        // every kind test folds away; same operations as the general instance)
-        const bool reg = allreg || (kw0 & REG_BIT) != 0u;
-        double Fx1 = 0.0, Fy1 = 0.0, TYn = 0.0, vYn = 0.0, uYn = 0.0;
-        auto stageA = [&](auto regc) {
-            constexpr bool REG = decltype(regc)::value;
-            // ---- stage A: fluxes of row j+1 (Eqs. pl8-pl11 at time level n-1)
-            {
-                double ru = 0.0;
-                if ((REG || flux_face(ukind(kw1)))) {
-                    const double w = Ra.U[lc], r1 = Ra.R[lc - 1], r2 = Ra.R[lc];
-                    ru = w > 0.0 ? r1 : r2;
-                    if (TVD && (REG || ckind(Ra.KK[lc - 2]) == CK_FLUID) && (REG || ckind(Ra.KK[lc - 1]) == CK_FLUID) &&
-                        (REG || ckind(kw1) == CK_FLUID) && (REG || ckind(Ra.KK[lc + 1]) == CK_FLUID))
-                        ru += psi_f(Ra.R[lc - 2], r1, r2, Ra.R[lc + 1], w) * (r2 - r1);
-                    Fx1 = ru * w * dy;
-                }
-                s.FX[nb][lc] = Fx1;
-                double rv = 0.0;
-                if ((REG || vkind(kw1) == FK_ACTIVE)) {
-                    const double w = Ra.V[lc], r1 = R0.R[lc], r2 = Ra.R[lc];
-                    rv = w > 0.0 ? r1 : r2;
-                    if (TVD && (REG || ckind(Rm.KK[lc]) == CK_FLUID) && (REG || ckind(kw0) == CK_FLUID) && (REG || ckind(kw1) == CK_FLUID) &&
-                        (REG || ckind(Rb.KK[lc]) == CK_FLUID))
-                        rv += psi_f(Rm.R[lc], r1, r2, Rb.R[lc], w) * (r2 - r1);
-                    Fy1 = rv * w * dx;
-                }
-                s.FY[nb][lc] = Fy1;
-            }
-            // TX at u-face (i, j): T flux through x^f_i (pl31_1)
-            {
-                double tx = 0.0;
-                if ((REG || flux_face(ukind(kw0)))) {
-                    const double F = s.FX[cb][lc], w = R0.U[lc], Tm = R0.T[lc - 1], Ti = R0.T[lc];
-                    const double ps = (TVD && (REG || ckind(R0.KK[lc - 2]) == CK_FLUID) && (REG || ckind(R0.KK[lc - 1]) == CK_FLUID) &&
-                                       (REG || ckind(kw0) == CK_FLUID) && (REG || ckind(R0.KK[lc + 1]) == CK_FLUID))
-                                    ? psi_f(R0.T[lc - 2], Tm, Ti, R0.T[lc + 1], w) : 0.0;
-                    tx = F * ((w > 0.0 ? Tm : Ti) + (Ti - Tm) * ps);
-                }
-                s.TX[lc] = tx;
-            }
-            // TY at v-face (i, j+1)
-            if ((REG || vkind(kw1) == FK_ACTIVE)) {
-                const double w = Ra.V[lc], Tj = R0.T[lc], Tp = Ra.T[lc];
-                const double ps = (TVD && (REG || ckind(Rm.KK[lc]) == CK_FLUID) && (REG || ckind(kw0) == CK_FLUID) &&
-                                   (REG || ckind(kw1) == CK_FLUID) && (REG || ckind(Rb.KK[lc]) == CK_FLUID))
-                                ? psi_f(Rm.T[lc], Tj, Tp, Rb.T[lc], w) : 0.0;
-                TYn = Fy1 * ((w > 0.0 ? Tj : Tp) + (Tp - Tj) * ps);
-            }
-            // uX at cell (i, j): u flux through the cell centre (transposed pl15_11 x-terms)
-            {
-                double ux = 0.0;
-                if ((REG || ckind(kw0) == CK_FLUID) && (REG || ukind(kw0) == FK_ACTIVE) && (REG || ukind(R0.KK[lc + 1]) == FK_ACTIVE)) {
-                    const double ui = R0.U[lc], up = R0.U[lc + 1], ub = 0.5 * (ui + up);
-                    const bool ok = TVD && (REG || ukind(R0.KK[lc - 1]) == FK_ACTIVE) && (REG || ukind(R0.KK[lc + 2]) == FK_ACTIVE);
-                    const double ps = ok ? psi_f(R0.U[lc - 1], ui, up, R0.U[lc + 2], ub) : 0.0;
-                    ux = dy * R0.R[lc] * ub * ((ub > 0.0 ? ui : up) + (up - ui) * ps);
-                } else if ((REG || ckind(kw0) == CK_FLUID)) {
-                    // a fixed / inlet / outlet face on one side: same formula, no limiter
-                    const double ui = R0.U[lc], up = R0.U[lc + 1], ub = 0.5 * (ui + up);
-                    ux = dy * R0.R[lc] * ub * (ub > 0.0 ? ui : up);
-                }
-                s.UX[lc] = ux;
-            }
-            // vX at (u-face column i, v-row j+1): v flux through x^f_i, both half faces
-            {
-                double vx = 0.0;
-                if ((REG || vkind(kw1) == FK_ACTIVE) || (REG || vkind(Ra.KK[lc - 1]) == FK_ACTIVE)) {
-                    const double vm = Ra.V[lc - 1], vi = Ra.V[lc];
-                    const bool ok = TVD && (REG || vkind(Ra.KK[lc - 2]) == FK_ACTIVE) && (REG || vkind(Ra.KK[lc - 1]) == FK_ACTIVE) &&
-                                    (REG || vkind(kw1) == FK_ACTIVE) && (REG || vkind(Ra.KK[lc + 1]) == FK_ACTIVE);
-                    double sum = 0.0;
-                    if ((REG || flux_face(ukind(kw0)))) {               // lower half: u-face (i, j)
-                        const double F = s.FX[cb][lc], w = R0.U[lc];
-                        const double ps = ok ? psi_f(Ra.V[lc - 2], vm, vi, Ra.V[lc + 1], w) : 0.0;
-                        sum += F * ((w > 0.0 ? vm : vi) + (vi - vm) * ps);
-                    }
-                    if ((REG || flux_face(ukind(kw1)))) {               // upper half: u-face (i, j+1)
-                        const double F = Fx1, w = Ra.U[lc];
-                        const double ps = ok ? psi_f(Ra.V[lc - 2], vm, vi, Ra.V[lc + 1], w) : 0.0;
-                        sum += F * ((w > 0.0 ? vm : vi) + (vi - vm) * ps);
-                    }
-                    vx = 0.5 * sum;
-                }
-                s.VX[lc] = vx;
-            }
-            // vY at cell (i, j+1): v flux through the cell centre (pl15_11 y-terms)
-            if ((REG || ckind(kw1) == CK_FLUID)) {
-                const double vi = Ra.V[lc], vp = Rb.V[lc], vb = 0.5 * (vi + vp);
-                const bool ok = TVD && (REG || vkind(kw1) == FK_ACTIVE) && (REG || vkind(Rb.KK[lc]) == FK_ACTIVE) &&
-                                (REG || vkind(kw0) == FK_ACTIVE) && (REG || vkind(s.ring[sc].KK[lc]) == FK_ACTIVE);
-                const double ps = ok ? psi_f(R0.V[lc], vi, vp, s.ring[sc].V[lc], vb) : 0.0;
-                vYn = dx * Ra.R[lc] * vb * ((vb > 0.0 ? vi : vp) + (vp - vi) * ps);
-            }
-        };
-        if (reg) stageA(std::true_type{}); else stageA(std::false_type{});
-        __syncthreads();                                  // B1
-        auto stageC = [&](auto regc) {
-            constexpr bool REG = decltype(regc)::value;
-            // ---- stage C: uY at (u column i, y^f_{j+1}) and the planes
-            {
-                const double ui = R0.U[lc], up = Ra.U[lc];
-                const bool ok = TVD && (REG || ukind(Rm.KK[lc]) == FK_ACTIVE) && (REG || ukind(kw0) == FK_ACTIVE) &&
-                                (REG || ukind(kw1) == FK_ACTIVE) && (REG || ukind(Rb.KK[lc]) == FK_ACTIVE);
-                double sum = 0.0;
-                for (int h = 0; h < 2; h++) {
-                    const int cc = lc - 1 + h;
-                    if ((!REG && vkind(Ra.KK[cc]) != FK_ACTIVE)) continue;
-                    const double F = s.FY[nb][cc], w = Ra.V[cc];
-                    const double ps = ok ? psi_f(Rm.U[lc], ui, up, Rb.U[lc], w) : 0.0;
-                    sum += F * ((w > 0.0 ? ui : up) + (up - ui) * ps);
-                }
-                uYn = 0.5 * sum;
-            }
-        };
-        if (reg) stageC(std::true_type{}); else stageC(std::false_type{});
-        if (owner) {
-            int tgt = -1000;                               // single-rank periodic: wrapped ghosts
-            if (k.xbc == 1 && k.mirror) {
-                if (gi < OFF) tgt = gi + k.nx;
-                else if (gi >= k.nx - OFF) tgt = gi - k.nx;
-            }
-            if (j >= J0) {                                 // T^exp, u^exp of row j
-                const long long id = gidx(k, gi, j);
-                const double te = ckind(kw0) == CK_FLUID ? (s.TX[lc] - s.TX[lc + 1] + TYc - TYn) : 0.0;
-                const double ue = ukind(kw0) == FK_ACTIVE ? (s.UX[lc - 1] - s.UX[lc] + uYc - uYn) : 0.0;
-                k.Te_w[id] = te;
-                k.ue_w[id] = ue;
-                if (tgt > -1000) { k.Te_w[gidx(k, tgt, j)] = te; k.ue_w[gidx(k, tgt, j)] = ue; }
-            }
-            if (j + 1 >= J0 && j + 1 < J1) {               // v^exp of v-face row j+1 (rows J0 .. J1-1)
-                const double ve = vkind(kw1) == FK_ACTIVE ? (s.VX[lc] - s.VX[lc + 1] + vYc - vYn) : 0.0;
-                k.ve_w[gidx(k, gi, j + 1)] = ve;
-                if (tgt > -1000) k.ve_w[gidx(k, tgt, j + 1)] = ve;
-            }
-        }
-        TYc = TYn;
-        uYc = uYn;
-        vYc = vYn;
-        sj = sa;
+    if (allreg) {
+        constexpr bool ALLREG = true;
+#include "sts_conv_loop.inc"
+    } else {
+        constexpr bool ALLREG = false;
+#include "sts_conv_loop.inc"
     }
     cp_wait_all();
 }
