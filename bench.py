@@ -366,6 +366,8 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--passes", type=int, default=10)
+    # (explicit_tvd: C3 from the free-stream start goes unstable after ~40 steps
+    #  at dt = 0.005 -- DESIGN section 9 -- so time it with --steps 40 or fewer)
     ap.add_argument("--variant", default="implicit_upwind",
                     choices=["implicit_upwind", "implicit_tvd", "explicit_upwind", "explicit_tvd"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
