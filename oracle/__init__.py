@@ -24,6 +24,8 @@ CFLAGS = ["-std=c99", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-Wall"]
 X_INOUT, X_PERIODIC = 0, 1
 EXPLICIT, IMPLICIT = 0, 1
 UPWIND, TVD = 0, 1
+# pressure-work forms of S^T_c (reading R9)
+PW_DPDT, PW_PRINTED, PW_NEG, PW_GAMMA = 0, 1, 2, 3
 FIELDS = {"u": 0, "v": 1, "p": 2, "T": 3, "rho": 4, "gamma": 5, "uexp": 6, "vexp": 7, "Texp": 8}
 
 
@@ -46,7 +48,7 @@ class Params(ctypes.Structure):
         ("T_wall", ctypes.c_double), ("T_square", ctypes.c_double),
         ("g_x", ctypes.c_double), ("g_y", ctypes.c_double),
         ("particle_frame", ctypes.c_int32),
-        ("pw_sign", ctypes.c_double),
+        ("pw_form", ctypes.c_int32), ("r37_off", ctypes.c_int32),
         ("time_scheme", ctypes.c_int32), ("space_scheme", ctypes.c_int32),
         ("dt", ctypes.c_double),
         ("min_passes", ctypes.c_int32), ("max_passes", ctypes.c_int32),
@@ -120,7 +122,8 @@ class Case:
         p.p_in, p.T_in = case.get("p_in", 1.0), case.get("T_in", 1.0)
         p.u_wall_bottom, p.u_wall_top = case.get("u_wall_bottom", 0.0), case.get("u_wall_top", 0.0)
         p.particle_frame = int(case.get("particle_frame", 0))
-        p.pw_sign = float(case["pw_sign"])
+        p.pw_form = int(case.get("pw_form", PW_DPDT))
+        p.r37_off = int(case.get("r37_off", 0))
         p.T_wall, p.T_square = case.get("T_wall", 1.0), case.get("T_square", 1.0)
         p.g_x, p.g_y = case.get("g_x", 0.0), case.get("g_y", 0.0)
         p.time_scheme, p.space_scheme = case["time"], case["space"]

@@ -39,6 +39,7 @@ struct orc_case {
     orc_params P;
     int nx, ny;
     double A, B, CT1, CT2, CT3, u_in;
+    double PWK;                  /* kappa of the p div(u) forms of R9 */
     unsigned char* solid;        /* nx*ny, 1 = inside a square          */
     level L[3];                  /* 0: time n-1, 1: old iterate, 2: new */
     double *ue, *ve, *Te;        /* explicit planes       */
@@ -83,11 +84,11 @@ static int flat(double f2, double f3)
     return fabs(f3 - f2) <= 1e-12 * (1.0 + fabs(f2) + fabs(f3));
 }
 
-/* psi_s, Eq. pl15_2.  Zero denominator -> 0 (R6, R37). */
-double orc_psi_s(double f1, double f2, double f3, double f4,
-                 double d1, double d2, double d3, double d4, double w)
+/* psi_s, Eq. pl15_2, without the R37 flat-stencil guard; a zero
+ * denominator gives 0 (R6). */
+static double psi_s_raw(double f1, double f2, double f3, double f4,
+                        double d1, double d2, double d3, double d4, double w)
 {
-    if (flat(f2, f3)) return 0.0;
     if (w > 0.0) {
         double den = (d1 + d2) * (f3 - f2);
         if (den == 0.0) return 0.0;
@@ -101,11 +102,10 @@ double orc_psi_s(double f1, double f2, double f3, double f4,
     }
 }
 
-/* psi_c, Eq. pl15_1.  Zero denominator -> 0 (R6, R37). */
-double orc_psi_c(double f1, double f2, double f3, double f4,
-                 double d1, double d2, double d3, double w)
+/* psi_c, Eq. pl15_1, without the R37 guard; zero denominator -> 0 (R6). */
+static double psi_c_raw(double f1, double f2, double f3, double f4,
+                        double d1, double d2, double d3, double w)
 {
-    if (flat(f2, f3)) return 0.0;
     if (w > 0.0) {
         double den = d1 * (f3 - f2);
         if (den == 0.0) return 0.0;
@@ -115,6 +115,33 @@ double orc_psi_c(double f1, double f2, double f3, double f4,
         if (den == 0.0) return 0.0;
         return -0.5 * orc_vanleer(d2 * (f4 - f3) / den);
     }
+}
+
+/* psi_s / psi_c of the method: the flat-stencil guard R37, then the limiter. */
+double orc_psi_s(double f1, double f2, double f3, double f4,
+                 double d1, double d2, double d3, double d4, double w)
+{
+    if (flat(f2, f3)) return 0.0;
+    return psi_s_raw(f1, f2, f3, f4, d1, d2, d3, d4, w);
+}
+double orc_psi_c(double f1, double f2, double f3, double f4,
+                 double d1, double d2, double d3, double w)
+{
+    if (flat(f2, f3)) return 0.0;
+    return psi_c_raw(f1, f2, f3, f4, d1, d2, d3, w);
+}
+/* The case's limiter: R37 on, or off for the conditioning test (test hook). */
+static double psi_s_c(const orc_case* c, double f1, double f2, double f3, double f4,
+                      double d1, double d2, double d3, double d4, double w)
+{
+    return c->P.r37_off ? psi_s_raw(f1, f2, f3, f4, d1, d2, d3, d4, w)
+                        : orc_psi_s(f1, f2, f3, f4, d1, d2, d3, d4, w);
+}
+static double psi_c_c(const orc_case* c, double f1, double f2, double f3, double f4,
+                      double d1, double d2, double d3, double w)
+{
+    return c->P.r37_off ? psi_c_raw(f1, f2, f3, f4, d1, d2, d3, w)
+                        : orc_psi_c(f1, f2, f3, f4, d1, d2, d3, w);
 }
 
 static double max0(double a) { return a > 0.0 ? a : 0.0; }
@@ -227,14 +254,14 @@ static int vfaces_ok_y(const orc_case* c, int i, int j0)
 static double psis_cell_x(const orc_case* c, const level* s, int f, int i, int j, double w)
 {
     if (!tvd(c) || !cells_ok_x(c, i - 2, j)) return 0.0;
-    return orc_psi_s(cell(c, s, f, i - 2, j), cell(c, s, f, i - 1, j), cell(c, s, f, i, j),
+    return psi_s_c(c, cell(c, s, f, i - 2, j), cell(c, s, f, i - 1, j), cell(c, s, f, i, j),
                      cell(c, s, f, i + 1, j), DX(c, i - 2), DX(c, i - 1), DX(c, i), DX(c, i + 1), w);
 }
 /* psi_s of a cell-centred scalar at v-face j (stencil j-2..j+1). */
 static double psis_cell_y(const orc_case* c, const level* s, int f, int i, int j, double w)
 {
     if (!tvd(c) || !cells_ok_y(c, i, j - 2)) return 0.0;
-    return orc_psi_s(cell(c, s, f, i, j - 2), cell(c, s, f, i, j - 1), cell(c, s, f, i, j),
+    return psi_s_c(c, cell(c, s, f, i, j - 2), cell(c, s, f, i, j - 1), cell(c, s, f, i, j),
                      cell(c, s, f, i, j + 1), DY(c, j - 2), DY(c, j - 1), DY(c, j), DY(c, j + 1), w);
 }
 
@@ -302,6 +329,60 @@ static double wall_T_of(const orc_case* c, int i, int j)
     return cell_kind(c, i, j) == K_WALLY ? c->P.T_wall : c->P.T_square;
 }
 
+/* Face value of a cell-centred scalar on the face between cells a (width da)
+ * and b (width db): linear interpolation between the two centres. */
+static double face_interp(double fa, double fb, double da, double db)
+{
+    return (db * fa + da * fb) / (da + db);
+}
+
+/* Pressure work of S^T_c per unit volume, reading R9.
+ * The continuum energy equation is the enthalpy form with +C^T3 Dp/Dt
+ * (Eq. pl6; C^T1, C^T2, C^T3 = (gamma-1)/gamma of Eq. pl37 are its
+ * c_p-form coefficients), the printed discrete source is +C^T3 p div(u)
+ * (Eq. pl29).  Default ORC_PW_DPDT discretises the continuum term at
+ * the old iterate, as the rest of S^T_c:
+ *   C^T3 [ (p_{i,j} - p^{n-1}_{i,j}) / dt
+ *          + ubar_{i,j} (p_e - p_w) / dx_i + vbar_{i,j} (p_n - p_s) / dy_j ],
+ * ubar = (u_{i,j} + u_{i+1,j}) / 2, vbar = (v_{i,j} + v_{i,j+1}) / 2, p_e the
+ * face value between cells i and i+1 (linear interpolation), p_e = p_{i,j}
+ * when the neighbour is solid or beyond a wall (dp/dn = 0 at a wall, no flow
+ * through it); likewise p_w, p_n, p_s.  The other forms are kappa p div(u)
+ * with kappa = +C^T3 (as printed), -C^T3 (round-1 reading) or -gamma C^T3. */
+static double pressure_work(const orc_case* c, int i, int j, double div)
+{
+    const level* o = OLD;
+    const double pc = PP(o, i, j);
+    if (c->P.pw_form != ORC_PW_DPDT) return c->PWK * pc * div;
+    const double dx = DX(c, i), dy = DY(c, j);
+    double pe = is_wallish(c, i + 1, j) ? pc : face_interp(pc, PP(o, i + 1, j), dx, DX(c, i + 1));
+    double pw = is_wallish(c, i - 1, j) ? pc : face_interp(PP(o, i - 1, j), pc, DX(c, i - 1), dx);
+    double pn = is_wallish(c, i, j + 1) ? pc : face_interp(pc, PP(o, i, j + 1), dy, DY(c, j + 1));
+    double ps = is_wallish(c, i, j - 1) ? pc : face_interp(PP(o, i, j - 1), pc, DY(c, j - 1), dy);
+    double ub = 0.5 * (U(c, o, i, j) + U(c, o, i + 1, j));
+    double vb = 0.5 * (V(c, o, i, j) + V(c, o, i, j + 1));
+    double dpdt = (pc - PP(N1, i, j)) / c->P.dt;
+    return c->CT3 * (dpdt + ub * (pe - pw) / dx + vb * (pn - ps) / dy);
+}
+
+/* Tangential wall velocity u_w of the wall cell (i, j): the channel walls
+ * move (BC spec 6, R14), the squares are at rest (R15). */
+static double wall_u_of(const orc_case* c, int i, int j)
+{
+    (void)i;
+    if (cell_kind(c, i, j) == K_WALLY) return j < 0 ? c->P.u_wall_bottom : c->P.u_wall_top;
+    return 0.0;
+}
+/* Gas velocity at a wall surface from the slip condition Eq. pl38,
+ * v_s - v_w = zeta (v_P - v_s) / dn, zeta = 1.1466 Kn / rho_local:
+ * v_s = (dn v_w + zeta v_P) / (dn + zeta); v_P = tangential velocity at the
+ * centre of the wall-adjacent cell, dn = half its width (reading R38). */
+static double slip_velocity(const orc_case* c, double vP, double vw, double rho, double dn)
+{
+    double zeta = 1.1466 * c->P.Kn / rho;
+    return (dn * vw + zeta * vP) / (dn + zeta);
+}
+
 /* ===================================================== phase A: energy */
 /* Temperature at fluid cell (i,j): Eqs. pl30-pl33, pl28-pl29, pl31_1
  * (P:432-498).  Returns T_{i,j} of this pass. */
@@ -363,10 +444,18 @@ static double T_equation(const orc_case* c, int i, int j)
     double vW = 0.25 * (V(c, o, i - 1, j) + V(c, o, i, j) + V(c, o, i - 1, j + 1) + V(c, o, i, j + 1));
     double uN = 0.25 * (U(c, o, i, j) + U(c, o, i + 1, j) + U(c, o, i, j + 1) + U(c, o, i + 1, j + 1));
     double uS = 0.25 * (U(c, o, i, j - 1) + U(c, o, i + 1, j - 1) + U(c, o, i, j) + U(c, o, i + 1, j));
+    /* A mid-face velocity on a face that lies on a wall is the gas velocity at
+     * the surface: the slip velocity of Eq. pl38 (reading R38) */
+    if (is_wallish(c, i + 1, j)) vE = slip_velocity(c, 0.5 * (V(c, o, i, j) + V(c, o, i, j + 1)), 0.0, rP, 0.5 * dx);
+    if (is_wallish(c, i - 1, j)) vW = slip_velocity(c, 0.5 * (V(c, o, i, j) + V(c, o, i, j + 1)), 0.0, rP, 0.5 * dx);
+    if (is_wallish(c, i, j + 1))
+        uN = slip_velocity(c, 0.5 * (U(c, o, i, j) + U(c, o, i + 1, j)), wall_u_of(c, i, j + 1), rP, 0.5 * dy);
+    if (is_wallish(c, i, j - 1))
+        uS = slip_velocity(c, 0.5 * (U(c, o, i, j) + U(c, o, i + 1, j)), wall_u_of(c, i, j - 1), rP, 0.5 * dy);
     double shear = (vE - vW) / dx + (uN - uS) / dy;
     double div = dudx + dvdy;
     double Sc = c->CT2 * gP * (2.0 * (dudx * dudx + dvdy * dvdy) + shear * shear - 2.0 / 3.0 * div * div) * dx * dy
-              + c->P.pw_sign * c->CT3 * PP(o, i, j) * div * dx * dy;               /* R9: sign s */
+              + pressure_work(c, i, j, div) * dx * dy;
 
     double Texp = impl ? 0.0 : c->Te[IC(c, i, j)];
     double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + Sc + Texp)
@@ -398,10 +487,10 @@ static void u_equation(const orc_case* c, int i, int j, double* uhat, double* du
     double psW = 0, psE = 0;
     if (impl && tvd(c)) {
         if (ufaces_ok_x(c, i - 2, j))
-            psW = orc_psi_c(U(c, o, i - 2, j), U(c, o, i - 1, j), U(c, o, i, j), U(c, o, i + 1, j),
+            psW = psi_c_c(c, U(c, o, i - 2, j), U(c, o, i - 1, j), U(c, o, i, j), U(c, o, i + 1, j),
                             DX(c, i - 2), DX(c, i - 1), DX(c, i), ubW);
         if (ufaces_ok_x(c, i - 1, j))
-            psE = orc_psi_c(U(c, o, i - 1, j), U(c, o, i, j), U(c, o, i + 1, j), U(c, o, i + 2, j),
+            psE = psi_c_c(c, U(c, o, i - 1, j), U(c, o, i, j), U(c, o, i + 1, j), U(c, o, i + 2, j),
                             DX(c, i - 1), DX(c, i), DX(c, i + 1), ubE);
     }
     a1 = (impl ? max0(FbW) - FbW * psW : 0.0) + 4.0 / 3.0 * Dux_i;
@@ -419,8 +508,8 @@ static void u_equation(const orc_case* c, int i, int j, double* uhat, double* du
         double p1 = 0, p2 = 0;
         if (impl && tvd(c) && ufaces_ok_y(c, i, j - 2)) {
             double f1 = U(c, o, i, j - 2), f2 = U(c, o, i, j - 1), f3 = U(c, o, i, j), f4 = U(c, o, i, j + 1);
-            p1 = orc_psi_s(f1, f2, f3, f4, DY(c, j - 2), DY(c, j - 1), DY(c, j), DY(c, j + 1), V(c, o, i, j));
-            p2 = orc_psi_s(f1, f2, f3, f4, DY(c, j - 2), DY(c, j - 1), DY(c, j), DY(c, j + 1), V(c, o, i - 1, j));
+            p1 = psi_s_c(c, f1, f2, f3, f4, DY(c, j - 2), DY(c, j - 1), DY(c, j), DY(c, j + 1), V(c, o, i, j));
+            p2 = psi_s_c(c, f1, f2, f3, f4, DY(c, j - 2), DY(c, j - 1), DY(c, j), DY(c, j + 1), V(c, o, i - 1, j));
         }
         double Duy = c->B * gam_corner(c, o, i, j) * (dxR + dxL) / (dy + DY(c, j - 1));
         a3 = (impl ? 0.5 * (max0(Fs_i) - Fs_i * p1 + max0(Fs_im1) - Fs_im1 * p2) : 0.0) + Duy;
@@ -436,8 +525,8 @@ static void u_equation(const orc_case* c, int i, int j, double* uhat, double* du
         double p1 = 0, p2 = 0;
         if (impl && tvd(c) && ufaces_ok_y(c, i, j - 1)) {
             double f1 = U(c, o, i, j - 1), f2 = U(c, o, i, j), f3 = U(c, o, i, j + 1), f4 = U(c, o, i, j + 2);
-            p1 = orc_psi_s(f1, f2, f3, f4, DY(c, j - 1), DY(c, j), DY(c, j + 1), DY(c, j + 2), V(c, o, i, j + 1));
-            p2 = orc_psi_s(f1, f2, f3, f4, DY(c, j - 1), DY(c, j), DY(c, j + 1), DY(c, j + 2), V(c, o, i - 1, j + 1));
+            p1 = psi_s_c(c, f1, f2, f3, f4, DY(c, j - 1), DY(c, j), DY(c, j + 1), DY(c, j + 2), V(c, o, i, j + 1));
+            p2 = psi_s_c(c, f1, f2, f3, f4, DY(c, j - 1), DY(c, j), DY(c, j + 1), DY(c, j + 2), V(c, o, i - 1, j + 1));
         }
         double Duy = c->B * gam_corner(c, o, i, j + 1) * (dxR + dxL) / (DY(c, j + 1) + dy);
         a4 = (impl ? 0.5 * (max0(-Fn_i) - Fn_i * p1 + max0(-Fn_im1) - Fn_im1 * p2) : 0.0) + Duy;
@@ -487,10 +576,10 @@ static void v_equation(const orc_case* c, int i, int j, double* vhat, double* dv
     double psS = 0, psN = 0;
     if (impl && tvd(c)) {
         if (vfaces_ok_y(c, i, j - 2))
-            psS = orc_psi_c(V(c, o, i, j - 2), V(c, o, i, j - 1), V(c, o, i, j), V(c, o, i, j + 1),
+            psS = psi_c_c(c, V(c, o, i, j - 2), V(c, o, i, j - 1), V(c, o, i, j), V(c, o, i, j + 1),
                             DY(c, j - 2), DY(c, j - 1), DY(c, j), vbS);
         if (vfaces_ok_y(c, i, j - 1))
-            psN = orc_psi_c(V(c, o, i, j - 1), V(c, o, i, j), V(c, o, i, j + 1), V(c, o, i, j + 2),
+            psN = psi_c_c(c, V(c, o, i, j - 1), V(c, o, i, j), V(c, o, i, j + 1), V(c, o, i, j + 2),
                             DY(c, j - 1), DY(c, j), DY(c, j + 1), vbN);
     }
     a3 = (impl ? max0(FbS) - FbS * psS : 0.0) + 4.0 / 3.0 * Dvy_j;      /* a^vc_3 + 4/3 D^vy */
@@ -508,8 +597,8 @@ static void v_equation(const orc_case* c, int i, int j, double* vhat, double* dv
         double p1 = 0, p2 = 0;
         if (impl && tvd(c) && vfaces_ok_x(c, i - 2, j)) {
             double f1 = V(c, o, i - 2, j), f2 = V(c, o, i - 1, j), f3 = V(c, o, i, j), f4 = V(c, o, i + 1, j);
-            p1 = orc_psi_s(f1, f2, f3, f4, DX(c, i - 2), DX(c, i - 1), DX(c, i), DX(c, i + 1), U(c, o, i, j));
-            p2 = orc_psi_s(f1, f2, f3, f4, DX(c, i - 2), DX(c, i - 1), DX(c, i), DX(c, i + 1), U(c, o, i, j - 1));
+            p1 = psi_s_c(c, f1, f2, f3, f4, DX(c, i - 2), DX(c, i - 1), DX(c, i), DX(c, i + 1), U(c, o, i, j));
+            p2 = psi_s_c(c, f1, f2, f3, f4, DX(c, i - 2), DX(c, i - 1), DX(c, i), DX(c, i + 1), U(c, o, i, j - 1));
         }
         double Dvx = c->B * gam_corner(c, o, i, j) * (dyT + dyB) / (dx + DX(c, i - 1));
         a1 = (impl ? 0.5 * (max0(Fw_j) - Fw_j * p1 + max0(Fw_jm1) - Fw_jm1 * p2) : 0.0) + Dvx;
@@ -525,8 +614,8 @@ static void v_equation(const orc_case* c, int i, int j, double* vhat, double* dv
         double p1 = 0, p2 = 0;
         if (impl && tvd(c) && vfaces_ok_x(c, i - 1, j)) {
             double f1 = V(c, o, i - 1, j), f2 = V(c, o, i, j), f3 = V(c, o, i + 1, j), f4 = V(c, o, i + 2, j);
-            p1 = orc_psi_s(f1, f2, f3, f4, DX(c, i - 1), DX(c, i), DX(c, i + 1), DX(c, i + 2), U(c, o, i + 1, j));
-            p2 = orc_psi_s(f1, f2, f3, f4, DX(c, i - 1), DX(c, i), DX(c, i + 1), DX(c, i + 2), U(c, o, i + 1, j - 1));
+            p1 = psi_s_c(c, f1, f2, f3, f4, DX(c, i - 1), DX(c, i), DX(c, i + 1), DX(c, i + 2), U(c, o, i + 1, j));
+            p2 = psi_s_c(c, f1, f2, f3, f4, DX(c, i - 1), DX(c, i), DX(c, i + 1), DX(c, i + 2), U(c, o, i + 1, j - 1));
         }
         double Dvx = c->B * gam_corner(c, o, i + 1, j) * (dyT + dyB) / (DX(c, i + 1) + dx);
         a2 = (impl ? 0.5 * (max0(-Fe_j) - Fe_j * p1 + max0(-Fe_jm1) - Fe_jm1 * p2) : 0.0) + Dvx;
@@ -598,7 +687,7 @@ static double v_explicit(const orc_case* c, int i, int j)
             int jj = (h == 0) ? j - 1 : j;
             if (!flux_face_u(ukind(c, i + 1, jj))) continue;
             double F = Fx(c, s, i + 1, jj), w = U(c, s, i + 1, jj);
-            double ps = ok ? orc_psi_s(V(c, s, i - 1, j), vi, vp, V(c, s, i + 2, j),
+            double ps = ok ? psi_s_c(c, V(c, s, i - 1, j), vi, vp, V(c, s, i + 2, j),
                                        DX(c, i - 1), DX(c, i), DX(c, i + 1), DX(c, i + 2), w) : 0.0;
             sum += F * (orc_upwind(vi, vp, w) + (vp - vi) * ps);
         }
@@ -613,7 +702,7 @@ static double v_explicit(const orc_case* c, int i, int j)
             int jj = (h == 0) ? j - 1 : j;
             if (!flux_face_u(ukind(c, i, jj))) continue;
             double F = Fx(c, s, i, jj), w = U(c, s, i, jj);
-            double ps = ok ? orc_psi_s(V(c, s, i - 2, j), vm, vi, V(c, s, i + 1, j),
+            double ps = ok ? psi_s_c(c, V(c, s, i - 2, j), vm, vi, V(c, s, i + 1, j),
                                        DX(c, i - 2), DX(c, i - 1), DX(c, i), DX(c, i + 1), w) : 0.0;
             sum += F * (orc_upwind(vm, vi, w) + (vi - vm) * ps);
         }
@@ -624,7 +713,7 @@ static double v_explicit(const orc_case* c, int i, int j)
         double vp = V(c, s, i, j + 1);
         double vb = 0.5 * (vi + vp);
         double ps = (tv && vfaces_ok_y(c, i, j - 1))
-                  ? orc_psi_c(V(c, s, i, j - 1), vi, vp, V(c, s, i, j + 2), DY(c, j - 1), DY(c, j), DY(c, j + 1), vb) : 0.0;
+                  ? psi_c_c(c, V(c, s, i, j - 1), vi, vp, V(c, s, i, j + 2), DY(c, j - 1), DY(c, j), DY(c, j + 1), vb) : 0.0;
         e += -DX(c, i) * RHO(s, i, j) * vb * (orc_upwind(vi, vp, vb) + (vp - vi) * ps);
     }
     /* south: + dx_i rho_{i,j-1} vbar_S [upwind(v_{j-1}, v_j, vbar_S) + (v_j - v_{j-1}) psi_c] */
@@ -632,7 +721,7 @@ static double v_explicit(const orc_case* c, int i, int j)
         double vm = V(c, s, i, j - 1);
         double vb = 0.5 * (vm + vi);
         double ps = (tv && vfaces_ok_y(c, i, j - 2))
-                  ? orc_psi_c(V(c, s, i, j - 2), vm, vi, V(c, s, i, j + 1), DY(c, j - 2), DY(c, j - 1), DY(c, j), vb) : 0.0;
+                  ? psi_c_c(c, V(c, s, i, j - 2), vm, vi, V(c, s, i, j + 1), DY(c, j - 2), DY(c, j - 1), DY(c, j), vb) : 0.0;
         e += DX(c, i) * RHO(s, i, j - 1) * vb * (orc_upwind(vm, vi, vb) + (vi - vm) * ps);
     }
     return e;
@@ -654,7 +743,7 @@ static double u_explicit(const orc_case* c, int i, int j)
             int ii = (h == 0) ? i - 1 : i;
             if (vkind(c, ii, j + 1) != F_ACTIVE) continue;
             double F = Fy(c, s, ii, j + 1), w = V(c, s, ii, j + 1);
-            double ps = ok ? orc_psi_s(U(c, s, i, j - 1), ui, up, U(c, s, i, j + 2),
+            double ps = ok ? psi_s_c(c, U(c, s, i, j - 1), ui, up, U(c, s, i, j + 2),
                                        DY(c, j - 1), DY(c, j), DY(c, j + 1), DY(c, j + 2), w) : 0.0;
             sum += F * (orc_upwind(ui, up, w) + (up - ui) * ps);
         }
@@ -669,7 +758,7 @@ static double u_explicit(const orc_case* c, int i, int j)
             int ii = (h == 0) ? i - 1 : i;
             if (vkind(c, ii, j) != F_ACTIVE) continue;
             double F = Fy(c, s, ii, j), w = V(c, s, ii, j);
-            double ps = ok ? orc_psi_s(U(c, s, i, j - 2), um, ui, U(c, s, i, j + 1),
+            double ps = ok ? psi_s_c(c, U(c, s, i, j - 2), um, ui, U(c, s, i, j + 1),
                                        DY(c, j - 2), DY(c, j - 1), DY(c, j), DY(c, j + 1), w) : 0.0;
             sum += F * (orc_upwind(um, ui, w) + (ui - um) * ps);
         }
@@ -680,7 +769,7 @@ static double u_explicit(const orc_case* c, int i, int j)
         double up = U(c, s, i + 1, j);
         double ub = 0.5 * (ui + up);
         double ps = (tv && ufaces_ok_x(c, i - 1, j))
-                  ? orc_psi_c(U(c, s, i - 1, j), ui, up, U(c, s, i + 2, j), DX(c, i - 1), DX(c, i), DX(c, i + 1), ub) : 0.0;
+                  ? psi_c_c(c, U(c, s, i - 1, j), ui, up, U(c, s, i + 2, j), DX(c, i - 1), DX(c, i), DX(c, i + 1), ub) : 0.0;
         e += -DY(c, j) * RHO(s, i, j) * ub * (orc_upwind(ui, up, ub) + (up - ui) * ps);
     }
     /* west: + dy_j rho_{i-1,j} ubar_W [...] */
@@ -688,7 +777,7 @@ static double u_explicit(const orc_case* c, int i, int j)
         double um = U(c, s, i - 1, j);
         double ub = 0.5 * (um + ui);
         double ps = (tv && ufaces_ok_x(c, i - 2, j))
-                  ? orc_psi_c(U(c, s, i - 2, j), um, ui, U(c, s, i + 1, j), DX(c, i - 2), DX(c, i - 1), DX(c, i), ub) : 0.0;
+                  ? psi_c_c(c, U(c, s, i - 2, j), um, ui, U(c, s, i + 1, j), DX(c, i - 2), DX(c, i - 1), DX(c, i), ub) : 0.0;
         e += DY(c, j) * RHO(s, i - 1, j) * ub * (orc_upwind(um, ui, ub) + (ui - um) * ps);
     }
     return e;
@@ -896,7 +985,7 @@ static void free_level(level* l)
 orc_case* orc_create(const orc_params* prm, const int32_t* squares, int32_t n_sq)
 {
     if (!prm || prm->nx < 1 || prm->ny < 1 || !(prm->dx > 0) || !(prm->dy > 0) || !(prm->Kn > 0) ||
-        !(prm->dt > 0) || prm->max_passes < 1 || !(prm->pw_sign == 1.0 || prm->pw_sign == -1.0))
+        !(prm->dt > 0) || prm->max_passes < 1 || prm->pw_form < ORC_PW_DPDT || prm->pw_form > ORC_PW_GAMMA)
         return NULL;
     orc_case* c = calloc(1, sizeof *c);
     c->P = *prm;
@@ -908,6 +997,8 @@ orc_case* orc_create(const orc_params* prm, const int32_t* squares, int32_t n_sq
     c->CT1 = prm->Kn * sqrt(M_PI * 225.0 / 1024.0);
     c->CT2 = sqrt(M_PI) / 4.0 * prm->Kn;
     c->CT3 = 2.0 / 5.0;
+    /* kappa of the p div(u) forms of reading R9 */
+    c->PWK = prm->pw_form == ORC_PW_PRINTED ? c->CT3 : prm->pw_form == ORC_PW_NEG ? -c->CT3 : -prm->gamma * c->CT3;
     /* u_in = M sqrt(gamma/2): V0 = sqrt(2 R T0), sound speed sqrt(gamma R T_in) */
     c->u_in = prm->mach * sqrt(prm->gamma / 2.0 * prm->T_in);
     if (prm->particle_frame) {           /* walls move with the gas in the particle frame (R14) */

@@ -28,6 +28,8 @@ enum { ORC_X_INOUT = 0, ORC_X_PERIODIC = 1 };
 enum { ORC_EXPLICIT = 0, ORC_IMPLICIT = 1 };
 /* Space treatment of the convective terms. */
 enum { ORC_UPWIND = 0, ORC_TVD = 1 };
+/* Pressure-work forms of S^T_c (reading R9). */
+enum { ORC_PW_DPDT = 0, ORC_PW_PRINTED = 1, ORC_PW_NEG = 2, ORC_PW_GAMMA = 3 };
 /* Field ids for set/get. */
 enum { ORC_U = 0, ORC_V = 1, ORC_P = 2, ORC_T = 3, ORC_RHO = 4, ORC_GAMMA = 5,
        ORC_UEXP = 6, ORC_VEXP = 7, ORC_TEXP = 8 };
@@ -43,9 +45,14 @@ typedef struct {
     double  g_x, g_y;         /* body force (Eqs. pl2/pl3)          */
     int32_t particle_frame;   /* 1: both channel walls move at +u_in (P:686,
                                  reading R14); overrides u_wall_bottom/top      */
-    double  pw_sign;          /* sign s of the pressure-work term of S^T_c,
-                                 s*C^T3*p*div(u)*dx*dy: +1 as printed,
-                                 -1 reading R9 (compression heats)       */
+    int32_t pw_form;          /* pressure-work term of S^T_c (reading R9):
+                                 ORC_PW_DPDT  C^T3 Dp/Dt of Eq. pl6 at
+                                              the old iterate (default)
+                                 ORC_PW_PRINTED  +C^T3 p div(u) (Eq. pl29)
+                                 ORC_PW_NEG      -C^T3 p div(u) (round-1 R9)
+                                 ORC_PW_GAMMA    -gamma C^T3 p div(u)          */
+    int32_t r37_off;          /* test hook: 1 switches the R37 flat-stencil
+                                 guard of psi_s / psi_c off (DESIGN R37)       */
     int32_t time_scheme;      /* ORC_EXPLICIT / ORC_IMPLICIT                   */
     int32_t space_scheme;     /* ORC_UPWIND / ORC_TVD                          */
     double  dt;               /* time step                                     */

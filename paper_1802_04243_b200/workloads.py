@@ -19,6 +19,9 @@ import numpy as np
 EXPLICIT, IMPLICIT = 0, 1
 UPWIND, TVD = 0, 1
 X_INOUT, X_PERIODIC = 0, 1
+# pressure-work forms of S^T_c (reading R9): C^T3 Dp/Dt (default), +C^T3 p div u
+# (as printed), -C^T3 p div u (round-1 reading), -gamma C^T3 p div u
+PW_DPDT, PW_PRINTED, PW_NEG, PW_GAMMA = 0, 1, 2, 3
 
 VARIANTS = {
     "explicit_upwind": (EXPLICIT, UPWIND),
@@ -29,7 +32,7 @@ VARIANTS = {
 
 PAPER_GAS = dict(Kn=0.001, mach=2.43, gamma=5.0 / 3.0, p_in=1.0, T_in=1.0,
                  T_wall=1.0, T_square=1.0, g_x=0.0, g_y=0.0, particle_frame=1,
-                 pw_sign=-1.0)   # reading R9: -1 = compression heats; +1 = as printed
+                 pw_form=0)   # reading R9: 0 = C^T3 Dp/Dt of Eq. pl6
 
 
 def _case(nx, ny, spacing, squares, variant, dt, passes, **kw):
@@ -42,15 +45,23 @@ def _case(nx, ny, spacing, squares, variant, dt, passes, **kw):
     return c
 
 
+def supersonic_dt(spacing, variant):
+    """Time step of the supersonic cases (reading R12): dt = 0.1 Delta (convective
+    CFL (u_in + c) dt / Delta = 0.31); explicit TVD takes half of it (R39: forward
+    Euler on the limited convective terms turns non-physical at CFL 0.31 within
+    ~50 steps in the oracle and on the GPU alike, stable at 0.16)."""
+    return (0.05 if variant == "explicit_tvd" else 0.1) * spacing
+
+
 def c1(variant="explicit_upwind", passes=10):
     """C1: L = 30, H = 10, Delta = 0.25 -> 120 x 40; one square [5.5,6.5]x[4.5,5.5]
     = cells i 22..25, j 18..21 (centred in y -> mirror symmetric); dt = 0.1 Delta."""
-    return _case(120, 40, 0.25, [(22, 18, 4, 4)], variant, 0.025, passes, name="C1")
+    return _case(120, 40, 0.25, [(22, 18, 4, 4)], variant, supersonic_dt(0.25, variant), passes, name="C1")
 
 
 def c1_small(variant="implicit_upwind", passes=4):
     """A 48 x 16 cut of C1 (Delta = 0.25, one 4x4 square centred in y) for fast parity."""
-    return _case(48, 16, 0.25, [(10, 6, 4, 4)], variant, 0.025, passes, name="C1s")
+    return _case(48, 16, 0.25, [(10, 6, 4, 4)], variant, supersonic_dt(0.25, variant), passes, name="C1s")
 
 
 def c3(H=200, variant="implicit_upwind", passes=10):
@@ -59,21 +70,21 @@ def c3(H=200, variant="implicit_upwind", passes=10):
     ny = int(round(H / 0.05))
     nsq = int(round(H / 10))
     squares = [(110, 90 + 200 * k, 20, 20) for k in range(nsq)]
-    return _case(4032, ny, 0.05, squares, variant, 0.005, passes, name=f"C3_H{H}")
+    return _case(4032, ny, 0.05, squares, variant, supersonic_dt(0.05, variant), passes, name=f"C3_H{H}")
 
 
 def c3_long(G, variant="implicit_upwind", passes=10):
     """Weak-scaling channel for G GPUs: G copies of the C3 H = 200 mesh laid end to
     end (4032 G x 4000, a column of 20 squares every 201.6 units), one slab per GPU."""
     squares = [(110 + 4032 * m, 90 + 200 * k, 20, 20) for m in range(G) for k in range(20)]
-    return _case(4032 * G, 4000, 0.05, squares, variant, 0.005, passes, name=f"C3L_G{G}")
+    return _case(4032 * G, 4000, 0.05, squares, variant, supersonic_dt(0.05, variant), passes, name=f"C3L_G{G}")
 
 
 def c4(variant="implicit_upwind", passes=10):
     """C4: H = 200, L = 201.6, Delta = 0.02 -> 10080 x 10000 (100.8 M FVs);
     20 squares of 50x50 cells at i0 = 275, j0 = 225 + 500k."""
     squares = [(275, 225 + 500 * k, 50, 50) for k in range(20)]
-    return _case(10080, 10000, 0.02, squares, variant, 0.002, passes, name="C4")
+    return _case(10080, 10000, 0.02, squares, variant, supersonic_dt(0.02, variant), passes, name="C4")
 
 
 def c5(G=1, variant="implicit_upwind", passes=10):
@@ -82,7 +93,7 @@ def c5(G=1, variant="implicit_upwind", passes=10):
     nx = 37500 * G
     squares = [(110 + 500 * m, 90 + 200 * k, 20, 20) for m in range(nx // 500) for k in range(20)
                if 110 + 500 * m + 20 <= nx - 1]
-    return _case(nx, 4000, 0.05, squares, variant, 0.005, passes, name=f"C5_G{G}")
+    return _case(nx, 4000, 0.05, squares, variant, supersonic_dt(0.05, variant), passes, name=f"C5_G{G}")
 
 
 def channel(nx, ny, spacing=0.25, variant="implicit_upwind", passes=4, squares=(), **kw):
