@@ -56,6 +56,8 @@ typedef enum { STS_UPWIND = 0, STS_TVD_VANLEER = 1 } sts_space_scheme;
  * (the paper's channel, DESIGN 3.5 items 2-3), or periodic
  * (validation cases, DESIGN 3.5 item 4). */
 typedef enum { STS_X_INFLOW_OUTFLOW = 0, STS_X_PERIODIC = 1 } sts_xbc;
+/* Pressure-work form of the energy source S^T_c (reading R9). */
+typedef enum { STS_PW_DPDT = 0, STS_PW_PRINTED = 1, STS_PW_NEG = 2, STS_PW_GAMMA = 3 } sts_pw_form;
 typedef enum {
     STS_U = 0, STS_V = 1, STS_P = 2, STS_T = 3, STS_RHO = 4,
     STS_UEXP = 6, STS_VEXP = 7, STS_TEXP = 8      /* explicit planes (read only) */
@@ -77,15 +79,20 @@ typedef struct { int32_t i0, j0, ni, nj; } sts_square;
  * (V0 = sqrt(2 R T0)).  particle_frame = 1 makes both channel walls
  * move at +u_in (reading R14) and overrides u_wall_*.  T_wall is the
  * channel-wall temperature (= reference), T_square the square's
- * (R15).  g_x, g_y: body force of Eqs. pl2/pl3 (R22).  pw_sign in {-1, +1}:
- * sign of the pressure-work term of S^T_c (Eq. pl29, reading R9). */
+ * (R15).  g_x, g_y: body force of Eqs. pl2/pl3 (R22).  pw_form: the
+ * pressure-work term of S^T_c (reading R9): STS_PW_DPDT (0,
+ * default) = C^T3 Dp/Dt of the continuum energy equation Eq. pl6 at the
+ * old iterate; STS_PW_PRINTED (1) = +C^T3 p div(u) as printed in Eq. pl29
+ * (P:479); STS_PW_NEG (2) = -C^T3 p div(u); STS_PW_GAMMA (3) =
+ * -gamma C^T3 p div(u).  Any other value -> STS_E_CONFIG. */
 typedef struct {
     double Kn, mach, gamma;
     double p_in, T_in;
     double u_wall_bottom, u_wall_top;
     double T_wall, T_square;
     double g_x, g_y;
-    double pw_sign;
+    int32_t pw_form;             /* sts_pw_form */
+    int32_t reserved0;           /* must be 0 */
     int32_t particle_frame;
     int32_t xbc;                 /* sts_xbc */
 } sts_gas;

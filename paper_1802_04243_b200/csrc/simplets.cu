@@ -7,7 +7,7 @@
 // the host during a run.  Multi-GPU slabs along x: halo exchange over
 // NCCL after every pass.
 #include "../../include/simplets.h"
-#include "sts_kernels.cuh"
+#include "sts_common.cuh"
 #include "sts_march.cuh"
 #include "sts_conv.cuh"
 
@@ -92,11 +92,9 @@ struct sts_ctx {
     Snapshot snap[3];
     int cur = 0;                           // index of the current state snapshot
     double *ue = nullptr, *ve = nullptr, *Te = nullptr;
-    uint8_t *ck = nullptr, *uk = nullptr, *vk = nullptr;
     uint32_t* kind32 = nullptr;            // packed ck | uk << 8 | vk << 16, (ny+1) x pitch
     std::vector<uint8_t> h_ck, h_uk, h_vk; // host copies of the local kind maps
     std::vector<uint8_t> h_solid;          // global solid map (nx x ny), for set_field
-    bool use_tile = false;                 // STS_KERNEL=tile: v1 2-D tile kernel
     int march_seg = 0, march_nseg = 0, march_nstrips = 0;
     int* cta_order = nullptr;              // launch order of the march CTAs (longest first)
     int* cta_split = nullptr;              // the same CTAs, edge strips (0, last) first, then the interior
@@ -267,13 +265,6 @@ __global__ void halo_unpack_kernel(int ny, int pitch, int c0, double* u, double*
 }
 
 // ------------------------------------------------------------- kernel table
-typedef void (*pass_fn)(Params);
-static pass_fn pass_table(int impl, int tvd)
-{
-    if (impl) return tvd ? pass_kernel<true, true> : pass_kernel<true, false>;
-    return tvd ? pass_kernel<false, true> : pass_kernel<false, false>;
-}
-static pass_fn conv_table(int tvd) { return tvd ? conv_kernel<true> : conv_kernel<false>; }
 typedef void (*march_fn)(MarchParams);
 static march_fn march_table(int impl, int tvd)
 {
@@ -291,9 +282,6 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
 {
     static bool done = false;
     if (done) return STS_OK;
-    const int bytes = (int)sizeof(Smem);
-    pass_fn fns[6] = {pass_table(0, 0), pass_table(0, 1), pass_table(1, 0), pass_table(1, 1), conv_table(0), conv_table(1)};
-    for (pass_fn f : fns) CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     march_fn mfs[8] = {march_table(0, 0), march_table(0, 1), march_table(1, 0), march_table(1, 1),
                        march_graph_table(0, 0), march_graph_table(0, 1), march_graph_table(1, 0), march_graph_table(1, 1)};
     for (march_fn f : mfs)
@@ -315,8 +303,10 @@ static Params make_params(const sts_ctx* c)
     k.A = c->A; k.B = c->B; k.CT1 = c->CT1; k.CT2 = c->CT2; k.CT3 = c->CT3; k.Kn = c->gas.Kn;
     k.u_in = c->u_in; k.p_in = c->gas.p_in; k.T_in = c->gas.T_in;
     k.u_wb = c->u_wb; k.u_wt = c->u_wt; k.T_wall = c->gas.T_wall; k.T_sq = c->gas.T_square;
-    k.g_x = c->gas.g_x; k.g_y = c->gas.g_y; k.pw_sign = c->gas.pw_sign;
-    k.ck = c->ck; k.uk = c->uk; k.vk = c->vk;
+    k.g_x = c->gas.g_x; k.g_y = c->gas.g_y;
+    // pressure-work form of S^T_c (reading R9) and kappa of the p div(u) forms
+    k.pw_form = c->gas.pw_form;
+    k.pwk = c->gas.pw_form == PW_PRINTED ? c->CT3 : c->gas.pw_form == PW_NEG ? -c->CT3 : -c->gas.gamma * c->CT3;
     return k;
 }
 
@@ -336,6 +326,7 @@ static MarchParams make_march(const sts_ctx* c, const Params& k)
     m.A_dy = c->A * dy; m.A_dx = c->A * dx;
     m.B43_dydx = 4.0 / 3.0 * m.B_dydx; m.B43_dxdy = 4.0 / 3.0 * m.B_dxdy;
     m.q_dx = 0.25 / dx; m.q_dy = 0.25 / dy;
+    m.h_dx = 0.5 / dx; m.h_dy = 0.5 / dy; m.inv_dt = 1.0 / dt;
     return m;
 }
 
@@ -617,7 +608,7 @@ static sts_status plan_host(const sts_grid* grid, const sts_square* squares, int
     if (std::fabs(fx - nx) > 1e-9 || std::fabs(fy - ny) > 1e-9 || nx < 1 || ny < 1)
         return fail(nullptr, STS_E_CONFIG, "channel lengths are not multiples of the spacing");
     if (!(gas->Kn > 0)) return fail(nullptr, STS_E_CONFIG, "Kn must be > 0");
-    if (!(gas->pw_sign == 1.0 || gas->pw_sign == -1.0)) return fail(nullptr, STS_E_CONFIG, "pw_sign must be +1 or -1");
+    if (gas->pw_form < PW_DPDT || gas->pw_form > PW_GAMMA) return fail(nullptr, STS_E_CONFIG, "bad pw_form");
     if (gas->xbc != STS_X_INFLOW_OUTFLOW && gas->xbc != STS_X_PERIODIC) return fail(nullptr, STS_E_ARG, "bad xbc");
     if (!(gas->p_in > 0) || !(gas->T_in > 0)) return fail(nullptr, STS_E_CONFIG, "inflow state must be positive");
     if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, STS_E_ARG, "bad rank/world");
@@ -749,15 +740,11 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
         ALLOC(ctx->halo, ctx->halo_elems);
     }
 #undef ALLOC
-    if (cudaMalloc(&ctx->ck, nce) != cudaSuccess || cudaMalloc(&ctx->uk, nce) != cudaSuccess || cudaMalloc(&ctx->vk, nve) != cudaSuccess ||
-        cudaMalloc(&ctx->red, (size_t)scheme->max_passes * 9 * sizeof(unsigned long long)) != cudaSuccess ||
+    if (cudaMalloc(&ctx->red, (size_t)scheme->max_passes * 9 * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMallocHost(&ctx->h_red, 9 * sizeof(unsigned long long)) != cudaSuccess) {
         sts_destroy(ctx);
         return fail(nullptr, STS_E_OOM, "device allocation failed");
     }
-    cudaMemcpy(ctx->ck, ctx->h_ck.data(), nce, cudaMemcpyHostToDevice);
-    cudaMemcpy(ctx->uk, ctx->h_uk.data(), nce, cudaMemcpyHostToDevice);
-    cudaMemcpy(ctx->vk, ctx->h_vk.data(), nve, cudaMemcpyHostToDevice);
     {
         std::vector<uint32_t> packed(nve);
         for (size_t e = 0; e < nve; e++) {
@@ -788,10 +775,6 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
         cudaMemcpy(ctx->kind32, packed.data(), nve * sizeof(uint32_t), cudaMemcpyHostToDevice);
         choose_segments(ctx, packed);
     }
-    {
-        const char* kv = getenv("STS_KERNEL");
-        ctx->use_tile = kv && std::string(kv) == "tile";
-    }
     if (world > 1 && !dist->nccl_id) {
         ctx->local_group = true;            // slabs of one process, driven by sts_advance_group
     } else if (world > 1 || (dist && dist->nccl_id && gas->xbc == STS_X_PERIODIC)) {
@@ -816,7 +799,7 @@ extern "C" void sts_destroy(sts_ctx* ctx)
     cudaDeviceSynchronize();
     for (int k = 0; k < 3; k++) { cudaFree(ctx->snap[k].u); cudaFree(ctx->snap[k].v); cudaFree(ctx->snap[k].p); cudaFree(ctx->snap[k].T); }
     cudaFree(ctx->ue); cudaFree(ctx->ve); cudaFree(ctx->Te); cudaFree(ctx->stage); cudaFree(ctx->halo);
-    cudaFree(ctx->ck); cudaFree(ctx->uk); cudaFree(ctx->vk); cudaFree(ctx->kind32); cudaFree(ctx->cta_order); cudaFree(ctx->cta_split); cudaFree(ctx->red);
+    cudaFree(ctx->kind32); cudaFree(ctx->cta_order); cudaFree(ctx->cta_split); cudaFree(ctx->red);
     if (ctx->h_red) cudaFreeHost(ctx->h_red);
     for (cudaGraphExec_t& g : ctx->tol_exec) if (g) cudaGraphExecDestroy(g);
     cudaFree(ctx->red2); cudaFree(ctx->d_ls);
@@ -1150,7 +1133,7 @@ __global__ void loop_check_kernel(unsigned long long* slot, LoopState* ls, cudaG
 
 static bool tol_graph_ok(const sts_ctx* c)
 {
-    return c->sch.tol > 0 && c->world == 1 && !c->comm && !c->use_tile && !c->profiling && !getenv("STS_NO_GRAPH");
+    return c->sch.tol > 0 && c->world == 1 && !c->comm && !c->profiling && !getenv("STS_NO_GRAPH");
 }
 
 #define CG(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
@@ -1272,9 +1255,8 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
     CU(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
     const int impl = ctx->sch.time == STS_IMPLICIT, tvd = ctx->sch.space == STS_TVD_VANLEER;
-    pass_fn pass = pass_table(impl, tvd);
     // test hook: the graph instances (early exit on a zero `done` flag) launched from the stream
-    const bool gk = getenv("STS_GRAPH_KERNEL") != nullptr && !ctx->use_tile;
+    const bool gk = getenv("STS_GRAPH_KERNEL") != nullptr;
     march_fn march = gk ? march_graph_table(impl, tvd) : march_table(impl, tvd);
     if (gk && !ctx->red2) {
         CU(cudaMalloc(&ctx->red2, 18 * sizeof(unsigned long long)));
@@ -1282,7 +1264,6 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
         CU(cudaMallocHost(&ctx->h_ls, sizeof(LoopState)));
         CU(cudaMemset(ctx->d_ls, 0, sizeof(LoopState)));
     }
-    const size_t smem = sizeof(Smem);
     const bool tolmode = ctx->sch.tol > 0;
     sts_status status = STS_OK;
     int last_it = -1;
@@ -1319,13 +1300,8 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 Params k = base(c, r);
                 k.ue_w = c->ue; k.ve_w = c->ve; k.Te_w = c->Te;
                 prof_begin(c, 1);
-                if (c->use_tile) {
-                    const dim3 grid((c->nloc + TX - 1) / TX, (c->ny + TY - 1) / TY);
-                    conv_table(tvd)<<<grid, NT, smem, st>>>(k);
-                } else {
-                    const dim3 mgrid(c->march_nstrips * c->march_nseg);
-                    conv_march_table(tvd)<<<mgrid, MX, sizeof(ConvSmem), st>>>(make_march(c, k));
-                }
+                const dim3 mgrid(c->march_nstrips * c->march_nseg);
+                conv_march_table(tvd)<<<mgrid, MX, sizeof(ConvSmem), st>>>(make_march(c, k));
                 prof_end(c);
                 c->launches++;
                 CU(cudaGetLastError());
@@ -1342,7 +1318,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
         // pass stream and need only pass p-1 (edge + interior), never the halo, so
         // the exchange of pass p overlaps the interior of pass p+1.  In-process
         // slab groups launch the same two CTA sets one after the other.
-        const bool split = !ctx->use_tile && (ctx->world > 1 || ctx->comm) && ctx->n_edge > 0 &&
+        const bool split = (ctx->world > 1 || ctx->comm) && ctx->n_edge > 0 &&
                            ctx->n_edge < ctx->n_split && !getenv("STS_NO_SPLIT");
         const bool overlap = split && n == 1 && ctx->comm;
         if (overlap) {
@@ -1363,13 +1339,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 k.u_o = c->snap[old[r]].u; k.v_o = c->snap[old[r]].v; k.p_o = c->snap[old[r]].p; k.T_o = c->snap[old[r]].T;
                 k.u_w = c->snap[nw[r]].u; k.v_w = c->snap[nw[r]].v; k.p_w = c->snap[nw[r]].p; k.T_w = c->snap[nw[r]].T;
                 k.red = c->red + (size_t)it * 9;
-                if (c->use_tile) {
-                    prof_begin(c, 0);
-                    const dim3 grid((c->nloc + TX - 1) / TX, (c->ny + TY - 1) / TY);
-                    pass<<<grid, NT, smem, st>>>(k);
-                    prof_end(c);
-                    c->launches++;
-                } else if (split) {
+                if (split) {
                     MarchParams ma = make_march(c, k), mb = ma;
                     ma.order = c->cta_split;
                     ma.seg = c->edge_seg;

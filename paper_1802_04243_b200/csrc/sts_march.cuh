@@ -32,7 +32,7 @@
 
 #include <type_traits>
 
-#include "sts_kernels.cuh"
+#include "sts_common.cuh"
 
 namespace sts {
 
@@ -55,6 +55,7 @@ struct MarchParams {
     double inv_dx, inv_dy, CT1_dydx, CT1_dxdy, B_dydx, B_dxdy, c_t, dV, A_dy, A_dx, half_dV;
     double B43_dydx, B43_dxdy;   // 4/3 B dy/dx, 4/3 B dx/dy (normal viscous links)
     double q_dx, q_dy;           // 1/(4 dx), 1/(4 dy) (bilinear differences in S^T_c)
+    double h_dx, h_dy, inv_dt;   // 1/(2 dx), 1/(2 dy), 1/dt (pressure work, R9)
     const int* done;             // graph-driven loop 2 (tolerance mode): loop finished -> the pass is a no-op
 };
 
@@ -246,7 +247,7 @@ struct StepVars {
 };
 struct NM1 {                      // n-1 state / explicit planes at this thread's points
     double p1n, T1n;              // row j+1
-    double T1c, u1c, v1n;         // T^{n-1}(i, j), u^{n-1}(i, j), v^{n-1}(i, j+1)
+    double p1c, T1c, u1c, v1n;    // p^{n-1}(i, j), T^{n-1}(i, j), u^{n-1}(i, j), v^{n-1}(i, j+1)
     double Tec, uec, ven;         // T^exp(i, j), u^exp(i, j), v^exp(i, j+1)
 };
 
@@ -483,16 +484,56 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         }
         const double a0 = IMPL ? dt * (a1 + a2 + a3 + a4 + FE - FW + FNl - FSl) + rP * m.dV
                                : dt * (a1 + a2 + a3 + a4) + rP * m.dV;
-        // S^T_c, Eq. pl29 (R4 bilinear = 4-point mean; R9 sign)
+        // S^T_c, Eq. pl29 (R4 bilinear = 4-point mean); a mid-face velocity on a
+        // wall face is the slip velocity of Eq. pl38 (R38)
         const double dudx = (R0.U[lc + 1] - R0.U[lc]) * m.inv_dx;
         const double dvdy = (Ra.V[lc] - R0.V[lc]) * m.inv_dy;
-        // dv/dx + du/dy from the bilinear face values (R4): v_E - v_W and u_N - u_S
-        // as one difference each (the shared corner values cancel)
-        const double shear = ((R0.V[lc + 1] + Ra.V[lc + 1]) - (R0.V[lc - 1] + Ra.V[lc - 1])) * m.q_dx
-                           + ((Ra.U[lc] + Ra.U[lc + 1]) - (Rm.U[lc] + Rm.U[lc + 1])) * m.q_dy;
+        double shear;
+        if (REG) {
+            // dv/dx + du/dy from the bilinear face values (R4): v_E - v_W and u_N - u_S
+            // as one difference each (the shared corner values cancel)
+            shear = ((R0.V[lc + 1] + Ra.V[lc + 1]) - (R0.V[lc - 1] + Ra.V[lc - 1])) * m.q_dx
+                  + ((Ra.U[lc] + Ra.U[lc + 1]) - (Rm.U[lc] + Rm.U[lc + 1])) * m.q_dy;
+        } else {
+            const double zeta = 1.1466 * k.Kn * rcp(rP);
+            auto slip = [&](double vP, double vw, double dn) { return (dn * vw + zeta * vP) * rcp(dn + zeta); };
+            const double vs = R0.V[lc] + Ra.V[lc], us = R0.U[lc] + R0.U[lc + 1];
+            const uint8_t kE = ckind(R0.KK[lc + 1]), kW = ckind(R0.KK[lc - 1]);
+            const uint8_t kN = ckind(kw1), kS = ckind(Rm.KK[lc]);
+            const double vE = wallish(kE) ? slip(0.5 * vs, 0.0, 0.5 * dx) : 0.25 * (vs + (R0.V[lc + 1] + Ra.V[lc + 1]));
+            const double vW = wallish(kW) ? slip(0.5 * vs, 0.0, 0.5 * dx) : 0.25 * ((R0.V[lc - 1] + Ra.V[lc - 1]) + vs);
+            const double uN = wallish(kN) ? slip(0.5 * us, kN == CK_WALLY ? k.u_wt : 0.0, 0.5 * dy)
+                                          : 0.25 * (us + (Ra.U[lc] + Ra.U[lc + 1]));
+            const double uS = wallish(kS) ? slip(0.5 * us, kS == CK_WALLY ? k.u_wb : 0.0, 0.5 * dy)
+                                          : 0.25 * ((Rm.U[lc] + Rm.U[lc + 1]) + us);
+            shear = (vE - vW) * m.inv_dx + (uN - uS) * m.inv_dy;
+        }
         const double div = dudx + dvdy;
+        // pressure work (R9): C^T3 Dp/Dt of Eq. pl6 at the old iterate --
+        // (p - p^{n-1}) / dt + ubar dp/dx + vbar dp/dy with face pressures p_f =
+        // mean of the two cells, = p of the cell at a wall -- or kappa p div(u)
+        double pwork;
+        const double pc = R0.P[lc];
+        if (k.pw_form == PW_DPDT) {
+            double dpx, dpy;
+            if (REG) {
+                dpx = (R0.P[lc + 1] - R0.P[lc - 1]) * m.h_dx;
+                dpy = (Ra.P[lc] - Rm.P[lc]) * m.h_dy;
+            } else {
+                const double pe = wallish(ckind(R0.KK[lc + 1])) ? pc : 0.5 * (pc + R0.P[lc + 1]);
+                const double pw = wallish(ckind(R0.KK[lc - 1])) ? pc : 0.5 * (R0.P[lc - 1] + pc);
+                const double pn = wallish(ckind(kw1)) ? pc : 0.5 * (pc + Ra.P[lc]);
+                const double ps = wallish(ckind(Rm.KK[lc])) ? pc : 0.5 * (Rm.P[lc] + pc);
+                dpx = (pe - pw) * m.inv_dx;
+                dpy = (pn - ps) * m.inv_dy;
+            }
+            const double ub = 0.5 * (R0.U[lc] + R0.U[lc + 1]), vb = 0.5 * (R0.V[lc] + Ra.V[lc]);
+            pwork = k.CT3 * ((pc - nm.p1c) * m.inv_dt + ub * dpx + vb * dpy);
+        } else {
+            pwork = k.pwk * pc * div;
+        }
         const double Sc = (k.CT2 * gP * (2.0 * (dudx * dudx + dvdy * dvdy) + shear * shear - 2.0 / 3.0 * div * div)
-                           + k.pw_sign * k.CT3 * R0.P[lc] * div) * m.dV;
+                           + pwork) * m.dV;
         const double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + Sc + nm.Tec) + s.R1[lc] * nm.T1c * m.dV;
         v.TN = rhs * rcp(a0);
     }
@@ -758,7 +799,7 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     NM1 nm;
     nm.Tec = nm.uec = nm.ven = 0.0;
     auto nm_prefetch_init = [&]() {
-        nm.p1n = ld(k.p_1, js + 1); nm.T1n = ld(k.T_1, js + 1);
+        nm.p1n = ld(k.p_1, js + 1); nm.T1n = ld(k.T_1, js + 1); nm.p1c = ld(k.p_1, js);
         nm.T1c = ld(k.T_1, js); nm.u1c = ld(k.u_1, js); nm.v1n = ldv(k.v_1, js + 1);
         if (!IMPL) { nm.Tec = ld(k.Te, js); nm.uec = ld(k.ue, js); nm.ven = ldv(k.ve, js + 1); }
     };

@@ -50,7 +50,8 @@ class sts_gas(ctypes.Structure):
                 ("p_in", ctypes.c_double), ("T_in", ctypes.c_double),
                 ("u_wall_bottom", ctypes.c_double), ("u_wall_top", ctypes.c_double),
                 ("T_wall", ctypes.c_double), ("T_square", ctypes.c_double),
-                ("g_x", ctypes.c_double), ("g_y", ctypes.c_double), ("pw_sign", ctypes.c_double),
+                ("g_x", ctypes.c_double), ("g_y", ctypes.c_double),
+                ("pw_form", ctypes.c_int32), ("reserved0", ctypes.c_int32),
                 ("particle_frame", ctypes.c_int32), ("xbc", ctypes.c_int32)]
 
 
@@ -151,7 +152,7 @@ def _structs(case: dict):
     gas = sts_gas(case["Kn"], case["mach"], case["gamma"], case.get("p_in", 1.0), case.get("T_in", 1.0),
                   case.get("u_wall_bottom", 0.0), case.get("u_wall_top", 0.0),
                   case.get("T_wall", 1.0), case.get("T_square", 1.0),
-                  case.get("g_x", 0.0), case.get("g_y", 0.0), float(case["pw_sign"]),
+                  case.get("g_x", 0.0), case.get("g_y", 0.0), int(case.get("pw_form", 0)), 0,
                   int(case.get("particle_frame", 0)), int(case.get("xbc", 0)))
     return grid, arr, len(sq), gas
 
@@ -191,21 +192,13 @@ class Solver:
                  nccl_id: bytes | None = None, stream: int | None = None):
         L = lib()
         self.case = dict(case)
-        sp = float(case["spacing"])
-        grid = sts_grid(case["nx"] * sp, case["ny"] * sp, sp)
-        sq = list(case.get("squares", []))
-        arr = (sts_square * max(1, len(sq)))(*[sts_square(*map(int, s)) for s in sq])
-        gas = sts_gas(case["Kn"], case["mach"], case["gamma"], case.get("p_in", 1.0), case.get("T_in", 1.0),
-                      case.get("u_wall_bottom", 0.0), case.get("u_wall_top", 0.0),
-                      case.get("T_wall", 1.0), case.get("T_square", 1.0),
-                      case.get("g_x", 0.0), case.get("g_y", 0.0), float(case["pw_sign"]),
-                      int(case.get("particle_frame", 0)), int(case.get("xbc", 0)))
+        grid, arr, nsq, gas = _structs(case)
         sch = sts_scheme(int(case["time"]), int(case["space"]), float(case["dt"]),
                          int(case.get("min_passes", 1)), int(case["max_passes"]), float(case.get("tol", 0.0)))
         self._idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         dist = sts_dist(rank, world, device, ctypes.cast(self._idbuf, ctypes.c_void_p) if self._idbuf else None)
         h = ctypes.c_void_p()
-        _check(L.sts_create(ctypes.byref(grid), arr, len(sq), ctypes.byref(gas), ctypes.byref(sch),
+        _check(L.sts_create(ctypes.byref(grid), arr, nsq, ctypes.byref(gas), ctypes.byref(sch),
                             ctypes.byref(dist), ctypes.byref(h)))
         self._h = h
         self.nx, self.ny = int(case["nx"]), int(case["ny"])

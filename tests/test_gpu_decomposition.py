@@ -157,25 +157,6 @@ def test_segments_bitwise(S, seg, variant):
 
 
 @pytest.mark.parametrize("variant", list(W.VARIANTS))
-def test_tile_kernel_agrees(S, oracle_mod, variant):
-    """The v1 2-D tile kernels (STS_KERNEL=tile: pass_kernel, conv_kernel) and the
-    y-march kernels (march_kernel, conv_march_kernel) agree to the parity tolerance
-    (different reciprocal arithmetic, same discrete spec)."""
-    case = W.c1(variant, passes=10)
-    a = S.Solver(case)
-    os.environ["STS_KERNEL"] = "tile"
-    try:
-        b = S.Solver(case)
-    finally:
-        del os.environ["STS_KERNEL"]
-    a.advance(10)
-    b.advance(10)
-    for f in FIELDS:
-        x, y = a.get_field(f), b.get_field(f)
-        assert np.abs(x - y).max() <= 1e-10 * max(1.0, np.abs(y).max()), f
-
-
-@pytest.mark.parametrize("variant", list(W.VARIANTS))
 def test_allreg_loop_bitwise(S, variant):
     """CTAs whose every point is regular run the regular-only copy of the row
     loop (launch-order bit 30) and skip the kind rows; forcing every CTA onto the

@@ -38,11 +38,12 @@ def _run_compare(S, oracle_mod, case, steps, seed=0, vscale=0.05, tol=TOL, extra
 
 
 @pytest.mark.parametrize("variant", list(W.VARIANTS))
-@pytest.mark.parametrize("pw", [-1.0, 1.0])
+@pytest.mark.parametrize("pw", [W.PW_DPDT, W.PW_PRINTED, W.PW_GAMMA])
 def test_parity_small_square(S, oracle_mod, variant, pw):
-    """48x16 channel, one square, 3 steps x 3 passes, both pressure-work signs (R9)."""
+    """48x16 channel, one square, 3 steps x 3 passes, the pressure-work forms (R9):
+    C^T3 Dp/Dt (default) and two of the kappa p div(u) forms."""
     case = W.c1_small(variant, passes=3)
-    case["pw_sign"] = pw
+    case["pw_form"] = pw
     extra = ("uexp", "vexp", "Texp") if variant.startswith("explicit") else ()
     _run_compare(S, oracle_mod, case, 3, seed=1, extra=extra)
 
