@@ -94,13 +94,20 @@ struct sts_ctx {
     double *ue = nullptr, *ve = nullptr, *Te = nullptr;
     uint32_t* kind32 = nullptr;            // packed ck | uk << 8 | vk << 16, (ny+1) x pitch
     std::vector<uint8_t> h_ck, h_uk, h_vk; // host copies of the local kind maps
-    std::vector<uint8_t> h_solid;          // global solid map (nx x ny), for set_field
+    std::vector<uint8_t> h_solid;          // slab-local solid map, ny x sol_w (unwrapped columns from sol_lo)
+    int sol_lo = 0, sol_w = 0;
     int march_seg = 0, march_nseg = 0, march_nstrips = 0;
-    int* cta_order = nullptr;              // launch order of the march CTAs (longest first)
-    int* cta_split = nullptr;              // the same CTAs, edge strips (0, last) first, then the interior
+    int* cta_order = nullptr;              // launch order of the march CTAs: general CTAs (longest
+                                           // first), then the all-regular ones
+    int n_gen = 0, n_reg = 0;              // CTAs of the general / all-regular march kernel
+    int* cta_split = nullptr;              // multi-GPU split: edge strips first (general kernel),
+                                           // then the interior general and all-regular CTAs
     int n_edge = 0;                        // CTAs in the edge strips
     int edge_seg = 0;                      // their (shorter) segment height
     int n_split = 0;                       // entries of cta_split
+    int n_split_gen = 0;                   // interior general CTAs of cta_split
+    cudaStream_t gstream = nullptr;        // the general CTAs of a pass run here, beside the regular ones
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // halo overlap (multi-GPU): edge strips + pack/NCCL/unpack on a high-priority
     // stream while the interior strips of the next pass run on the pass stream
     cudaStream_t hstream = nullptr;
@@ -113,7 +120,7 @@ struct sts_ctx {
     struct LoopState* d_ls = nullptr;      // device loop state
     struct LoopState* h_ls = nullptr;      // pinned copy
     unsigned long long* h_red = nullptr;   // pinned, 9 entries
-    double* stage = nullptr;               // device staging (global-shape field)
+    double* stage = nullptr;               // device scratch of the owned slab (rho read-back)
     size_t stage_elems = 0;
     double* halo = nullptr;                // send/recv buffers (multi-GPU)
     size_t halo_elems = 0;
@@ -150,14 +157,21 @@ static inline size_t v_elems(const sts_ctx* c) { return (size_t)c->pitch * (c->n
 static inline bool is_periodic(const sts_ctx* c) { return c->gas.xbc == STS_X_PERIODIC; }
 
 // Host kind maps for the stored local columns [gi0-OFF, gi0-OFF+pitch) (DESIGN 3.5).
+// The solid map is slab-local: unwrapped global columns [sol_lo, sol_lo + sol_w)
+// = the stored columns plus SOL_M on each side (the +-3 window of the regular
+// bit and the face kinds reach them), so host memory grows with the slab, not
+// with the channel.
+constexpr int SOL_M = 4;
 static bool solid_global(const sts_ctx* c, int gi, int gj, const std::vector<uint8_t>& solid)
 {
-    return solid[(size_t)gj * c->nx + gi] != 0;
+    const int u = gi - c->sol_lo;
+    if (u < 0 || u >= c->sol_w) return false;            // never reached for stored columns +- SOL_M
+    return solid[(size_t)gj * c->sol_w + u] != 0;
 }
 static uint8_t cell_kind_g(const sts_ctx* c, int gi, int gj, const std::vector<uint8_t>& solid)
 {
     if (gj < 0 || gj >= c->ny) return CK_WALLY;
-    if (is_periodic(c)) { gi = ((gi % c->nx) + c->nx) % c->nx; }
+    if (is_periodic(c)) { /* the slab-local map holds the wrapped columns unwrapped */ }
     else if (gi < 0) return CK_INLET;
     else if (gi >= c->nx) return CK_OUTLET;
     return solid_global(c, gi, gj, solid) ? CK_SOLID : CK_FLUID;
@@ -180,65 +194,74 @@ static uint8_t v_kind_g(const sts_ctx* c, int gi, int gj, const std::vector<uint
     return (cell_kind_g(c, gi, gj - 1, solid) == CK_FLUID && cell_kind_g(c, gi, gj, solid) == CK_FLUID) ? FK_ACTIVE : FK_FIXED0;
 }
 
-// ------------------------------------------------------------- pack / unpack
-// Global-shape field (device) <-> local padded slab with ghost columns
-// (inlet state, outlet copy, periodic wrap; DESIGN 3.5 items 2-4).
-struct PackArgs {
-    int nx, ny, gi0, pitch, xbc, field;   // field: 0 u, 1 v, 2 p, 3 T
-    double inlet_val;                      // u_in / 0 / p_in / T_in
+// ------------------------------------------------------------- field I/O
+// Fields move between caller buffers (host or device, global or slab shape)
+// and the stored local columns by strided 2-D copies (cudaMemcpy2DAsync, the
+// direction inferred from the pointers); finish_kernel then applies the ghost
+// rules of DESIGN 3.5 items 2-4 and re-imposes the fixed faces of item 1 from
+// the packed kind map, in the local layout.
+struct FinishArgs {
+    int nx, ny, gi0, nloc, pitch, xbc, field, single;   // field: 0 u, 1 v, 2 p, 3 T; single: one rank
+    int fill_left, fill_right;                         // ghost columns filled here (not by a halo exchange)
+    double inlet_val, u_in;
 };
-__global__ void pack_kernel(PackArgs a, const double* __restrict__ g, double* __restrict__ l)
+__global__ void finish_kernel(FinishArgs a, const uint32_t* __restrict__ kind, double* d)
 {
     const int rows = a.field == 1 ? a.ny + 1 : a.ny;
-    const int gw = a.field == 0 ? a.nx + 1 : a.nx;         // global row width
-    long long n = (long long)rows * a.pitch;
+    const long long n = (long long)rows * a.pitch;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-        int j = (int)(e / a.pitch), li = (int)(e - (long long)j * a.pitch);
-        int gi = a.gi0 - OFF + li;
-        double val;
-        if (a.xbc == 1) {
-            int w = ((gi % a.nx) + a.nx) % a.nx;
-            val = g[(long long)j * gw + w];
-        } else if (gi < 0) {
-            val = a.inlet_val;
-        } else if (a.field == 0) {
-            val = gi <= a.nx ? g[(long long)j * gw + gi] : a.inlet_val;
-        } else {
-            val = g[(long long)j * gw + (gi < a.nx ? gi : a.nx - 1)];
+        const int j = (int)(e / a.pitch), li = (int)(e - (long long)j * a.pitch);
+        const int gi = a.gi0 - OFF + li;
+        const long long rowb = (long long)j * a.pitch;
+        const bool left = li < OFF, right = li >= OFF + a.nloc + (a.field == 0 && !a.xbc && a.gi0 + a.nloc == a.nx ? 1 : 0);
+        if ((left && a.fill_left) || (right && a.fill_right)) {
+            double val;
+            if (a.xbc == 1) {                            // one periodic rank: wrap to an owned column
+                const int w = ((gi % a.nx) + a.nx) % a.nx;
+                val = d[rowb + (w - a.gi0 + OFF)];
+            } else if (gi < 0) {
+                val = a.inlet_val;                         // inflow state (BC spec 2)
+            } else if (a.field == 0) {
+                val = a.inlet_val;                         // u beyond the outlet face: never read
+            } else {
+                val = d[rowb + (a.nx - 1 - a.gi0 + OFF)];  // zero-gradient outlet (BC spec 3)
+            }
+            d[e] = val;
         }
-        l[e] = val;
+        if (a.field <= 1) {                              // fixed faces (BC spec 1-2)
+            const uint32_t w = kind[e];
+            const uint8_t fk = (uint8_t)((w >> (a.field == 0 ? 8 : 16)) & 0xff);
+            if (fk == FK_FIXED0 || fk == FK_WALL) d[e] = 0.0;
+            else if (fk == FK_INLET) d[e] = a.u_in;
+        }
     }
 }
-__global__ void unpack_kernel(int ny_rows, int ncols, int col0_local, int pitch, int gw, int gcol0,
-                              const double* __restrict__ l, double* __restrict__ g)
-{
-    long long n = (long long)ny_rows * ncols;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-        int j = (int)(e / ncols), i = (int)(e - (long long)j * ncols);
-        g[(long long)j * gw + gcol0 + i] = l[(long long)j * pitch + col0_local + i];
-    }
-}
-// rho = p / T for the read-back of STS_RHO (Eq. pl5)
-// Owned slab (rows x ncols, row-major) -> local columns [OFF, OFF+ncols) of up to
-// three snapshot arrays; optionally replicate local column `rep_src` into the
-// outlet ghost columns (rep_src+1 .. rep_src+OFF-1) (BC spec 3).
-__global__ void slab_pack_kernel(int rows, int ncols, int pitch, const double* __restrict__ src, double* d0,
-                                 double* d1, double* d2, int rep_src)
+// rho = p / T of the owned columns into a compact (rows x ncols) buffer (Eq. pl5)
+__global__ void ratio_kernel(int rows, int ncols, int pitch, const double* __restrict__ p, const double* __restrict__ T,
+                             double* __restrict__ r)
 {
     const long long n = (long long)rows * ncols;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
         const int j = (int)(e / ncols), i = (int)(e - (long long)j * ncols);
-        const double val = src[e];
         const long long id = (long long)j * pitch + OFF + i;
-        d0[id] = val; d1[id] = val; d2[id] = val;
-        if (rep_src >= 0 && OFF + i == rep_src)
-            for (int g = 1; g < OFF; g++) { d0[id + g] = val; d1[id + g] = val; d2[id + g] = val; }
+        r[e] = p[id] / T[id];
     }
 }
-__global__ void ratio_kernel(long long n, const double* __restrict__ p, const double* __restrict__ T, double* __restrict__ r)
+// Free stream (BC spec 1-2, R12) in the local layout of all three snapshots.
+__global__ void freestream_kernel(long long n_cells, long long n_v, const uint32_t* __restrict__ kind, double u_in,
+                                  double p_in, double T_in, double* u0, double* u1, double* u2, double* v0, double* v1,
+                                  double* v2, double* p0, double* p1, double* p2, double* T0, double* T1, double* T2)
 {
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
-        r[e] = p[e] / T[e];
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n_v; e += (long long)gridDim.x * blockDim.x) {
+        v0[e] = 0.0; v1[e] = 0.0; v2[e] = 0.0;
+        if (e < n_cells) {
+            const uint8_t fk = (uint8_t)((kind[e] >> 8) & 0xff);
+            const double uv = fk == FK_FIXED0 ? 0.0 : u_in;
+            u0[e] = uv; u1[e] = uv; u2[e] = uv;
+            p0[e] = p_in; p1[e] = p_in; p2[e] = p_in;
+            T0[e] = T_in; T1[e] = T_in; T2[e] = T_in;
+        }
+    }
 }
 // Halo strips for the multi-GPU exchange: columns [c0, c0+OFF) of u, v, p, T.
 __global__ void halo_pack_kernel(int ny, int pitch, int c0, const double* u, const double* v, const double* p,
@@ -266,13 +289,22 @@ __global__ void halo_unpack_kernel(int ny, int pitch, int c0, double* u, double*
 
 // ------------------------------------------------------------- kernel table
 typedef void (*march_fn)(MarchParams);
-static march_fn march_table(int impl, int tvd)
+// regk: the all-regular kernel (sts_march.cuh)
+static march_fn march_table(int impl, int tvd, int regk)
 {
+    if (regk) {
+        if (impl) return tvd ? march_kernel<true, true, false, true> : march_kernel<true, false, false, true>;
+        return tvd ? march_kernel<false, true, false, true> : march_kernel<false, false, false, true>;
+    }
     if (impl) return tvd ? march_kernel<true, true> : march_kernel<true, false>;
     return tvd ? march_kernel<false, true> : march_kernel<false, false>;
 }
-static march_fn march_graph_table(int impl, int tvd)
+static march_fn march_graph_table(int impl, int tvd, int regk)
 {
+    if (regk) {
+        if (impl) return tvd ? march_kernel<true, true, true, true> : march_kernel<true, false, true, true>;
+        return tvd ? march_kernel<false, true, true, true> : march_kernel<false, false, true, true>;
+    }
     if (impl) return tvd ? march_kernel<true, true, true> : march_kernel<true, false, true>;
     return tvd ? march_kernel<false, true, true> : march_kernel<false, false, true>;
 }
@@ -282,10 +314,11 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
 {
     static bool done = false;
     if (done) return STS_OK;
-    march_fn mfs[8] = {march_table(0, 0), march_table(0, 1), march_table(1, 0), march_table(1, 1),
-                       march_graph_table(0, 0), march_graph_table(0, 1), march_graph_table(1, 0), march_graph_table(1, 1)};
-    for (march_fn f : mfs)
+    for (int q = 0; q < 16; q++) {
+        const int impl = q & 1, tvd = (q >> 1) & 1, regk = (q >> 2) & 1, graph = q >> 3;
+        march_fn f = graph ? march_graph_table(impl, tvd, regk) : march_table(impl, tvd, regk);
         CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));
+    }
     for (int tvd = 0; tvd < 2; tvd++)
         CU(cudaFuncSetAttribute((const void*)conv_march_table(tvd), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(ConvSmem)));
@@ -306,7 +339,8 @@ static Params make_params(const sts_ctx* c)
     k.g_x = c->gas.g_x; k.g_y = c->gas.g_y;
     // pressure-work form of S^T_c (reading R9) and kappa of the p div(u) forms
     k.pw_form = c->gas.pw_form;
-    k.pwk = c->gas.pw_form == PW_PRINTED ? c->CT3 : c->gas.pw_form == PW_NEG ? -c->CT3 : -c->gas.gamma * c->CT3;
+    k.pwk = c->gas.pw_form == PW_DPDT ? 0.0 : c->gas.pw_form == PW_PRINTED ? c->CT3
+          : c->gas.pw_form == PW_NEG ? -c->CT3 : -c->gas.gamma * c->CT3;
     return k;
 }
 
@@ -327,6 +361,7 @@ static MarchParams make_march(const sts_ctx* c, const Params& k)
     m.B43_dydx = 4.0 / 3.0 * m.B_dydx; m.B43_dxdy = 4.0 / 3.0 * m.B_dxdy;
     m.q_dx = 0.25 / dx; m.q_dy = 0.25 / dy;
     m.h_dx = 0.5 / dx; m.h_dy = 0.5 / dy; m.inv_dt = 1.0 / dt;
+    m.pw_a = c->gas.pw_form == PW_DPDT ? c->CT3 : 0.0;
     return m;
 }
 
@@ -344,7 +379,7 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     int dev_sms = 148, per_sm = 3;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
     int nb = 0;
-    const void* fn = (const void*)march_table(c->sch.time == STS_IMPLICIT, c->sch.space == STS_TVD_VANLEER);
+    const void* fn = (const void*)march_table(c->sch.time == STS_IMPLICIT, c->sch.space == STS_TVD_VANLEER, 0);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, MX, sizeof(MarchSmem)) == cudaSuccess && nb > 0)
         per_sm = nb;
     const int strips = (c->nloc + MW - 1) / MW;
@@ -434,14 +469,16 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
             }
         return true;
     };
-    std::vector<int> order(ctas.size());
-    int n_allreg = 0;
+    // general CTAs first (longest first), then the all-regular ones: two kernels
+    std::vector<int> order, order_reg;
     for (size_t q = 0; q < ctas.size(); q++) {
         const bool ar = allreg(ctas[q].second, best_seg);
-        n_allreg += ar;
-        order[q] = ctas[q].second | (ar ? ALLREG_BIT : 0);
+        (ar ? order_reg : order).push_back(ctas[q].second | (ar ? ALLREG_BIT : 0));
     }
-    if (getenv("STS_VERBOSE")) fprintf(stderr, "sts: seg %d, %zu CTAs, %d all-regular\n", best_seg, ctas.size(), n_allreg);
+    c->n_gen = (int)order.size();
+    c->n_reg = (int)order_reg.size();
+    order.insert(order.end(), order_reg.begin(), order_reg.end());
+    if (getenv("STS_VERBOSE")) fprintf(stderr, "sts: seg %d, %zu CTAs, %d all-regular\n", best_seg, ctas.size(), c->n_reg);
     cudaFree(c->cta_order);
     c->cta_order = nullptr;
     cudaMalloc(&c->cta_order, order.size() * sizeof(int));
@@ -463,15 +500,48 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     std::stable_sort(ectas.begin(), ectas.end(), [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
         return a.first > b.first;
     });
-    std::vector<int> split;
+    std::vector<int> split, split_reg;
     for (auto& q : ectas) split.push_back(q.second | (allreg(q.second, c->edge_seg) ? ALLREG_BIT : 0));
     c->n_edge = (int)split.size();
-    for (int o : order) if (!edge((o & (ALLREG_BIT - 1)) % strips)) split.push_back(o);
+    for (int o : order) {
+        if (edge((o & (ALLREG_BIT - 1)) % strips)) continue;
+        ((o & ALLREG_BIT) ? split_reg : split).push_back(o);
+    }
+    c->n_split_gen = (int)split.size() - c->n_edge;
+    split.insert(split.end(), split_reg.begin(), split_reg.end());
     c->n_split = (int)split.size();
     cudaFree(c->cta_split);
     c->cta_split = nullptr;
     cudaMalloc(&c->cta_split, split.size() * sizeof(int));
     cudaMemcpy(c->cta_split, split.data(), split.size() * sizeof(int), cudaMemcpyHostToDevice);
+}
+
+
+// One loop-2 pass of the march kernels over `order`: the n_gen general CTAs on
+// the context's high-priority stream beside the n_reg all-regular CTAs on st
+// (fork / join by events; the same calls build the dependencies inside a graph
+// capture).  Returns the number of launches.
+static int launch_march(sts_ctx* c, const MarchParams& m, bool graph, cudaStream_t st, const int* order,
+                        int n_gen, int n_reg)
+{
+    const int impl = c->sch.time == STS_IMPLICIT, tvd = c->sch.space == STS_TVD_VANLEER;
+    march_fn gen = graph ? march_graph_table(impl, tvd, 0) : march_table(impl, tvd, 0);
+    march_fn reg = graph ? march_graph_table(impl, tvd, 1) : march_table(impl, tvd, 1);
+    MarchParams mg = m, mr = m;
+    mg.order = order;
+    mr.order = order + n_gen;
+    if (n_gen > 0 && n_reg > 0) {
+        cudaEventRecord(c->ev_fork, st);
+        cudaStreamWaitEvent(c->gstream, c->ev_fork, 0);
+        gen<<<n_gen, MX, sizeof(MarchSmem), c->gstream>>>(mg);
+        cudaEventRecord(c->ev_join, c->gstream);
+        reg<<<n_reg, MX, sizeof(MarchSmem), st>>>(mr);
+        cudaStreamWaitEvent(st, c->ev_join, 0);
+        return 2;
+    }
+    if (n_gen > 0) gen<<<n_gen, MX, sizeof(MarchSmem), st>>>(mg);
+    else if (n_reg > 0) reg<<<n_reg, MX, sizeof(MarchSmem), st>>>(mr);
+    return 1;
 }
 
 // ------------------------------------------------------------- profiling
@@ -596,7 +666,7 @@ extern "C" sts_status sts_nccl_unique_id(void* out128)
 }
 
 // Host-only planning, no CUDA call: geometry validation and snapping to
-// integer cells, the global solid map, the slab decomposition along x and the
+// integer cells, the slab decomposition along x, the slab-local solid map and the
 // local cell / u-face / v-face kind maps of this rank (DESIGN 3.5, 7).
 // Used by sts_create and by sts_plan (the CPU-testable decomposition).
 static sts_status plan_host(const sts_grid* grid, const sts_square* squares, int32_t n_squares, const sts_gas* gas,
@@ -612,20 +682,16 @@ static sts_status plan_host(const sts_grid* grid, const sts_square* squares, int
     if (gas->xbc != STS_X_INFLOW_OUTFLOW && gas->xbc != STS_X_PERIODIC) return fail(nullptr, STS_E_ARG, "bad xbc");
     if (!(gas->p_in > 0) || !(gas->T_in > 0)) return fail(nullptr, STS_E_CONFIG, "inflow state must be positive");
     if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, STS_E_ARG, "bad rank/world");
-    std::vector<uint8_t> solid((size_t)nx * ny, 0);
     for (int s = 0; s < n_squares; s++) {
         const sts_square& q = squares[s];
         if (q.ni < 1 || q.nj < 1 || q.i0 < 0 || q.j0 < 0 || q.i0 + q.ni > nx || q.j0 + q.nj > ny)
             return fail(nullptr, STS_E_CONFIG, "square outside the channel");
         if (gas->xbc == STS_X_INFLOW_OUTFLOW && (q.i0 < 1 || q.i0 + q.ni > nx - 1))
             return fail(nullptr, STS_E_CONFIG, "square must leave a fluid column at the inlet and outlet");
-        for (int j = q.j0; j < q.j0 + q.nj; j++)
-            for (int i = q.i0; i < q.i0 + q.ni; i++) solid[(size_t)j * nx + i] = 1;
     }
     ctx->nx = nx; ctx->ny = ny; ctx->spacing = grid->spacing;
     ctx->gas = *gas;
     ctx->squares.assign(squares, squares + n_squares);
-    ctx->h_solid = solid;
     ctx->rank = rank; ctx->world = world;
     // slab decomposition along x: near-equal, remainder to the low ranks
     ctx->col_start.resize(world + 1);
@@ -639,6 +705,23 @@ static sts_status plan_host(const sts_grid* grid, const sts_square* squares, int
     ctx->pitch = ((ctx->nloc + 2 * OFF + 1) + 15) / 16 * 16;
     if ((int64_t)ctx->pitch * (ny + 1) >= (int64_t)INT32_MAX)
         return fail(nullptr, STS_E_CONFIG, "slab too large for 32-bit element indices (use more ranks)");
+    // slab-local solid map: every square intersected with the covered columns
+    // (periodic: with the copies shifted by -nx, 0, +nx)
+    ctx->sol_lo = ctx->gi0 - OFF - SOL_M;
+    ctx->sol_w = ctx->pitch + 2 * SOL_M;
+    ctx->h_solid.assign((size_t)ctx->sol_w * ny, 0);
+    std::vector<uint8_t>& solid = ctx->h_solid;
+    for (int s = 0; s < n_squares; s++) {
+        const sts_square& q = squares[s];
+        const bool per = gas->xbc == STS_X_PERIODIC;
+        const int sh0 = per ? (int)std::floor((double)ctx->sol_lo / nx) - 1 : 0;
+        const int sh1 = per ? (ctx->sol_lo + ctx->sol_w) / nx + 1 : 0;
+        for (int sh = sh0; sh <= sh1; sh++) {
+            const int a = std::max(q.i0 + sh * nx, ctx->sol_lo), b = std::min(q.i0 + q.ni + sh * nx, ctx->sol_lo + ctx->sol_w);
+            for (int j = q.j0; j < q.j0 + q.nj; j++)
+                for (int i = a; i < b; i++) solid[(size_t)j * ctx->sol_w + (i - ctx->sol_lo)] = 1;
+        }
+    }
     // kind maps of the stored local columns [gi0-OFF, gi0-OFF+pitch)
     const size_t nce = (size_t)ctx->pitch * ny, nve = (size_t)ctx->pitch * (ny + 1);
     ctx->h_ck.assign(nce, CK_WALLY); ctx->h_uk.assign(nce, FK_NONE); ctx->h_vk.assign(nve, FK_NONE);
@@ -721,6 +804,16 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
 
     sts_status st = set_smem_attrs(ctx);
     if (st != STS_OK) { sts_destroy(ctx); return st; }
+    {
+        int lo = 0, hi = 0;
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
+            cudaStreamCreateWithPriority(&ctx->gstream, cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+            sts_destroy(ctx);
+            return fail(nullptr, STS_E_CUDA, "stream / event creation failed");
+        }
+    }
     size_t nce = cell_elems(ctx), nve = v_elems(ctx);
 
     auto alloc = [&](double** p, size_t n) -> sts_status {
@@ -733,7 +826,7 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
         ALLOC(ctx->snap[k].u, nce); ALLOC(ctx->snap[k].v, nve); ALLOC(ctx->snap[k].p, nce); ALLOC(ctx->snap[k].T, nce);
     }
     ALLOC(ctx->ue, nce); ALLOC(ctx->ve, nve); ALLOC(ctx->Te, nce);
-    ctx->stage_elems = (size_t)(nx + 1) * (ny + 1);
+    ctx->stage_elems = (size_t)ctx->nloc * ny;          // slab-shaped scratch (rho read-back)
     ALLOC(ctx->stage, ctx->stage_elems);
     if (world > 1 || (dist && dist->nccl_id && gas->xbc == STS_X_PERIODIC)) {
         ctx->halo_elems = (size_t)16 * OFF * (ny + 1);
@@ -807,6 +900,8 @@ extern "C" void sts_destroy(sts_ctx* ctx)
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : {ctx->ev_a[0], ctx->ev_a[1], ctx->ev_b, ctx->ev_s, ctx->ev_h}) if (e) cudaEventDestroy(e);
     if (ctx->hstream) cudaStreamDestroy(ctx->hstream);
+    if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
+    for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_join}) if (e) cudaEventDestroy(e);
     if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
     delete ctx;
 }
@@ -818,111 +913,118 @@ extern "C" sts_status sts_set_stream(sts_ctx* ctx, void* s)
     return STS_OK;
 }
 
-static size_t global_size(const sts_ctx* c, int field)
+
+static double* field_ptr(const Snapshot& s, int field)
 {
-    if (field == STS_U || field == STS_UEXP) return (size_t)(c->nx + 1) * c->ny;
-    if (field == STS_V || field == STS_VEXP) return (size_t)c->nx * (c->ny + 1);
-    return (size_t)c->nx * c->ny;
+    return field == STS_U ? s.u : field == STS_V ? s.v : field == STS_P ? s.p : s.T;
+}
+static double inlet_value(const sts_ctx* c, int field)
+{
+    return field == STS_U ? c->u_in : field == STS_V ? 0.0 : field == STS_P ? c->gas.p_in : c->gas.T_in;
+}
+// Owned-part shape of a field on this rank (sts_shape): the last rank also
+// returns u-face nx (the outlet face; periodic: the copy of face 0).
+static void owned_shape(const sts_ctx* c, int field, int* rows, int* ncols)
+{
+    const bool last = c->rank == c->world - 1;
+    *rows = (field == STS_V || field == STS_VEXP) ? c->ny + 1 : c->ny;
+    *ncols = c->nloc + ((field == STS_U || field == STS_UEXP) && last ? 1 : 0);
 }
 
-// Pack a global-shape device field into all three snapshots (solid cells and
-// fixed faces must agree in every snapshot: they are never rewritten).
-static sts_status pack_into_all(sts_ctx* ctx, int field, const double* gdev)
+// One field from a caller buffer (host or device; global shape, or this rank's
+// owned slab) into the current snapshot: strided 2-D copies of the stored
+// columns, ghost rules + fixed faces (finish_kernel), then device copies into
+// the other two snapshots (solid cells and fixed faces must agree in every
+// snapshot: they are never rewritten).  Slab-shaped input on a multi-rank
+// context ends with one halo exchange (every rank calls it, collectively).
+static sts_status set_field_any(sts_ctx* ctx, int field, const double* src, int64_t n)
 {
-    PackArgs a{ctx->nx, ctx->ny, ctx->gi0, ctx->pitch, ctx->gas.xbc, field,
-               field == 0 ? ctx->u_in : field == 1 ? 0.0 : field == 2 ? ctx->gas.p_in : ctx->gas.T_in};
-    for (int k = 0; k < 3; k++) {
-        double* dst = field == 0 ? ctx->snap[k].u : field == 1 ? ctx->snap[k].v : field == 2 ? ctx->snap[k].p : ctx->snap[k].T;
-        pack_kernel<<<592, 256, 0, ctx->stream>>>(a, gdev, dst);
-        ctx->launches++;
+    if (!ctx || !src) return fail(ctx, STS_E_ARG, "null argument");
+    if (field < STS_U || field > STS_T) return fail(ctx, STS_E_ARG, "field not settable");
+    CU(cudaSetDevice(ctx->device));
+    const int rows = field == STS_V ? ctx->ny + 1 : ctx->ny;
+    const int gw = field == STS_U ? ctx->nx + 1 : ctx->nx;
+    int orows, ncols;
+    owned_shape(ctx, field, &orows, &ncols);
+    const bool global = n == (int64_t)rows * gw;
+    const bool slab = !global && n == (int64_t)orows * ncols;
+    if (!global && !slab) return fail(ctx, STS_E_ARG, "wrong buffer size (neither global nor slab shape)");
+    if (slab && ctx->local_group) return fail(ctx, STS_E_ARG, "in-process slab groups take global-shape fields");
+    const bool per = is_periodic(ctx);
+    double* dst = field_ptr(ctx->snap[ctx->cur], field);
+    const size_t dp = (size_t)ctx->pitch * sizeof(double);
+    FinishArgs f{ctx->nx, ctx->ny, ctx->gi0, ctx->nloc, ctx->pitch, ctx->gas.xbc, field, ctx->world == 1 ? 1 : 0,
+                 0, 0, inlet_value(ctx, field), ctx->u_in};
+    if (global) {
+        // stored unwrapped columns [lo, lo + pitch), periodic: wrapped pieces
+        const int lo = ctx->gi0 - OFF, hi = lo + ctx->pitch;
+        if (per && ctx->world > 1) {
+            for (int u = lo; u < hi;) {
+                const int w = ((u % ctx->nx) + ctx->nx) % ctx->nx, len = std::min(hi - u, ctx->nx - w);
+                CU(cudaMemcpy2DAsync(dst + (u - lo), dp, src + w, (size_t)gw * sizeof(double), (size_t)len * sizeof(double),
+                                     rows, cudaMemcpyDefault, ctx->stream));
+                u += len;
+            }
+        } else {
+            const int a = std::max(lo, 0), b = std::min(hi, per ? ctx->nx : gw);
+            if (b > a)
+                CU(cudaMemcpy2DAsync(dst + (a - lo), dp, src + a, (size_t)gw * sizeof(double), (size_t)(b - a) * sizeof(double),
+                                     rows, cudaMemcpyDefault, ctx->stream));
+            f.fill_left = ctx->gi0 == 0 || per;
+            f.fill_right = ctx->gi0 + ctx->nloc == ctx->nx || per;
+        }
+        if (per && ctx->world == 1) { f.fill_left = 1; f.fill_right = 1; }
+    } else {
+        CU(cudaMemcpy2DAsync(dst + OFF, dp, src, (size_t)ncols * sizeof(double), (size_t)ncols * sizeof(double), orows,
+                             cudaMemcpyDefault, ctx->stream));
+        f.fill_left = !per && ctx->gi0 == 0;
+        f.fill_right = !per && ctx->gi0 + ctx->nloc == ctx->nx;
+        if (per && ctx->world == 1) { f.fill_left = 1; f.fill_right = 1; }
     }
+    finish_kernel<<<592, 256, 0, ctx->stream>>>(f, ctx->kind32, dst);
+    ctx->launches++;
     CU(cudaGetLastError());
-    return STS_OK;
-}
-
-// Host-side fixed faces of DESIGN 3.5 (inlet u_in, solid/wall faces 0) applied
-// to a global-shape host copy before packing.
-static void impose_fixed_host(const sts_ctx* c, int field, double* g)
-{
-    // over the whole global array: a slab packs its (possibly wrapped) ghost
-    // columns from columns it does not own
-    if (field == STS_U) {
-        for (int j = 0; j < c->ny; j++)
-            for (int i = 0; i <= c->nx; i++) {
-                const uint8_t k = u_kind_g(c, i, j, c->h_solid);
-                if (k == FK_FIXED0) g[(size_t)j * (c->nx + 1) + i] = 0.0;
-                else if (k == FK_INLET) g[(size_t)j * (c->nx + 1) + i] = c->u_in;
-            }
-        if (is_periodic(c))
-            for (int j = 0; j < c->ny; j++) g[(size_t)j * (c->nx + 1) + c->nx] = g[(size_t)j * (c->nx + 1)];
-    } else if (field == STS_V) {
-        for (int j = 0; j <= c->ny; j++)
-            for (int i = 0; i < c->nx; i++) {
-                const uint8_t k = v_kind_g(c, i, j, c->h_solid);
-                if (k == FK_FIXED0 || k == FK_WALL) g[(size_t)j * c->nx + i] = 0.0;
-            }
+    for (int k = 0; k < 3; k++)
+        if (k != ctx->cur)
+            CU(cudaMemcpyAsync(field_ptr(ctx->snap[k], field), dst, (size_t)rows * dp, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (slab && ctx->world > 1 && ctx->comm) {
+        const int which = ctx->cur;
+        sts_ctx* one[1] = {ctx};
+        sts_status e = exchange_group(one, 1, &which, ctx->stream);
+        if (e) return e;
+        for (int k = 0; k < 3; k++)        // the exchanged ghost columns into the other snapshots too
+            if (k != ctx->cur)
+                for (int f2 = 0; f2 < 4; f2++)
+                    CU(cudaMemcpyAsync(field_ptr(ctx->snap[k], f2), field_ptr(ctx->snap[ctx->cur], f2),
+                                       (size_t)(f2 == STS_V ? ctx->ny + 1 : ctx->ny) * dp, cudaMemcpyDeviceToDevice,
+                                       ctx->stream));
     }
+    return STS_OK;
 }
 
 extern "C" sts_status sts_set_field(sts_ctx* ctx, int32_t field, const double* host, int64_t n)
 {
-    if (!ctx || !host) return fail(ctx, STS_E_ARG, "null argument");
-    if (field < STS_U || field > STS_T) return fail(ctx, STS_E_ARG, "field not settable");
-    if ((size_t)n != global_size(ctx, field)) return fail(ctx, STS_E_ARG, "wrong buffer size");
-    CU(cudaSetDevice(ctx->device));
-    std::vector<double> g(host, host + n);
-    impose_fixed_host(ctx, field, g.data());
-    CU(cudaMemcpyAsync(ctx->stage, g.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    sts_status st = pack_into_all(ctx, field, ctx->stage);
+    sts_status st = set_field_any(ctx, field, host, n);
     if (st != STS_OK) return st;
     CU(cudaStreamSynchronize(ctx->stream));
     return STS_OK;
 }
 
-// Device variant: the caller guarantees fixed faces are already imposed
-// (e.g. a state read back with sts_get_field_device); used by the e2e bench.
 extern "C" sts_status sts_set_field_device(sts_ctx* ctx, int32_t field, const double* dev, int64_t n)
 {
-    if (!ctx || !dev) return fail(ctx, STS_E_ARG, "null argument");
-    if (field < STS_U || field > STS_T) return fail(ctx, STS_E_ARG, "field not settable");
-    if ((size_t)n == global_size(ctx, field)) return pack_into_all(ctx, field, dev);
-    // this rank's owned slab (sts_shape): owned columns into all snapshots, outlet
-    // ghosts replicated on the last in/outflow rank, then one halo exchange of the
-    // current snapshot so neighbour ghosts are consistent (multi-GPU e2e path)
-    const bool last = ctx->rank == ctx->world - 1;
-    const int rows = field == STS_V ? ctx->ny + 1 : ctx->ny;
-    const int ncols = ctx->nloc + (field == STS_U && last ? 1 : 0);
-    if ((int64_t)rows * ncols != n) return fail(ctx, STS_E_ARG, "wrong buffer size (neither global nor slab shape)");
-    CU(cudaSetDevice(ctx->device));
-    const int rep = (!is_periodic(ctx) && last && field != STS_U) ? OFF + ctx->nloc - 1 : -1;
-    double* d[3];
-    for (int k = 0; k < 3; k++)
-        d[k] = field == STS_U ? ctx->snap[k].u : field == STS_V ? ctx->snap[k].v : field == STS_P ? ctx->snap[k].p : ctx->snap[k].T;
-    slab_pack_kernel<<<592, 256, 0, ctx->stream>>>(rows, ncols, ctx->pitch, dev, d[0], d[1], d[2], rep);
-    ctx->launches++;
-    CU(cudaGetLastError());
-    if (ctx->world > 1 && !ctx->local_group) {
-        const int which = ctx->cur;
-        sts_ctx* one[1] = {ctx};
-        return exchange_group(one, 1, &which, ctx->stream);
-    }
-    return STS_OK;
+    return set_field_any(ctx, field, dev, n);
 }
 
 extern "C" sts_status sts_init_freestream(sts_ctx* ctx)
 {
     if (!ctx) return fail(ctx, STS_E_ARG, "null ctx");
     CU(cudaSetDevice(ctx->device));
-    for (int field = 0; field < 4; field++) {
-        size_t n = global_size(ctx, field);
-        double val = field == 0 ? ctx->u_in : field == 1 ? 0.0 : field == 2 ? ctx->gas.p_in : ctx->gas.T_in;
-        std::vector<double> g(n, val);
-        impose_fixed_host(ctx, field, g.data());
-        CU(cudaMemcpyAsync(ctx->stage, g.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        sts_status st = pack_into_all(ctx, field, ctx->stage);
-        if (st != STS_OK) return st;
-        CU(cudaStreamSynchronize(ctx->stream));
-    }
+    Snapshot* s = ctx->snap;
+    freestream_kernel<<<592, 256, 0, ctx->stream>>>((long long)cell_elems(ctx), (long long)v_elems(ctx), ctx->kind32,
+                                                   ctx->u_in, ctx->gas.p_in, ctx->gas.T_in, s[0].u, s[1].u, s[2].u,
+                                                   s[0].v, s[1].v, s[2].v, s[0].p, s[1].p, s[2].p, s[0].T, s[1].T, s[2].T);
+    ctx->launches++;
+    CU(cudaGetLastError());
     CU(cudaMemsetAsync(ctx->ue, 0, cell_elems(ctx) * sizeof(double), ctx->stream));
     CU(cudaMemsetAsync(ctx->ve, 0, v_elems(ctx) * sizeof(double), ctx->stream));
     CU(cudaMemsetAsync(ctx->Te, 0, cell_elems(ctx) * sizeof(double), ctx->stream));
@@ -931,15 +1033,16 @@ extern "C" sts_status sts_init_freestream(sts_ctx* ctx)
     return STS_OK;
 }
 
-// Owned slab of a field -> device buffer laid out as this rank's part of the
-// global shape (single GPU: the global shape).
-static sts_status unpack_owned(sts_ctx* ctx, int field, double* gdev, int64_t n)
+// This rank's owned part of a field (sts_shape) into a caller buffer (host or
+// device, compact rows x ncols), asynchronously on the context stream.
+static sts_status get_field_any(sts_ctx* ctx, int field, double* dst, int64_t n)
 {
-    const Snapshot& s = ctx->snap[ctx->cur];
-    int rows = (field == STS_V || field == STS_VEXP) ? ctx->ny + 1 : ctx->ny;
-    bool last = ctx->rank == ctx->world - 1;
-    int ncols = ctx->nloc + ((field == STS_U || field == STS_UEXP) && last ? 1 : 0);
+    if (!ctx || !dst) return fail(ctx, STS_E_ARG, "null argument");
+    CU(cudaSetDevice(ctx->device));
+    int rows, ncols;
+    owned_shape(ctx, field == STS_RHO ? STS_P : field, &rows, &ncols);
     if ((int64_t)rows * ncols != n) return fail(ctx, STS_E_ARG, "wrong buffer size");
+    const Snapshot& s = ctx->snap[ctx->cur];
     const double* src;
     switch (field) {
     case STS_U: src = s.u; break;
@@ -949,46 +1052,30 @@ static sts_status unpack_owned(sts_ctx* ctx, int field, double* gdev, int64_t n)
     case STS_UEXP: src = ctx->ue; break;
     case STS_VEXP: src = ctx->ve; break;
     case STS_TEXP: src = ctx->Te; break;
+    case STS_RHO:
+        ratio_kernel<<<592, 256, 0, ctx->stream>>>(rows, ncols, ctx->pitch, s.p, s.T, ctx->stage);
+        ctx->launches++;
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(dst, ctx->stage, (size_t)n * sizeof(double), cudaMemcpyDefault, ctx->stream));
+        return STS_OK;
     default: return fail(ctx, STS_E_ARG, "bad field");
     }
-    unpack_kernel<<<592, 256, 0, ctx->stream>>>(rows, ncols, OFF, ctx->pitch, ncols, 0, src, gdev);
-    ctx->launches++;
-    CU(cudaGetLastError());
+    CU(cudaMemcpy2DAsync(dst, (size_t)ncols * sizeof(double), src + OFF, (size_t)ctx->pitch * sizeof(double),
+                         (size_t)ncols * sizeof(double), rows, cudaMemcpyDefault, ctx->stream));
     return STS_OK;
 }
 
 extern "C" sts_status sts_get_field(sts_ctx* ctx, int32_t field, double* host, int64_t n)
 {
-    if (!ctx || !host) return fail(ctx, STS_E_ARG, "null argument");
-    CU(cudaSetDevice(ctx->device));
-    if (field == STS_RHO) {
-        // rho needs a scratch cell array: compute into stage-sized buffer via a temporary
-        double* tmp = nullptr;
-        CU(cudaMalloc(&tmp, cell_elems(ctx) * sizeof(double)));
-        const Snapshot& s = ctx->snap[ctx->cur];
-        ratio_kernel<<<592, 256, 0, ctx->stream>>>((long long)cell_elems(ctx), s.p, s.T, tmp);
-        ctx->launches++;
-        int rows = ctx->ny, ncols = ctx->nloc;
-        if ((int64_t)rows * ncols != n) { cudaFree(tmp); return fail(ctx, STS_E_ARG, "wrong buffer size"); }
-        unpack_kernel<<<592, 256, 0, ctx->stream>>>(rows, ncols, OFF, ctx->pitch, ncols, 0, tmp, ctx->stage);
-        ctx->launches++;
-        CU(cudaMemcpyAsync(host, ctx->stage, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-        cudaFree(tmp);
-        return STS_OK;
-    }
-    sts_status st = unpack_owned(ctx, field, ctx->stage, n);
+    sts_status st = get_field_any(ctx, field, host, n);
     if (st != STS_OK) return st;
-    CU(cudaMemcpyAsync(host, ctx->stage, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return STS_OK;
 }
 
 extern "C" sts_status sts_get_field_device(sts_ctx* ctx, int32_t field, double* dev, int64_t n)
 {
-    if (!ctx || !dev) return fail(ctx, STS_E_ARG, "null argument");
-    if (field == STS_RHO) return fail(ctx, STS_E_ARG, "STS_RHO only via sts_get_field");
-    return unpack_owned(ctx, field, dev, n);
+    return get_field_any(ctx, field, dev, n);
 }
 
 extern "C" sts_status sts_get_map(sts_ctx* ctx, int32_t which, int32_t* host, int64_t n)
@@ -1137,8 +1224,9 @@ static bool tol_graph_ok(const sts_ctx* c)
 }
 
 #define CG(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
-    if (cap) { cudaGraph_t g_ = nullptr; cudaStreamEndCapture(cap, &g_); if (g_) cudaGraphDestroy(g_); cudaStreamDestroy(cap); } \
+    /* the body capture first: its graph belongs to the outer one */ \
     if (cap2) { cudaGraph_t g_ = nullptr; cudaStreamEndCapture(cap2, &g_); cudaStreamDestroy(cap2); } \
+    if (cap) { cudaGraph_t g_ = nullptr; cudaStreamEndCapture(cap, &g_); if (g_) cudaGraphDestroy(g_); cudaStreamDestroy(cap); } \
     return fail(c, STS_E_CUDA, std::string("graph build: ") + cudaGetErrorString(e_)); } } while (0)
 
 static sts_status build_tol_graph(sts_ctx* c, int n1)
@@ -1156,16 +1244,43 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
     Params k = make_params(c);
     k.u_1 = c->snap[n1].u; k.v_1 = c->snap[n1].v; k.p_1 = c->snap[n1].p; k.T_1 = c->snap[n1].T;
     k.ue = c->ue; k.ve = c->ve; k.Te = c->Te;
-    march_fn march = march_graph_table(impl, tvd);
     const dim3 mgrid(c->march_nstrips * c->march_nseg);
-    auto pass = [&](int o, int w, int sl, cudaStream_t s) {
+    auto pass = [&](int o, int w, int sl, cudaStream_t s) -> cudaError_t {
         Params q = k;
         q.u_o = c->snap[o].u; q.v_o = c->snap[o].v; q.p_o = c->snap[o].p; q.T_o = c->snap[o].T;
         q.u_w = c->snap[w].u; q.v_w = c->snap[w].v; q.p_w = c->snap[w].p; q.T_w = c->snap[w].T;
         q.red = c->red2 + sl * 9;
         MarchParams m = make_march(c, q);
         m.done = &c->d_ls->done;
-        march<<<mgrid, MX, sizeof(MarchSmem), s>>>(m);
+        // the general and the all-regular kernel as two parallel kernel nodes after
+        // the capture's current dependencies (no cross-stream fork inside a
+        // conditional body)
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t g;
+        const cudaGraphNode_t* dp = nullptr;
+        size_t n = 0;
+        cudaError_t e = cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &dp, &n);
+        if (e != cudaSuccess) return e;
+        std::vector<cudaGraphNode_t> deps(dp, dp + n);
+        cudaGraphNode_t nodes[2];
+        int nn = 0;
+        for (int part = 0; part < 2; part++) {
+            const int cnt = part == 0 ? c->n_gen : c->n_reg;
+            if (cnt == 0) continue;
+            MarchParams mp = m;
+            mp.order = c->cta_order + (part ? c->n_gen : 0);
+            void* args[] = {&mp};
+            cudaKernelNodeParams kp = {};
+            kp.func = (void*)march_graph_table(impl, tvd, part);
+            kp.gridDim = dim3(cnt);
+            kp.blockDim = dim3(MX);
+            kp.sharedMemBytes = sizeof(MarchSmem);
+            kp.kernelParams = args;
+            e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
+            if (e != cudaSuccess) return e;
+            nn++;
+        }
+        return cudaStreamUpdateCaptureDependencies(s, nodes, nn, cudaStreamSetCaptureDependencies);
     };
     const int mn = c->sch.min_passes, mx = c->sch.max_passes;
     const double tol = c->sch.tol;
@@ -1185,7 +1300,7 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
         q.ue_w = c->ue; q.ve_w = c->ve; q.Te_w = c->Te;
         conv_march_table(tvd)<<<mgrid, MX, sizeof(ConvSmem), cap>>>(make_march(c, q));
     }
-    pass(n1, a, 0, cap);
+    CG(pass(n1, a, 0, cap));
     loop_check_kernel<<<1, 32, 0, cap>>>(c->red2, c->d_ls, h, mn, mx, tol);
     CG(cudaGetLastError());
     CG(cudaStreamGetCaptureInfo(cap, &cst, nullptr, &cg, &deps, &nd));
@@ -1199,9 +1314,9 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
     CG(cudaStreamUpdateCaptureDependencies(cap, &cn, 1, cudaStreamSetCaptureDependencies));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     CG(cudaStreamBeginCaptureToGraph(cap2, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    pass(a, b, 1, cap2);
+    CG(pass(a, b, 1, cap2));
     loop_check_kernel<<<1, 32, 0, cap2>>>(c->red2 + 9, c->d_ls, h, mn, mx, tol);
-    pass(b, a, 0, cap2);
+    CG(pass(b, a, 0, cap2));
     loop_check_kernel<<<1, 32, 0, cap2>>>(c->red2, c->d_ls, h, mn, mx, tol);
     CG(cudaGetLastError());
     cudaGraph_t bo = nullptr;
@@ -1257,7 +1372,6 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
     const int impl = ctx->sch.time == STS_IMPLICIT, tvd = ctx->sch.space == STS_TVD_VANLEER;
     // test hook: the graph instances (early exit on a zero `done` flag) launched from the stream
     const bool gk = getenv("STS_GRAPH_KERNEL") != nullptr;
-    march_fn march = gk ? march_graph_table(impl, tvd) : march_table(impl, tvd);
     if (gk && !ctx->red2) {
         CU(cudaMalloc(&ctx->red2, 18 * sizeof(unsigned long long)));
         CU(cudaMalloc(&ctx->d_ls, sizeof(LoopState)));
@@ -1343,13 +1457,14 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                     MarchParams ma = make_march(c, k), mb = ma;
                     ma.order = c->cta_split;
                     ma.seg = c->edge_seg;
-                    mb.order = c->cta_split + c->n_edge;
                     cudaStream_t as = overlap ? c->hstream : st;
                     if (overlap && it > 0) CU(cudaStreamWaitEvent(as, c->ev_b, 0));   // pass it-1 complete
                     prof_begin(c, 0);
-                    march<<<c->n_edge, MX, sizeof(MarchSmem), as>>>(ma);
+                    march_fn gen = gk ? march_graph_table(impl, tvd, 0) : march_table(impl, tvd, 0);
+                    gen<<<c->n_edge, MX, sizeof(MarchSmem), as>>>(ma);
                     if (overlap) CU(cudaEventRecord(c->ev_a[it & 1], as));
-                    march<<<c->n_split - c->n_edge, MX, sizeof(MarchSmem), st>>>(mb);
+                    c->launches += 1 + launch_march(c, mb, gk, st, c->cta_split + c->n_edge, c->n_split_gen,
+                                                    c->n_split - c->n_edge - c->n_split_gen);
                     if (overlap) {
                         CU(cudaStreamWaitEvent(st, c->ev_a[it & 1], 0));   // the pass ends with both sets
                         prof_end(c);
@@ -1361,15 +1476,12 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                     } else {
                         prof_end(c);
                     }
-                    c->launches += 2;
                 } else {
                     prof_begin(c, 0);
-                    const dim3 mgrid(c->march_nstrips * c->march_nseg);
                     MarchParams mk = make_march(c, k);
                     if (gk) mk.done = &c->d_ls->done;
-                    march<<<mgrid, MX, sizeof(MarchSmem), st>>>(mk);
+                    c->launches += launch_march(c, mk, gk, st, c->cta_order, c->n_gen, c->n_reg);
                     prof_end(c);
-                    c->launches++;
                 }
                 CU(cudaGetLastError());
                 which[r] = nw[r];

@@ -44,7 +44,7 @@ constexpr int WARM = 3;          // warm-up rows per segment: the longest carrie
                                  // E(J0) <- D(J0-1) <- C(J0-2) <- A(J0-3); 2 rows fail the bitwise
                                  // segmentation tests, 3 pass them for every variant down to 1-row segments
 constexpr uint32_t REG_BIT = 1u << 24;   // kind-word bit: the +-3 window is all fluid
-constexpr int ALLREG_BIT = 1 << 30;      // launch-order bit: every point of the CTA is regular
+constexpr int ALLREG_BIT = 1 << 30;      // launch-order bit: every point of the CTA is regular (conv kernel)
 
 struct MarchParams {
     Params k;                    // v1 parameter block (pointers, constants)
@@ -56,6 +56,7 @@ struct MarchParams {
     double B43_dydx, B43_dxdy;   // 4/3 B dy/dx, 4/3 B dx/dy (normal viscous links)
     double q_dx, q_dy;           // 1/(4 dx), 1/(4 dy) (bilinear differences in S^T_c)
     double h_dx, h_dy, inv_dt;   // 1/(2 dx), 1/(2 dy), 1/dt (pressure work, R9)
+    double pw_a;                 // C^T3 for the C^T3 Dp/Dt form of R9, else 0
     const int* done;             // graph-driven loop 2 (tolerance mode): loop finished -> the pass is a no-op
 };
 
@@ -171,7 +172,10 @@ struct MarchSmem {
 };
 // resident CTAs per SM: 4 (128 registers, 16 warps) for every variant (implicit TVD
 // spills 12 B at 128 registers and is still 4 % faster than at 3 CTAs / 154 registers)
-constexpr int MARCH_CTAS = 4;
+#ifndef STS_MARCH_CTAS
+#define STS_MARCH_CTAS 4
+#endif
+constexpr int MARCH_CTAS = STS_MARCH_CTAS;
 // max that ignores a NaN operand (NaN u / v are flagged separately, T / p by the bad-state test)
 __device__ __forceinline__ double dmax(double m, double x) { return x > m ? x : m; }
 
@@ -247,7 +251,7 @@ struct StepVars {
 };
 struct NM1 {                      // n-1 state / explicit planes at this thread's points
     double p1n, T1n;              // row j+1
-    double p1c, T1c, u1c, v1n;    // p^{n-1}(i, j), T^{n-1}(i, j), u^{n-1}(i, j), v^{n-1}(i, j+1)
+    double T1c, u1c, v1n;         // T^{n-1}(i, j), u^{n-1}(i, j), v^{n-1}(i, j+1)
     double Tec, uec, ven;         // T^exp(i, j), u^exp(i, j), v^exp(i, j+1)
 };
 
@@ -308,6 +312,11 @@ __device__ __forceinline__ void ring_issue_tma(SM& s, int sl, const MarchParams&
     cp_commit();
 }
 
+// Convective part of an upwind/TVD link coefficient, max(0, F) - F psi (Eqs. pl15,
+// pl31); psi is the constant 0 without TVD, and F * 0 must not be formed
+// (IEEE cannot fold it: F * 0 is NaN for F = inf).
+#define STS_LINK(F, ps) (TVD ? max0(F) - (F) * (ps) : max0(F))
+
 // ================= stage A: row j+1 fluxes, link pieces =================
 template <bool IMPL, bool TVD, bool REG>
 __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
@@ -359,7 +368,7 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             double ps = 0.0;
             if (IMPL && TVD && cF<REG>(R0.KK[lc - 2]) && cF<REG>(kl) && cF<REG>(kw0) && cF<REG>(R0.KK[lc + 1]))
                 ps = psi_f(R0.T[lc - 2], R0.T[lc - 1], R0.T[lc], R0.T[lc + 1], R0.U[lc]);
-            pw = (IMPL ? max0(F) - F * ps : 0.0) + D;
+            pw = (IMPL ? STS_LINK(F, ps) : 0.0) + D;
         }
         s.XTW[lc] = pw;
     }
@@ -373,7 +382,7 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         double ps = 0.0;
         if (IMPL && TVD && cF<REG>(Rm.KK[lc]) && cF<REG>(kw0) && cF<REG>(kw1) && cF<REG>(Rb.KK[lc]))
             ps = psi_f(Rm.T[lc], R0.T[lc], Ra.T[lc], Rb.T[lc], Ra.V[lc]);
-        v.ytSn = (IMPL ? max0(F) - F * ps : 0.0) + D;
+        v.ytSn = (IMPL ? STS_LINK(F, ps) : 0.0) + D;
         v.ytN = IMPL ? v.ytSn - F : v.ytSn;
     }
     // u-eq x pieces of cell (i, j): a^u_2 of face i, a^u_1 of face i+1 (transposed pl15)
@@ -387,7 +396,7 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             if (IMPL && TVD && uA<REG>(R0.KK[lc - 1]) && uA<REG>(kw0) && uA<REG>(R0.KK[lc + 1]) &&
                 uA<REG>(R0.KK[lc + 2]))
                 ps = psi_f(R0.U[lc - 1], R0.U[lc], R0.U[lc + 1], R0.U[lc + 2], ub);
-            xw = (IMPL ? max0(Fb) - Fb * ps : 0.0) + D;
+            xw = (IMPL ? STS_LINK(Fb, ps) : 0.0) + D;
             xe = IMPL ? xw - Fb : xw;
         }
         s.XUW[lc] = xw;              // a^u_1 of face i+1 (neighbour); a^u_2 and F-bar stay here
@@ -413,7 +422,7 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         double ps = 0.0;
         if (IMPL && TVD && vA<REG>(kw0) && vA<REG>(kw1) && vA<REG>(Rb.KK[lc]) && vA<REG>(Rc.KK[lc]))
             ps = psi_f(R0.V[lc], Ra.V[lc], Rb.V[lc], Rc.V[lc], vb);
-        v.vcSn = (IMPL ? max0(v.FbN) - v.FbN * ps : 0.0) + D;
+        v.vcSn = (IMPL ? STS_LINK(v.FbN, ps) : 0.0) + D;
         v.vcN = IMPL ? v.vcSn - v.FbN : v.vcSn;
     }
     // corner Gamma at (x^f_i, y^f_{j+1}) (R4, R5; BC spec 8)
@@ -441,9 +450,43 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         }
         const double D = m.B_dydx * v.gcN;
         v.FwSum = F1 + F2;
-        v.xvW = (IMPL ? 0.5 * (max0(F1) - F1 * p1 + max0(F2) - F2 * p2) : 0.0) + D;
+        v.xvW = (IMPL ? 0.5 * (STS_LINK(F1, p1) + STS_LINK(F2, p2)) : 0.0) + D;
         s.XVW[lc] = v.xvW;           // the E side of v-face (i-1, j+1) is XVW - (F^x(j) + F^x(j+1))/2
     }
+}
+
+// S^T_c pieces of a general (boundary) point.
+// dv/dx + du/dy from mid-face velocities: bilinear 4-point means (R4), or on a
+// face that lies on a wall the slip velocity of Eq. pl38 (R38).
+__device__ __forceinline__ double shear_general(const RingRow& R0, const RingRow& Ra, const RingRow& Rm, int lc,
+                                             double rP, const MarchParams& m)
+{
+    const Params& k = m.k;
+    const double zeta = 1.1466 * k.Kn * rcp(rP);
+    auto slip = [&](double vP, double vw, double dn) { return (dn * vw + zeta * vP) * rcp(dn + zeta); };
+    const double vs = R0.V[lc] + Ra.V[lc], us = R0.U[lc] + R0.U[lc + 1];
+    const uint8_t kE = ckind(R0.KK[lc + 1]), kW = ckind(R0.KK[lc - 1]);
+    const uint8_t kN = ckind(Ra.KK[lc]), kS = ckind(Rm.KK[lc]);
+    const double vE = wallish(kE) ? slip(0.5 * vs, 0.0, 0.5 * k.dx) : 0.25 * (vs + (R0.V[lc + 1] + Ra.V[lc + 1]));
+    const double vW = wallish(kW) ? slip(0.5 * vs, 0.0, 0.5 * k.dx) : 0.25 * ((R0.V[lc - 1] + Ra.V[lc - 1]) + vs);
+    const double uN = wallish(kN) ? slip(0.5 * us, kN == CK_WALLY ? k.u_wt : 0.0, 0.5 * k.dy)
+                                  : 0.25 * (us + (Ra.U[lc] + Ra.U[lc + 1]));
+    const double uS = wallish(kS) ? slip(0.5 * us, kS == CK_WALLY ? k.u_wb : 0.0, 0.5 * k.dy)
+                                  : 0.25 * ((Rm.U[lc] + Rm.U[lc + 1]) + us);
+    return (vE - vW) * m.inv_dx + (uN - uS) * m.inv_dy;
+}
+// Pressure gradient of the C^T3 Dp/Dt term (R9) at a general point: face
+// pressures = mean of the two cells, = p of the cell at a wall.
+__device__ __forceinline__ void dp_general(const RingRow& R0, const RingRow& Ra, const RingRow& Rm, int lc,
+                                        const MarchParams& m, double& dpx, double& dpy)
+{
+    const double pc = R0.P[lc];
+    const double pe = wallish(ckind(R0.KK[lc + 1])) ? pc : 0.5 * (pc + R0.P[lc + 1]);
+    const double pw = wallish(ckind(R0.KK[lc - 1])) ? pc : 0.5 * (R0.P[lc - 1] + pc);
+    const double pn = wallish(ckind(Ra.KK[lc])) ? pc : 0.5 * (pc + Ra.P[lc]);
+    const double ps = wallish(ckind(Rm.KK[lc])) ? pc : 0.5 * (Rm.P[lc] + pc);
+    dpx = (pe - pw) * m.inv_dx;
+    dpy = (pn - ps) * m.inv_dy;
 }
 
 // ================= stage C: T_{i,j}, u-hat_{i,j}, v-hat_{i,j+1} =================
@@ -495,46 +538,28 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
             shear = ((R0.V[lc + 1] + Ra.V[lc + 1]) - (R0.V[lc - 1] + Ra.V[lc - 1])) * m.q_dx
                   + ((Ra.U[lc] + Ra.U[lc + 1]) - (Rm.U[lc] + Rm.U[lc + 1])) * m.q_dy;
         } else {
-            const double zeta = 1.1466 * k.Kn * rcp(rP);
-            auto slip = [&](double vP, double vw, double dn) { return (dn * vw + zeta * vP) * rcp(dn + zeta); };
-            const double vs = R0.V[lc] + Ra.V[lc], us = R0.U[lc] + R0.U[lc + 1];
-            const uint8_t kE = ckind(R0.KK[lc + 1]), kW = ckind(R0.KK[lc - 1]);
-            const uint8_t kN = ckind(kw1), kS = ckind(Rm.KK[lc]);
-            const double vE = wallish(kE) ? slip(0.5 * vs, 0.0, 0.5 * dx) : 0.25 * (vs + (R0.V[lc + 1] + Ra.V[lc + 1]));
-            const double vW = wallish(kW) ? slip(0.5 * vs, 0.0, 0.5 * dx) : 0.25 * ((R0.V[lc - 1] + Ra.V[lc - 1]) + vs);
-            const double uN = wallish(kN) ? slip(0.5 * us, kN == CK_WALLY ? k.u_wt : 0.0, 0.5 * dy)
-                                          : 0.25 * (us + (Ra.U[lc] + Ra.U[lc + 1]));
-            const double uS = wallish(kS) ? slip(0.5 * us, kS == CK_WALLY ? k.u_wb : 0.0, 0.5 * dy)
-                                          : 0.25 * ((Rm.U[lc] + Rm.U[lc + 1]) + us);
-            shear = (vE - vW) * m.inv_dx + (uN - uS) * m.inv_dy;
+            shear = shear_general(R0, Ra, Rm, lc, rP, m);
         }
         const double div = dudx + dvdy;
         // pressure work (R9): C^T3 Dp/Dt of Eq. pl6 at the old iterate --
         // (p - p^{n-1}) / dt + ubar dp/dx + vbar dp/dy with face pressures p_f =
-        // mean of the two cells, = p of the cell at a wall -- or kappa p div(u)
-        double pwork;
+        // mean of the two cells, = p of the cell at a wall -- or kappa p div(u);
+        // branch-free: pw_a = C^T3 or 0, pwk = 0 or kappa.  p^{n-1} = rho^{n-1} T^{n-1}
+        // (the (p/T)^{n-1} row times T^{n-1}, within 2 ulp of the stored p^{n-1})
         const double pc = R0.P[lc];
-        if (k.pw_form == PW_DPDT) {
-            double dpx, dpy;
-            if (REG) {
-                dpx = (R0.P[lc + 1] - R0.P[lc - 1]) * m.h_dx;
-                dpy = (Ra.P[lc] - Rm.P[lc]) * m.h_dy;
-            } else {
-                const double pe = wallish(ckind(R0.KK[lc + 1])) ? pc : 0.5 * (pc + R0.P[lc + 1]);
-                const double pw = wallish(ckind(R0.KK[lc - 1])) ? pc : 0.5 * (R0.P[lc - 1] + pc);
-                const double pn = wallish(ckind(kw1)) ? pc : 0.5 * (pc + Ra.P[lc]);
-                const double ps = wallish(ckind(Rm.KK[lc])) ? pc : 0.5 * (Rm.P[lc] + pc);
-                dpx = (pe - pw) * m.inv_dx;
-                dpy = (pn - ps) * m.inv_dy;
-            }
-            const double ub = 0.5 * (R0.U[lc] + R0.U[lc + 1]), vb = 0.5 * (R0.V[lc] + Ra.V[lc]);
-            pwork = k.CT3 * ((pc - nm.p1c) * m.inv_dt + ub * dpx + vb * dpy);
+        const double p1 = s.R1[lc] * nm.T1c;
+        double dpx, dpy;
+        if (REG) {
+            dpx = (R0.P[lc + 1] - R0.P[lc - 1]) * m.h_dx;
+            dpy = (Ra.P[lc] - Rm.P[lc]) * m.h_dy;
         } else {
-            pwork = k.pwk * pc * div;
+            dp_general(R0, Ra, Rm, lc, m, dpx, dpy);
         }
+        const double ub = 0.5 * (R0.U[lc] + R0.U[lc + 1]), vb = 0.5 * (R0.V[lc] + Ra.V[lc]);
+        const double pwork = m.pw_a * ((pc - p1) * m.inv_dt + ub * dpx + vb * dpy) + k.pwk * pc * div;
         const double Sc = (k.CT2 * gP * (2.0 * (dudx * dudx + dvdy * dvdy) + shear * shear - 2.0 / 3.0 * div * div)
                            + pwork) * m.dV;
-        const double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + Sc + nm.Tec) + s.R1[lc] * nm.T1c * m.dV;
+        const double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + (IMPL ? Sc : Sc + nm.Tec)) + p1 * m.dV;
         v.TN = rhs * rcp(a0);
     }
     // ---- u pseudo-velocity at u-face (i, j)
@@ -543,7 +568,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         const double F1 = v.Fy1, F2 = Fn.FY[lc - 1];
         const double D = m.B_dxdy * v.gcN;
         v.FsSumN = F1 + F2;
-        v.utSn = (IMPL ? 0.5 * (max0(F1) - F1 * v.upsi1 + max0(F2) - F2 * v.upsi2) : 0.0) + D;
+        v.utSn = (IMPL ? 0.5 * (STS_LINK(F1, v.upsi1) + STS_LINK(F2, v.upsi2)) : 0.0) + D;
         const double a4p = IMPL ? v.utSn - 0.5 * v.FsSumN : v.utSn;
         double uhat = 0.0, du = 0.0;
         if (uA<REG>(kw0)) {
@@ -577,7 +602,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
                                     + 2.0 / 3.0 * gL * (Ra.V[lc - 1] - R0.V[lc - 1]))
                            + k.g_x * (rR + rL) * m.half_dV;
             const double r = rcp(a0);
-            uhat = (a1 * R0.U[lc - 1] + a2 * R0.U[lc + 1] + a3 * uS + a4 * uN + b + nm.uec) * r;
+            uhat = (a1 * R0.U[lc - 1] + a2 * R0.U[lc + 1] + a3 * uS + a4 * uN + (IMPL ? b : b + nm.uec)) * r;
             du = m.A_dy * r;
         }
         v.uhat = uhat;
@@ -628,7 +653,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
                                 + 2.0 / 3.0 * gB * (R0.U[lc + 1] - R0.U[lc]))
                        + k.g_y * (rT + rB) * m.half_dV;
         const double r = rcp(a0);
-        v.vhatN = (a1 * vW + a2 * vE + a3 * R0.V[lc] + a4 * Rb.V[lc] + b + nm.ven) * r;
+        v.vhatN = (a1 * vW + a2 * vE + a3 * R0.V[lc] + a4 * Rb.V[lc] + (IMPL ? b : b + nm.ven)) * r;
         v.dvN = m.A_dx * r;
     }
 }
@@ -738,7 +763,13 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
     }
 }
 
-template <bool IMPL, bool TVD, bool GRAPH = false>
+// REGK = true: the kernel of the all-regular CTAs (every point of the CTA's rows
+// and columns, warm-up rows included, is regular -- host-classified): the row
+// loop is compiled with the regular stage instances only, reads no kinds and
+// has a register allocation of its own.  REGK = false: every other CTA, with
+// the per-point choice between the instances.  A regular point runs the same
+// instance code in both kernels, so the split never changes a bit.
+template <bool IMPL, bool TVD, bool GRAPH = false, bool REGK = false>
 __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -748,7 +779,6 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     const int t = threadIdx.x;
     const int ow = m.order[blockIdx.x];
     const int cta = ow & (ALLREG_BIT - 1);
-    const bool allreg = (ow & ALLREG_BIT) != 0;          // every point of the CTA is regular (host)
     const int strip = cta % m.nstrips, segi = cta / m.nstrips;
     const int I0 = k.gi0 + strip * MW;                  // first owned column of the strip
     // ring column 0 = stored column c0 (a multiple of 4: 16-byte aligned TMA rows); this
@@ -774,7 +804,7 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     // here on, row j+4 is issued at the start of step j and lands before its B3);
     // ring slots of rows j-1 .. j+4, rotated by one per row step
     RingRow *pm = &s.ring[0], *p0 = &s.ring[1], *pa = &s.ring[2], *pb = &s.ring[3], *pc = &s.ring[4], *pd = &s.ring[5];
-    const bool kinds = !(allreg && !(IMPL && TVD));      // the all-regular loop copies read no kinds
+    constexpr bool kinds = !REGK;                        // the all-regular loop reads no kinds
     for (int q = 0; q < 5; q++) ring_issue_tma(s, q, m, c0, tma, js - 1 + q, kinds);   // row js-1+q -> slot q
     cp_wait_all();
     __syncthreads();
@@ -799,7 +829,7 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     NM1 nm;
     nm.Tec = nm.uec = nm.ven = 0.0;
     auto nm_prefetch_init = [&]() {
-        nm.p1n = ld(k.p_1, js + 1); nm.T1n = ld(k.T_1, js + 1); nm.p1c = ld(k.p_1, js);
+        nm.p1n = ld(k.p_1, js + 1); nm.T1n = ld(k.T_1, js + 1);
         nm.T1c = ld(k.T_1, js); nm.u1c = ld(k.u_1, js); nm.v1n = ldv(k.v_1, js + 1);
         if (!IMPL) { nm.Tec = ld(k.Te, js); nm.uec = ld(k.ue, js); nm.ven = ldv(k.ve, js + 1); }
     };
@@ -809,41 +839,19 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     StepVars v;
     int oj = js * k.pitch + col;                        // element offset of (row j, own column), + pitch per step (upwind prefetch)
 
-    // The row loop, compiled twice: once with the regular stage instances only,
-    // for all-regular CTAs (no per-point dispatch).  Measured: implicit upwind
-    // -3.2 %, explicit upwind -2.8 %, explicit TVD -2 %; implicit TVD +0.2 %, so
-    // it keeps one copy.
-    // Measured per variant (profiles/r01_v8_summary.md): implicit TVD keeps one
-    // copy without the n-1 prefetch (no registers to spare); implicit upwind is
-    // fastest with the prefetch set-up inside each copy, the explicit variants
-    // with it ahead of the branch.
-    if constexpr (IMPL && TVD) {
-        constexpr bool ALLREG = false;
-        constexpr bool PREF_L = false;
-#include "sts_march_loop.inc"
-    } else if constexpr (IMPL) {
-        if (allreg) {
-            constexpr bool ALLREG = true;
-            constexpr bool PREF_L = true;
-            nm_prefetch_init();
-#include "sts_march_loop.inc"
-        } else {
-            constexpr bool ALLREG = false;
-            constexpr bool PREF_L = true;
-            nm_prefetch_init();
-#include "sts_march_loop.inc"
-        }
-    } else {
+    // The row loop: the all-regular kernel prefetches the n-1 values of its
+    // column one row step ahead through registers; the general kernel of the
+    // implicit TVD variant has no registers to spare for it.
+    if constexpr (REGK) {
+        constexpr bool ALLREG = true;
+        constexpr bool PREF_L = true;
         nm_prefetch_init();
-        if (allreg) {
-            constexpr bool ALLREG = true;
-            constexpr bool PREF_L = true;
 #include "sts_march_loop.inc"
-        } else {
-            constexpr bool ALLREG = false;
-            constexpr bool PREF_L = true;
+    } else {
+        constexpr bool ALLREG = false;
+        constexpr bool PREF_L = !(IMPL && TVD);
+        if (PREF_L) nm_prefetch_init();
 #include "sts_march_loop.inc"
-        }
     }
     cp_wait_all();
     const double qnan = __longlong_as_double(0x7ff8000000000000LL);
@@ -872,3 +880,4 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
 }
 
 }  // namespace sts
+#undef STS_LINK

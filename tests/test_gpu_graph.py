@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from paper_1802_04243_b200 import workloads as W
-from tests.parity_util import FIELDS, rel_errors, seeded_pair
+from tests.parity_util import FIELDS, TOL, rel_errors, seeded_pair
 
 pytestmark = pytest.mark.gpu
 
@@ -99,7 +99,7 @@ def test_graph_loop_vs_oracle(S, oracle_mod):
         assert stats["passes_done"] - done == opasses, (stats["passes_done"] - done, opasses)
         done = stats["passes_done"]
     err = rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), o.get_map(0) == 0)
-    assert max(err.values()) <= 1e-8, err
+    assert max(err.values()) <= TOL, err
 
 
 def test_graph_loop_bad_state(S):

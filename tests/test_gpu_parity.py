@@ -72,10 +72,13 @@ def test_parity_transposition_box(S, oracle_mod):
 
 @pytest.mark.parametrize("variant", list(W.VARIANTS))
 def test_parity_c1(S, oracle_mod, variant):
-    """C1 (120 x 40, Delta = 0.25, supersonic past one square), 20 steps x 10 passes
-    from the free stream (explicit TVD: 10 steps, it oscillates later)."""
+    """BASELINE configs[0] at its stated length: C1 (120 x 40, Delta = 0.25,
+    supersonic past one square), 200 steps x 10 passes from the free stream, every
+    variant (explicit TVD at dt = 0.05 Delta, R39).  Implicit TVD's loop 2 does not
+    converge here (limiter switching, DESIGN 9), yet GPU and oracle stay within
+    1e-11 over the 2000 passes (tools/drift.py)."""
     case = W.c1(variant, passes=10)
-    steps = 10 if variant == "explicit_tvd" else 20
+    steps = 200
     g = S.Solver(case)
     o = oracle_mod.Case(case)
     g.advance(steps)
@@ -138,7 +141,7 @@ def test_tolerance_mode_converges(S, oracle_mod):
     assert stats["converged"] == 1 and ost == 0
     assert max(stats["res"]) < 1e-9
     err = rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), o.get_map(0) == 0)
-    assert max(err.values()) <= 1e-8, err
+    assert max(err.values()) <= TOL, err
 
 
 def test_parity_bench_configuration(S, oracle_mod):
@@ -223,4 +226,66 @@ def test_parity_paper_mesh_tolerance_mode(S, oracle_mod):
     assert st == 0 and ost == 0 and stats["converged"] == 1
     assert stats["passes_done"] == opasses, (stats["passes_done"], opasses)
     err = rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), o.get_map(0) == 0)
-    assert max(err.values()) <= 1e-8, err
+    assert max(err.values()) <= TOL, err
+
+
+@pytest.mark.parametrize("variant", ["implicit_upwind", "explicit_tvd", "explicit_upwind"])
+def test_parity_paper_mesh_bench_length(S, oracle_mod, variant):
+    """The paper's 4032 x 200 mesh (C3, H = 10) at SURVEY 8(d).2's C3 run length,
+    20 steps x 10 passes from the free stream, in the bench's launch
+    configuration: every element of u, v, p, T, rho compared with the oracle
+    (~1.5 min of oracle time each)."""
+    case = W.c3(10, variant, passes=10)
+    g = S.Solver(case)
+    o = oracle_mod.Case(case)
+    g.advance(20)
+    assert o.advance(20)[0] == 0
+    err = rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), o.get_map(0) == 0)
+    assert max(err.values()) <= TOL, err
+
+
+def test_parity_implicit_tvd_paper_mesh_conditioning(S, oracle_mod):
+    """Implicit TVD on the paper mesh: loop 2 is not a contraction there (the limiter
+    switches between passes), so the method amplifies ANY rounding-level difference:
+    two oracle runs whose T differs by one ulp differ by 1.2e-8 after 2 steps x 10
+    passes (tools/ulp_growth.py).  The 1e-9 bar is therefore tested at 1 step x 10
+    passes (the bench's pass count), and over 3 steps the GPU-vs-oracle difference
+    must stay within the oracle's own one-ulp sensitivity (x10)."""
+    case = W.c3(10, "implicit_tvd", passes=10)
+    g = S.Solver(case)
+    o = oracle_mod.Case(case)
+    o2 = oracle_mod.Case(case)
+    o2.set("T", np.nextafter(o2.get("T"), 2.0))
+    fluid = o.get_map(0) == 0
+    g.advance(1)
+    assert o.advance(1)[0] == 0 and o2.advance(1)[0] == 0
+    err = rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), fluid)
+    assert max(err.values()) <= TOL, err
+    g.advance(2)
+    assert o.advance(2)[0] == 0 and o2.advance(2)[0] == 0
+    e_gpu = max(rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), fluid).values())
+    e_ulp = max(rel_errors(o2.fields(), o.fields(), fluid).values())
+    assert e_gpu <= 10 * e_ulp, (e_gpu, e_ulp)
+
+
+def test_parity_c2_full(S, oracle_mod):
+    """BASELINE configs[1] against the oracle: C2 (4096 x 256, 1 M FVs, periodic
+    slip Poiseuille, implicit upwind), 20 steps x 10 passes from the seeded
+    perturbed closed-form state (~2 min of oracle time)."""
+    import math
+    case = W.c2(small=False, variant="implicit_upwind", passes=10)
+    H, N, Kn, gx = 1.0, case["ny"], case["Kn"], case["g_x"]
+    B = 5.0 * math.sqrt(math.pi) / 16.0 * Kn
+    y = (np.arange(N) + 0.5) * H / N
+    prof = (gx / (2 * B)) * (y * (H - y) + 1.1466 * Kn * H)
+    g = S.Solver(case)
+    o = oracle_mod.Case(case)
+    noise = W.perturbation(case, seed=8, amplitude=0.001)
+    st = {"u": prof[:, None] * noise["u"], "v": 0.001 * noise["v"], "p": noise["p"], "T": noise["T"]}
+    for k in ("p", "T", "u", "v"):
+        g.set_field(k, st[k])
+        o.set(k, st[k])
+    g.advance(20)
+    assert o.advance(20)[0] == 0
+    err = rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), o.get_map(0) == 0)
+    assert max(err.values()) <= TOL, err
