@@ -116,14 +116,18 @@ typedef struct {
 typedef struct { int32_t rank, world, device; const void* nccl_id; } sts_dist;
 
 /* Statistics of the last sts_advance: steps/passes done (cumulative), last
- * residuals (u, v, p, T), converged flag of the last step, first bad cell
- * (flat global index, -1 if none) and its field (STS_P / STS_T / STS_U ...). */
+ * residuals (u, v, p, T), converged flag of the last step.  On STS_E_STATE:
+ * the FIRST bad state of the call -- its cell (flat global index j*nx + i, -1
+ * for a NaN velocity), field (STS_P / STS_T, STS_U for a NaN velocity) and the
+ * cumulative pass index at which it appeared.  The passes after it do no work
+ * (a sticky device flag), and the state is undefined. */
 typedef struct {
     int64_t steps_done, passes_done;
     double res[4];
     int32_t converged;
     int32_t bad_field;
     int64_t bad_cell;
+    int64_t bad_pass;
 } sts_stats;
 
 typedef struct sts_ctx sts_ctx;

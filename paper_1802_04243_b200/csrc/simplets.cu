@@ -96,14 +96,13 @@ struct sts_ctx {
     std::vector<uint8_t> h_ck, h_uk, h_vk; // host copies of the local kind maps
     std::vector<uint8_t> h_solid;          // slab-local solid map, ny x sol_w (unwrapped columns from sol_lo)
     int sol_lo = 0, sol_w = 0;
-    int march_seg = 0, march_nseg = 0, march_nstrips = 0;
-    int* cta_order = nullptr;              // launch order of the march CTAs: general CTAs (longest
+    int march_seg = 0, march_nstrips = 0;   // regular CTA height (Hr), strips
+    int* cta_order = nullptr;              // (int4) launch order of the march CTAs: general CTAs (longest
                                            // first), then the all-regular ones
     int n_gen = 0, n_reg = 0;              // CTAs of the general / all-regular march kernel
-    int* cta_split = nullptr;              // multi-GPU split: edge strips first (general kernel),
+    int* cta_split = nullptr;              // (int4) multi-GPU split: edge strips first (general kernel),
                                            // then the interior general and all-regular CTAs
     int n_edge = 0;                        // CTAs in the edge strips
-    int edge_seg = 0;                      // their (shorter) segment height
     int n_split = 0;                       // entries of cta_split
     int n_split_gen = 0;                   // interior general CTAs of cta_split
     cudaStream_t gstream = nullptr;        // the general CTAs of a pass run here, beside the regular ones
@@ -112,7 +111,8 @@ struct sts_ctx {
     // stream while the interior strips of the next pass run on the pass stream
     cudaStream_t hstream = nullptr;
     cudaEvent_t ev_a[2] = {nullptr, nullptr}, ev_b = nullptr, ev_s = nullptr, ev_h = nullptr;
-    unsigned long long* red = nullptr;     // [max_passes][9]
+    unsigned long long* red = nullptr;     // [max_passes][9] residual slots, then the sticky bad key
+    unsigned long long* bad = nullptr;     // = red + 9 max_passes: first bad state of the advance call
     // graph-driven loop 2 (tolerance mode, one context without NCCL): one CUDA
     // graph per snapshot rotation, loop 2 as a conditional WHILE node
     cudaGraphExec_t tol_exec[3] = {nullptr, nullptr, nullptr};
@@ -131,6 +131,7 @@ struct sts_ctx {
     // stats / profiling
     sts_stats stats{};
     bool profiling = false;
+    long long pass0 = 0;                   // passes_done when the current advance call started
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, int>> ev_used;   // (start idx, kind)
     double prof_pass_n = 0, prof_pass_ms = 0, prof_conv_n = 0, prof_conv_ms = 0, launches = 0;
@@ -349,9 +350,7 @@ static MarchParams make_march(const sts_ctx* c, const Params& k)
     MarchParams m{};
     m.k = k;
     m.kind = c->kind32;
-    m.seg = c->march_seg;
-    m.nstrips = c->march_nstrips;
-    m.order = c->cta_order;
+    m.order = (const int4*)c->cta_order;
     const double dx = c->spacing, dy = c->spacing, dt = c->sch.dt;
     m.inv_dx = 1.0 / dx; m.inv_dy = 1.0 / dy;
     m.CT1_dydx = c->CT1 * dy / dx; m.CT1_dxdy = c->CT1 * dx / dy;
@@ -362,24 +361,31 @@ static MarchParams make_march(const sts_ctx* c, const Params& k)
     m.q_dx = 0.25 / dx; m.q_dy = 0.25 / dy;
     m.h_dx = 0.5 / dx; m.h_dy = 0.5 / dy; m.inv_dt = 1.0 / dt;
     m.pw_a = c->gas.pw_form == PW_DPDT ? c->CT3 : 0.0;
+    m.bad = c->bad;
+    m.pass_key = 0xFFFFF;
     return m;
 }
 
-// Segment height and CTA order of the y-march.  Cost model per row step of a
-// CTA (it advances at the pace of its slowest warp, barriers every stage): a
-// warp whose 32 points are all regular costs 1, an all-general warp 1.35, a
-// mixed warp 2.35 (both instances).  For each candidate segment count the
-// CTAs (+WARM = 3 warm-up rows each) are list-scheduled longest-first onto the
-// resident slots (148 SMs x CTAs/SM from the occupancy API); the count with
-// the smallest makespan wins, and the same longest-first order is the launch
-// order (blockIdx.x -> CTA), so the boundary CTAs (inlet, squares, walls)
-// start in the first wave.
+// CTA schedule of the y-march (DESIGN 5.1).  Every strip of MX columns is cut
+// along y into CTAs {strip, J0, J1, flags}.  Row j of a strip can belong to an
+// all-regular CTA when every point of rows j-3 .. j (the warm-up reach) in the
+// strip's 128 columns is regular; such rows form regular runs, run by the
+// all-regular kernel in CTAs of about Hr rows.  The other rows (near the
+// channel walls and the squares, the inlet and outlet strips) form general
+// runs, cut into CTAs of at most Hg rows: a general row step costs up to 2.35
+// regular ones (warps that mix both instances run both), so short general CTAs
+// keep them off the critical path.  Cost of a CTA = its rows + WARM warm-up rows,
+// each weighted by the slowest warp of the row (regular 1, general 1.35, mixed
+// 2.35); Hg and Hr minimise the makespan of a longest-first list schedule onto
+// the resident slots (148 SMs x CTAs/SM from the occupancy API).
+struct CtaE { int strip, J0, J1, flags; double cost; };
+
 static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
 {
     int dev_sms = 148, per_sm = 3;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
     int nb = 0;
-    const void* fn = (const void*)march_table(c->sch.time == STS_IMPLICIT, c->sch.space == STS_TVD_VANLEER, 0);
+    const void* fn = (const void*)march_table(c->sch.time == STS_IMPLICIT, c->sch.space == STS_TVD_VANLEER, 1);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, MX, sizeof(MarchSmem)) == cudaSuccess && nb > 0)
         per_sm = nb;
     const int strips = (c->nloc + MW - 1) / MW;
@@ -387,135 +393,128 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     const int ny = c->ny;
     double w_gen = 1.35, w_mix = 2.35;                  // warp costs relative to an all-regular warp
     if (const char* cv = getenv("STS_COST")) sscanf(cv, "%lf,%lf", &w_gen, &w_mix);   // tuning hook
-    // row cost of every (strip, row), prefix-summed over rows
-    std::vector<double> pre((size_t)strips * (ny + 1), 0.0);
-    for (int st = 0; st < strips; st++) {
-        const int I0 = c->gi0 + st * MW;
+    const bool no_allreg = getenv("STS_NO_ALLREG") != nullptr;   // test hook: every CTA general
+    int forced = 0;
+    if (const char* sv = getenv("STS_SEG")) forced = std::max(0, atoi(sv));   // test hook: all heights
+    // per (strip, row): cost of a row step and "all 128 points regular"
+    std::vector<double> rcost((size_t)strips * ny);
+    std::vector<uint8_t> rreg((size_t)strips * ny);
+    for (int st = 0; st < strips; st++)
         for (int j = 0; j < ny; j++) {
             double rc = 1.0;
+            int all = 1;
             for (int w = 0; w < MX / 32; w++) {
                 int nreg = 0;
                 for (int l = 0; l < 32; l++) {
-                    const int li = I0 - 2 + 32 * w + l - c->gi0 + OFF;
+                    const int li = st * MW - 2 + 32 * w + l + OFF;
                     if (li >= 0 && li < c->pitch && (packed[(size_t)j * c->pitch + li] & REG_BIT)) nreg++;
                 }
-                const double wc = nreg == 32 ? 1.0 : (nreg == 0 ? w_gen : w_mix);
-                rc = std::max(rc, wc);
+                rc = std::max(rc, nreg == 32 ? 1.0 : (nreg == 0 ? w_gen : w_mix));
+                all &= nreg == 32;
             }
-            pre[(size_t)st * (ny + 1) + j + 1] = pre[(size_t)st * (ny + 1) + j] + rc;
+            rcost[(size_t)st * ny + j] = rc;
+            rreg[(size_t)st * ny + j] = (uint8_t)(all && !no_allreg);
         }
-    }
-    auto seg_cost = [&](int st, int J0, int J1) {
-        const double* p = &pre[(size_t)st * (ny + 1)];
-        return p[J1] - p[J0] + WARM * (J0 > 0 ? (p[J0] - p[J0 - 1]) : 1.0);
-    };
-    int forced = 0;
-    if (const char* sv = getenv("STS_SEG")) forced = std::max(0, atoi(sv));   // test hook
-    double best = 1e300;
-    int best_seg = ny;
-    std::vector<std::pair<double, int>> ctas;
-    auto schedule = [&](int seg, bool keep) -> double {
-        const int nseg = (ny + seg - 1) / seg;
-        ctas.clear();
-        for (int g = 0; g < nseg; g++)
-            for (int st = 0; st < strips; st++)
-                ctas.push_back({seg_cost(st, g * seg, std::min(ny, (g + 1) * seg)), st + strips * g});
-        std::stable_sort(ctas.begin(), ctas.end(), [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
-            return a.first > b.first;
-        });
-        // greedy list scheduling onto the least-loaded slot (min-heap)
-        std::priority_queue<double, std::vector<double>, std::greater<double>> load;
-        for (size_t q = 0; q < std::min<size_t>(slots, ctas.size()); q++) load.push(0.0);
-        double makespan = 0.0;
-        for (auto& q : ctas) {
-            double l = load.top() + q.first;
-            load.pop();
-            load.push(l);
-            makespan = std::max(makespan, l);
-        }
-        (void)keep;
-        return makespan;
-    };
-    if (forced > 0) {
-        best_seg = forced;
-    } else {
-        // candidate heights 8, 10, ..., 32, 40, ... growing ~6 % per step (about
-        // 70 candidates); short segments fill the SMs on the paper's small meshes
-        // (4032 x 200: 33 strips) at the price of 3 warm-up rows each
-        for (int seg = std::max(1, std::min(ny, 8)); seg <= ny;
-             seg = seg < 32 ? seg + 2 : std::max(seg + 8, (int)(seg * 1.06))) {
-            const double ms = schedule(seg, false);
-            if (ms < best * (1.0 - 1e-3)) { best = ms; best_seg = seg; }
-        }
-    }
-    schedule(best_seg, true);
-    c->march_seg = best_seg;
-    c->march_nseg = (ny + best_seg - 1) / best_seg;
-    c->march_nstrips = strips;
-    // bit 30 of a launch-order entry: every point of the CTA's rows (warm-up rows
-    // included) and columns is regular, so the kernel runs the loop body compiled
-    // with the regular stage instances only (no per-point dispatch); a regular
-    // point runs the same instance either way
-    const bool no_allreg = getenv("STS_NO_ALLREG") != nullptr;   // test hook: every CTA takes the general loop
-    auto allreg = [&](int id, int seg) {
-        if (no_allreg) return false;
-        const int st = id % strips, g = id / strips;
-        const int J0 = g * seg, J1 = std::min(ny, J0 + seg);
-        if (J0 - WARM < 0) return false;
-        for (int j = J0 - WARM; j < J1; j++)
-            for (int t = 0; t < MX; t++) {
-                const int li = st * MW - 2 + t + OFF;
-                if (li < 0 || li >= c->pitch || !(packed[(size_t)j * c->pitch + li] & REG_BIT)) return false;
-            }
+    // row j can be in an all-regular CTA: rows j-WARM .. j all regular
+    auto R = [&](int st, int j) {
+        if (j < WARM) return false;
+        for (int q = j - WARM; q <= j; q++) if (!rreg[(size_t)st * ny + q]) return false;
         return true;
     };
-    // general CTAs first (longest first), then the all-regular ones: two kernels
-    std::vector<int> order, order_reg;
-    for (size_t q = 0; q < ctas.size(); q++) {
-        const bool ar = allreg(ctas[q].second, best_seg);
-        (ar ? order_reg : order).push_back(ctas[q].second | (ar ? ALLREG_BIT : 0));
+    auto cta_cost = [&](int st, int J0, int J1) {
+        double cst = 0.0;
+        for (int q = std::max(0, J0 - WARM); q < J1; q++) cst += rcost[(size_t)st * ny + q];
+        if (J0 - WARM < 0) cst += (WARM - J0) * rcost[(size_t)st * ny + 0];
+        return cst;
+    };
+    // the CTAs of one strip for heights (Hg, Hr)
+    auto cut = [&](int st, int Hg, int Hr, std::vector<CtaE>& out) {
+        int j = 0;
+        while (j < ny) {
+            const bool reg = R(st, j);
+            int e = j;
+            while (e < ny && R(st, e) == reg) e++;
+            const int len = e - j, H = reg ? Hr : Hg;
+            const int n = reg ? std::max(1, (len + H / 2) / H) : (len + H - 1) / H;
+            for (int q = 0; q < n; q++) {
+                const int a = j + (int)((long long)len * q / n), b = j + (int)((long long)len * (q + 1) / n);
+                out.push_back({st, a, b, reg ? ALLREG_BIT : 0, cta_cost(st, a, b) * (reg ? 1.0 : 1.0)});
+            }
+            j = e;
+        }
+    };
+    auto makespan = [&](std::vector<CtaE>& v) {
+        std::stable_sort(v.begin(), v.end(), [](const CtaE& x, const CtaE& y) { return x.cost > y.cost; });
+        std::priority_queue<double, std::vector<double>, std::greater<double>> load;
+        for (size_t q = 0; q < std::min<size_t>(slots, v.size()); q++) load.push(0.0);
+        double ms = 0.0;
+        for (auto& q : v) {
+            const double l = load.top() + q.cost;
+            load.pop();
+            load.push(l);
+            ms = std::max(ms, l);
+        }
+        return ms;
+    };
+    std::vector<CtaE> best, cur;
+    double best_ms = 1e300;
+    int best_hg = 8, best_hr = 8;
+    std::vector<int> hg_c, hr_c;
+    if (forced > 0) { hg_c = {forced}; hr_c = {forced}; }
+    else {
+        hg_c = {8, 12, 16, 24, 32, 48};
+        // Hr: 8, 10, ..., 32, then ~6 % steps
+        for (int h = std::min(ny, 8); h <= ny; h = h < 32 ? h + 2 : std::max(h + 8, (int)(h * 1.06))) hr_c.push_back(h);
+        if (hr_c.empty()) hr_c.push_back(std::max(1, ny));
     }
+    for (int hg : hg_c)
+        for (int hr : hr_c) {
+            cur.clear();
+            for (int st = 0; st < strips; st++) cut(st, hg, hr, cur);
+            const double ms = makespan(cur);
+            if (ms < best_ms * (1.0 - 1e-3)) { best_ms = ms; best = cur; best_hg = hg; best_hr = hr; }
+        }
+    c->march_seg = best_hr;
+    c->march_nstrips = strips;
+    // launch order: general CTAs (longest first), then the all-regular ones
+    auto upload = [&](int** dst, const std::vector<int4>& v) {
+        cudaFree(*dst);
+        *dst = nullptr;
+        cudaMalloc(dst, std::max<size_t>(1, v.size()) * sizeof(int4));
+        cudaMemcpy(*dst, v.data(), v.size() * sizeof(int4), cudaMemcpyHostToDevice);
+    };
+    std::vector<int4> order, order_reg;
+    for (auto& q : best) ((q.flags & ALLREG_BIT) ? order_reg : order).push_back(make_int4(q.strip, q.J0, q.J1, q.flags));
     c->n_gen = (int)order.size();
     c->n_reg = (int)order_reg.size();
     order.insert(order.end(), order_reg.begin(), order_reg.end());
-    if (getenv("STS_VERBOSE")) fprintf(stderr, "sts: seg %d, %zu CTAs, %d all-regular\n", best_seg, ctas.size(), c->n_reg);
-    cudaFree(c->cta_order);
-    c->cta_order = nullptr;
-    cudaMalloc(&c->cta_order, order.size() * sizeof(int));
-    cudaMemcpy(c->cta_order, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (getenv("STS_VERBOSE"))
+        fprintf(stderr, "sts: Hg %d Hr %d, %d general + %d all-regular CTAs, makespan %.0f\n", best_hg, best_hr,
+                c->n_gen, c->n_reg, best_ms);
+    upload(&c->cta_order, order);
     // Split order for the multi-GPU halo overlap: the CTAs of the edge strips
-    // (strip st, local first column I0 = st MW, reads local columns I0-4 ..
-    // I0+127 and writes I0 .. I0+124: an edge strip reads a ghost column or
-    // writes one of the 4 columns sent to a neighbour), then the interior ones
-    // in the longest-first order.  The edge strips get ~15 % shorter segments,
+    // (strip st reads local columns st MW .. st MW + 127 and writes st MW + 2 ..
+    // + 126: an edge strip reads a ghost column or writes one of the 4 columns
+    // sent to a neighbour), all run by the general kernel and cut ~15 % shorter
     // so that they finish early enough for the halo exchange to hide behind the
-    // interior strips of the next pass (the height never changes a bit).
+    // interior of the next pass; then the interior general and regular CTAs.
     auto edge = [&](int st) { const int I0 = st * MW; return I0 < OFF || I0 + MX >= c->nloc; };
-    c->edge_seg = std::max(8, std::min(best_seg, (int)(best_seg * 0.85)));
-    const int nseg_e = (ny + c->edge_seg - 1) / c->edge_seg;
-    std::vector<std::pair<double, int>> ectas;
-    for (int g = 0; g < nseg_e; g++)
-        for (int st = 0; st < strips; st++)
-            if (edge(st)) ectas.push_back({seg_cost(st, g * c->edge_seg, std::min(ny, (g + 1) * c->edge_seg)), st + strips * g});
-    std::stable_sort(ectas.begin(), ectas.end(), [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
-        return a.first > b.first;
-    });
-    std::vector<int> split, split_reg;
-    for (auto& q : ectas) split.push_back(q.second | (allreg(q.second, c->edge_seg) ? ALLREG_BIT : 0));
+    std::vector<CtaE> ev;
+    for (int st = 0; st < strips; st++)
+        if (edge(st)) cut(st, std::max(1, (int)(best_hg * 0.85)), std::max(1, std::min(best_hr, (int)(best_hr * 0.85))), ev);
+    std::stable_sort(ev.begin(), ev.end(), [](const CtaE& x, const CtaE& y) { return x.cost > y.cost; });
+    std::vector<int4> split, split_reg;
+    for (auto& q : ev) split.push_back(make_int4(q.strip, q.J0, q.J1, q.flags));
     c->n_edge = (int)split.size();
-    for (int o : order) {
-        if (edge((o & (ALLREG_BIT - 1)) % strips)) continue;
-        ((o & ALLREG_BIT) ? split_reg : split).push_back(o);
+    for (auto& q : order) {
+        if (edge(q.x)) continue;
+        ((q.w & ALLREG_BIT) ? split_reg : split).push_back(q);
     }
     c->n_split_gen = (int)split.size() - c->n_edge;
     split.insert(split.end(), split_reg.begin(), split_reg.end());
     c->n_split = (int)split.size();
-    cudaFree(c->cta_split);
-    c->cta_split = nullptr;
-    cudaMalloc(&c->cta_split, split.size() * sizeof(int));
-    cudaMemcpy(c->cta_split, split.data(), split.size() * sizeof(int), cudaMemcpyHostToDevice);
+    upload(&c->cta_split, split);
 }
-
 
 // One loop-2 pass of the march kernels over `order`: the n_gen general CTAs on
 // the context's high-priority stream beside the n_reg all-regular CTAs on st
@@ -528,8 +527,8 @@ static int launch_march(sts_ctx* c, const MarchParams& m, bool graph, cudaStream
     march_fn gen = graph ? march_graph_table(impl, tvd, 0) : march_table(impl, tvd, 0);
     march_fn reg = graph ? march_graph_table(impl, tvd, 1) : march_table(impl, tvd, 1);
     MarchParams mg = m, mr = m;
-    mg.order = order;
-    mr.order = order + n_gen;
+    mg.order = (const int4*)order;
+    mr.order = (const int4*)order + n_gen;
     if (n_gen > 0 && n_reg > 0) {
         cudaEventRecord(c->ev_fork, st);
         cudaStreamWaitEvent(c->gstream, c->ev_fork, 0);
@@ -833,11 +832,13 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
         ALLOC(ctx->halo, ctx->halo_elems);
     }
 #undef ALLOC
-    if (cudaMalloc(&ctx->red, (size_t)scheme->max_passes * 9 * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMallocHost(&ctx->h_red, 9 * sizeof(unsigned long long)) != cudaSuccess) {
+    if (cudaMalloc(&ctx->red, ((size_t)scheme->max_passes * 9 + 1) * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMallocHost(&ctx->h_red, 10 * sizeof(unsigned long long)) != cudaSuccess) {
         sts_destroy(ctx);
         return fail(nullptr, STS_E_OOM, "device allocation failed");
     }
+    ctx->bad = ctx->red + (size_t)scheme->max_passes * 9;
+    cudaMemset(ctx->bad, 0, sizeof(unsigned long long));
     {
         std::vector<uint32_t> packed(nve);
         for (size_t e = 0; e < nve; e++) {
@@ -1134,8 +1135,9 @@ extern "C" sts_status sts_profile_read(sts_ctx* ctx, double* out, int32_t reset)
     return STS_OK;
 }
 
-// residual slots -> stats (reading R35); returns STS_E_STATE on a bad state
-static sts_status finish_residuals(sts_ctx* ctx, const unsigned long long* r)
+// residual slots + sticky bad key -> stats (reading R35); returns STS_E_STATE
+// on a bad state (the first one of the advance call: pass, cell, field)
+static sts_status finish_residuals(sts_ctx* ctx, const unsigned long long* r, unsigned long long key)
 {
     double v[7];
     for (int q = 0; q < 7; q++) { long long b = (long long)r[q]; memcpy(&v[q], &b, 8); }
@@ -1144,11 +1146,18 @@ static sts_status finish_residuals(sts_ctx* ctx, const unsigned long long* r)
     ctx->stats.res[1] = vel > 0 ? v[1] / vel : v[1];
     ctx->stats.res[2] = pm > 0 ? v[2] / pm : v[2];
     ctx->stats.res[3] = Tm > 0 ? v[3] / Tm : v[3];
-    bool bad = r[7] != 0;
+    bool bad = key != 0;
     for (int q = 0; q < 7; q++) if (!(v[q] == v[q]) || std::isinf(v[q])) bad = true;
     if (bad) {
-        ctx->stats.bad_cell = r[7] ? (long long)(0x7fffffffffffffffULL - r[7]) : -1;
-        ctx->stats.bad_field = (int)r[8];
+        ctx->stats.bad_cell = -1;
+        ctx->stats.bad_field = STS_U;
+        ctx->stats.bad_pass = -1;
+        if (key) {
+            const long long flat = (long long)(((1ULL << 42) - 1) - ((key >> 2) & ((1ULL << 42) - 1)));
+            ctx->stats.bad_cell = flat == BAD_NOCELL ? -1 : flat;
+            ctx->stats.bad_field = (int)(key & 3);
+            ctx->stats.bad_pass = ctx->pass0 + (0xFFFFF - (long long)(key >> 44));
+        }
         return fail(ctx, STS_E_STATE, "non-finite or non-positive state (see sts_stats.bad_cell)");
     }
     return STS_OK;
@@ -1159,17 +1168,19 @@ static sts_status finish_residuals(sts_ctx* ctx, const unsigned long long* r)
 static sts_status gather_red(sts_ctx** cs, int n, int it, unsigned long long* out, cudaStream_t st)
 {
     sts_ctx* ctx = cs[0];
-    for (int q = 0; q < 9; q++) out[q] = 0;
+    for (int q = 0; q < 10; q++) out[q] = 0;
     if (n == 1 && ctx->comm) {
         unsigned long long* slot = ctx->red + (size_t)it * 9;
         if (g_nccl.AllReduce(slot, slot, 9, NCCL_UINT64, NCCL_MAX, ctx->comm, st)) return fail(ctx, STS_E_COMM, "ncclAllReduce");
+        if (g_nccl.AllReduce(ctx->bad, ctx->bad, 1, NCCL_UINT64, NCCL_MAX, ctx->comm, st)) return fail(ctx, STS_E_COMM, "ncclAllReduce");
     }
     for (int r = 0; r < n; r++) {
         CU(cudaMemcpyAsync(cs[r]->h_red, cs[r]->red + (size_t)it * 9, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(cs[r]->h_red + 9, cs[r]->bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     }
     CU(cudaStreamSynchronize(st));
     for (int r = 0; r < n; r++)
-        for (int q = 0; q < 9; q++) out[q] = std::max(out[q], cs[r]->h_red[q]);
+        for (int q = 0; q < 10; q++) out[q] = std::max(out[q], cs[r]->h_red[q]);
     return STS_OK;
 }
 
@@ -1188,6 +1199,7 @@ static sts_status gather_red(sts_ctx** cs, int n, int it, unsigned long long* ou
 struct LoopState {
     int passes, done, conv, checked;
     unsigned long long red[9];   // residual slots of the last checked pass
+    unsigned long long bad;      // sticky bad-state key (the march kernels' MarchParams.bad)
 };
 
 __global__ void loop_check_kernel(unsigned long long* slot, LoopState* ls, cudaGraphConditionalHandle h,
@@ -1198,9 +1210,10 @@ __global__ void loop_check_kernel(unsigned long long* slot, LoopState* ls, cudaG
     const int passes = ls->passes + 1;
     ls->passes = passes;
     bool done = passes >= max_passes;
-    if (passes >= min_passes) {
+    const bool bad_state = *(volatile unsigned long long*)&ls->bad != 0;
+    if (passes >= min_passes || bad_state) {
         double v[7];
-        bool bad = slot[7] != 0;
+        bool bad = bad_state;
         for (int q = 0; q < 7; q++) {
             v[q] = __longlong_as_double((long long)slot[q]);
             if (!(v[q] == v[q]) || isinf(v[q])) bad = true;
@@ -1244,7 +1257,7 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
     Params k = make_params(c);
     k.u_1 = c->snap[n1].u; k.v_1 = c->snap[n1].v; k.p_1 = c->snap[n1].p; k.T_1 = c->snap[n1].T;
     k.ue = c->ue; k.ve = c->ve; k.Te = c->Te;
-    const dim3 mgrid(c->march_nstrips * c->march_nseg);
+    const dim3 mgrid(c->n_gen + c->n_reg);                 // the conv kernel: every CTA of the schedule
     auto pass = [&](int o, int w, int sl, cudaStream_t s) -> cudaError_t {
         Params q = k;
         q.u_o = c->snap[o].u; q.v_o = c->snap[o].v; q.p_o = c->snap[o].p; q.T_o = c->snap[o].T;
@@ -1252,6 +1265,7 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
         q.red = c->red2 + sl * 9;
         MarchParams m = make_march(c, q);
         m.done = &c->d_ls->done;
+        m.bad = &c->d_ls->bad;
         // the general and the all-regular kernel as two parallel kernel nodes after
         // the capture's current dependencies (no cross-stream fork inside a
         // conditional body)
@@ -1268,7 +1282,7 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
             const int cnt = part == 0 ? c->n_gen : c->n_reg;
             if (cnt == 0) continue;
             MarchParams mp = m;
-            mp.order = c->cta_order + (part ? c->n_gen : 0);
+            mp.order = (const int4*)c->cta_order + (part ? c->n_gen : 0);
             void* args[] = {&mp};
             cudaKernelNodeParams kp = {};
             kp.func = (void*)march_graph_table(impl, tvd, part);
@@ -1353,7 +1367,8 @@ static sts_status graph_step(sts_ctx* ctx, bool* conv)
     c->cur = (ls.passes & 1) ? a : b;             // pass 1 writes a, pass 2 b, ...
     *conv = ls.conv != 0;
     if (ls.checked) {
-        sts_status e = finish_residuals(c, ls.red);
+        c->pass0 = c->stats.passes_done + ls.passes - 1;   // graph passes carry pass key 0xFFFFF
+        sts_status e = finish_residuals(c, ls.red, ls.bad);
         if (e) return e;
     }
     c->stats.steps_done++;
@@ -1382,7 +1397,12 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
     sts_status status = STS_OK;
     int last_it = -1;
     std::vector<int> n1(n), a(n), b(n), old(n), nw(n), which(n);
-    unsigned long long red[9];
+    unsigned long long red[10];
+    for (int r = 0; r < n; r++) {                    // a new advance call: clear the sticky bad state
+        cs[r]->pass0 = cs[r]->stats.passes_done;
+        CU(cudaMemsetAsync(cs[r]->bad, 0, sizeof(unsigned long long), st));
+    }
+    long long prel = 0;                               // pass index within this advance call
     if (n == 1 && tol_graph_ok(ctx)) {
         for (int step = 0; step < n_steps; step++) {
             bool conv = false;
@@ -1414,7 +1434,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 Params k = base(c, r);
                 k.ue_w = c->ue; k.ve_w = c->ve; k.Te_w = c->Te;
                 prof_begin(c, 1);
-                const dim3 mgrid(c->march_nstrips * c->march_nseg);
+                const dim3 mgrid(c->n_gen + c->n_reg);                 // the conv kernel: every CTA of the schedule
                 conv_march_table(tvd)<<<mgrid, MX, sizeof(ConvSmem), st>>>(make_march(c, k));
                 prof_end(c);
                 c->launches++;
@@ -1453,17 +1473,19 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 k.u_o = c->snap[old[r]].u; k.v_o = c->snap[old[r]].v; k.p_o = c->snap[old[r]].p; k.T_o = c->snap[old[r]].T;
                 k.u_w = c->snap[nw[r]].u; k.v_w = c->snap[nw[r]].v; k.p_w = c->snap[nw[r]].p; k.T_w = c->snap[nw[r]].T;
                 k.red = c->red + (size_t)it * 9;
+                const int pkey = 0xFFFFF - (int)std::min<long long>(prel, 0xFFFFE);
                 if (split) {
-                    MarchParams ma = make_march(c, k), mb = ma;
-                    ma.order = c->cta_split;
-                    ma.seg = c->edge_seg;
+                    MarchParams ma = make_march(c, k);
+                    ma.pass_key = pkey;
+                    MarchParams mb = ma;
+                    ma.order = (const int4*)c->cta_split;
                     cudaStream_t as = overlap ? c->hstream : st;
                     if (overlap && it > 0) CU(cudaStreamWaitEvent(as, c->ev_b, 0));   // pass it-1 complete
                     prof_begin(c, 0);
                     march_fn gen = gk ? march_graph_table(impl, tvd, 0) : march_table(impl, tvd, 0);
                     gen<<<c->n_edge, MX, sizeof(MarchSmem), as>>>(ma);
                     if (overlap) CU(cudaEventRecord(c->ev_a[it & 1], as));
-                    c->launches += 1 + launch_march(c, mb, gk, st, c->cta_split + c->n_edge, c->n_split_gen,
+                    c->launches += 1 + launch_march(c, mb, gk, st, c->cta_split + 4 * c->n_edge, c->n_split_gen,
                                                     c->n_split - c->n_edge - c->n_split_gen);
                     if (overlap) {
                         CU(cudaStreamWaitEvent(st, c->ev_a[it & 1], 0));   // the pass ends with both sets
@@ -1479,6 +1501,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 } else {
                     prof_begin(c, 0);
                     MarchParams mk = make_march(c, k);
+                    mk.pass_key = pkey;
                     if (gk) mk.done = &c->d_ls->done;
                     c->launches += launch_march(c, mk, gk, st, c->cta_order, c->n_gen, c->n_reg);
                     prof_end(c);
@@ -1491,6 +1514,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 if (e) return e;
             }
             passes++;
+            prel++;
             last_it = it;
             for (int r = 0; r < n; r++) { old[r] = nw[r]; nw[r] = (nw[r] == a[r]) ? b[r] : a[r]; }
             if (tolmode && passes >= ctx->sch.min_passes) {
@@ -1501,7 +1525,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 sts_status e = gather_red(cs, n, it, red, st);
                 if (e) return e;
                 for (int r = 0; r < n; r++) cs[r]->cur = old[r];
-                e = finish_residuals(ctx, red);
+                e = finish_residuals(ctx, red, red[9]);
                 for (int r = 1; r < n; r++) { cs[r]->stats = ctx->stats; }
                 if (e) return e;
                 const double* rs = ctx->stats.res;
@@ -1524,7 +1548,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
     if (last_it >= 0 && !tolmode) {
         sts_status e = gather_red(cs, n, last_it, red, st);
         if (e) return e;
-        e = finish_residuals(ctx, red);
+        e = finish_residuals(ctx, red, red[9]);
         for (int r = 1; r < n; r++) { cs[r]->stats.res[0] = ctx->stats.res[0]; cs[r]->stats.res[1] = ctx->stats.res[1];
                                       cs[r]->stats.res[2] = ctx->stats.res[2]; cs[r]->stats.res[3] = ctx->stats.res[3]; }
         if (e) { if (out) *out = ctx->stats; return e; }

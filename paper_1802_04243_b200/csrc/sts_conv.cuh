@@ -39,10 +39,9 @@ __global__ void __launch_bounds__(MX, 5) conv_march_kernel(MarchParams m)
     ConvSmem& s = *reinterpret_cast<ConvSmem*>(smem_raw);
     const Params& k = m.k;
     const int t = threadIdx.x;
-    const int ow = m.order[blockIdx.x];
-    const int cta = ow & (ALLREG_BIT - 1);
-    const bool allreg = (ow & ALLREG_BIT) != 0;
-    const int strip = cta % m.nstrips, segi = cta / m.nstrips;
+    const int4 ce = m.order[blockIdx.x];
+    const bool allreg = (ce.w & ALLREG_BIT) != 0;
+    const int strip = ce.x;
     const int I0 = k.gi0 + strip * MW;
     // ring rows by TMA as in march_kernel: ring column 0 = stored column c0 (a multiple of 4)
     const int wbase = I0 - 4 - k.gi0 + OFF;
@@ -56,8 +55,7 @@ __global__ void __launch_bounds__(MX, 5) conv_march_kernel(MarchParams m)
     }
     __syncthreads();
     const int gi = I0 - 2 + t;
-    const int J0 = segi * m.seg;
-    const int J1 = min(J0 + m.seg, k.ny);
+    const int J0 = ce.y, J1 = ce.z;
     const int js = J0 - 2;                              // 2 warm-up rows (carried TY, uY, vY, fluxes)
     const bool owner = t >= 2 && t < 2 + MW && gi < k.gi0 + k.nloc;
     const double dx = k.dx, dy = k.dy;

@@ -44,20 +44,20 @@ constexpr int WARM = 3;          // warm-up rows per segment: the longest carrie
                                  // E(J0) <- D(J0-1) <- C(J0-2) <- A(J0-3); 2 rows fail the bitwise
                                  // segmentation tests, 3 pass them for every variant down to 1-row segments
 constexpr uint32_t REG_BIT = 1u << 24;   // kind-word bit: the +-3 window is all fluid
-constexpr int ALLREG_BIT = 1 << 30;      // launch-order bit: every point of the CTA is regular (conv kernel)
+constexpr int ALLREG_BIT = 1;            // launch-order flag (int4 .w): every point of the CTA is regular
 
 struct MarchParams {
     Params k;                    // v1 parameter block (pointers, constants)
     const uint32_t* kind;        // packed kinds: ck | uk << 8 | vk << 16 | regular << 24, (ny+1) x pitch
-    int seg;                     // rows per segment
-    int nstrips;                 // strips per row of CTAs
-    const int* order;            // CTA schedule (longest first); blockIdx.x -> strip + nstrips * segment
+    const int4* order;           // CTA schedule: blockIdx.x -> {strip, first row J0, end row J1, flags}
     double inv_dx, inv_dy, CT1_dydx, CT1_dxdy, B_dydx, B_dxdy, c_t, dV, A_dy, A_dx, half_dV;
     double B43_dydx, B43_dxdy;   // 4/3 B dy/dx, 4/3 B dx/dy (normal viscous links)
     double q_dx, q_dy;           // 1/(4 dx), 1/(4 dy) (bilinear differences in S^T_c)
     double h_dx, h_dy, inv_dt;   // 1/(2 dx), 1/(2 dy), 1/dt (pressure work, R9)
     double pw_a;                 // C^T3 for the C^T3 Dp/Dt form of R9, else 0
     const int* done;             // graph-driven loop 2 (tolerance mode): loop finished -> the pass is a no-op
+    unsigned long long* bad;     // sticky first-bad-state key of the advance call (bad_key)
+    int pass_key;                // 0xFFFFF - pass index within the advance call
 };
 
 // fp64 reciprocal: MUFU.RCP64H seed (relative error <= 2^-19.9, measured) and
@@ -706,6 +706,15 @@ __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int 
 }
 
 struct Resid { double du, dv, dp, dT, vel, p, T; long long bad; int badf; bool nanv; };
+// Sticky bad-state key: bits 63..44 = 0xFFFFF - pass index (earliest pass wins
+// the max), 43..2 = 2^42 - 1 - flat cell index j nx + i (lowest cell wins),
+// 1..0 = field (sts_field: 0 u, 1 v, 2 p, 3 T).  BAD_NOCELL: a NaN velocity.
+constexpr long long BAD_NOCELL = (1LL << 42) - 2;
+__host__ __device__ __forceinline__ unsigned long long bad_key(int pass_key, long long flat, int field)
+{
+    return ((unsigned long long)pass_key << 44) | ((((1ULL << 42) - 1) - (unsigned long long)flat) << 2) |
+           (unsigned long long)(field & 3);
+}
 
 // ================= stage E: corrections, writes, residuals =================
 template <bool IMPL, bool TVD, bool REG>
@@ -776,10 +785,10 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     MarchSmem& s = *reinterpret_cast<MarchSmem*>(smem_raw);
     const Params& k = m.k;
     if (GRAPH && *(volatile const int*)m.done) return;  // converged earlier in this graph launch (CTA-uniform)
+    if (*(volatile const unsigned long long*)m.bad) return;   // a bad state earlier in this advance call
     const int t = threadIdx.x;
-    const int ow = m.order[blockIdx.x];
-    const int cta = ow & (ALLREG_BIT - 1);
-    const int strip = cta % m.nstrips, segi = cta / m.nstrips;
+    const int4 ce = m.order[blockIdx.x];
+    const int strip = ce.x;
     const int I0 = k.gi0 + strip * MW;                  // first owned column of the strip
     // ring column 0 = stored column c0 (a multiple of 4: 16-byte aligned TMA rows); this
     // thread's column sits at ring column lc
@@ -794,8 +803,7 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     }
     __syncthreads();
     const int gi = I0 - 2 + t;                          // this thread's global column
-    const int J0 = segi * m.seg;
-    const int J1 = min(J0 + m.seg, k.ny);
+    const int J0 = ce.y, J1 = ce.z;
     const int js = J0 - WARM;
     const bool col_stored = stored_col(k, gi);
     const bool owner = t >= 2 && t < 2 + MW && gi < k.gi0 + k.nloc;
@@ -873,9 +881,12 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
         for (int w = 0; w < MX / 32; w++) val = nmax(val, part[w][threadIdx.x]);
         atomicMax(&k.red[threadIdx.x], (unsigned long long)__double_as_longlong(val));
     }
-    if (rs.bad >= 0) {
-        atomicMax(&k.red[7], 0x7fffffffffffffffULL - (unsigned long long)rs.bad);
-        k.red[8] = (unsigned long long)rs.badf;
+    // first bad state of the advance call, sticky: one u64 key per context,
+    // (earliest pass, then lowest cell, field) ordered so that one atomicMax
+    // (and one NCCL MAX allreduce) keeps it; later passes see it and exit
+    if (rs.bad >= 0 || rs.nanv) {
+        const long long flat = rs.bad >= 0 ? rs.bad : BAD_NOCELL;
+        atomicMax(m.bad, bad_key(m.pass_key, flat, rs.bad >= 0 ? rs.badf : 0));
     }
 }
 

@@ -72,7 +72,8 @@ class sts_plan_info(ctypes.Structure):
 
 class sts_stats(ctypes.Structure):
     _fields_ = [("steps_done", ctypes.c_int64), ("passes_done", ctypes.c_int64), ("res", ctypes.c_double * 4),
-                ("converged", ctypes.c_int32), ("bad_field", ctypes.c_int32), ("bad_cell", ctypes.c_int64)]
+                ("converged", ctypes.c_int32), ("bad_field", ctypes.c_int32), ("bad_cell", ctypes.c_int64),
+                ("bad_pass", ctypes.c_int64)]
 
 
 _lib = None
@@ -273,7 +274,8 @@ class Solver:
         if check:
             _check(st, self._h)
         return st, {"steps_done": s.steps_done, "passes_done": s.passes_done, "res": list(s.res),
-                    "converged": s.converged, "bad_cell": s.bad_cell, "bad_field": s.bad_field}
+                    "converged": s.converged, "bad_cell": s.bad_cell, "bad_field": s.bad_field,
+                    "bad_pass": s.bad_pass}
 
     def constants(self):
         out = (ctypes.c_double * 7)()

@@ -119,15 +119,24 @@ def test_constants_match(S, oracle_mod):
 
 
 def test_bad_state_reported(S):
-    """A non-positive temperature is reported as STS_E_STATE with the cell index."""
+    """A non-positive temperature is reported as STS_E_STATE with the FIRST bad
+    state of the call (sticky device key): its cell, field and pass -- the first
+    pass of the first of 3 steps -- and the later passes do no work."""
     case = W.c1_small("implicit_upwind", passes=2)
     g = S.Solver(case)
     T = g.get_field("T")
     T[5, 3] = -1.0
     g.set_field("T", T)
-    st, stats = g.advance(1, check=False)
+    st, stats = g.advance(3, check=False)
     assert st == S.STS_E_STATE
-    assert stats["bad_cell"] >= 0
+    # the lowest bad cell of the first pass: (3, 5) or a neighbour it poisoned
+    bj, bi = divmod(stats["bad_cell"], case["nx"])
+    assert abs(bi - 3) <= 1 and abs(bj - 5) <= 1, stats
+    assert stats["bad_field"] in (2, 3) and stats["bad_pass"] == 0, stats
+    # a fresh call on a healthy state is clean again
+    g.init_freestream()
+    st, stats = g.advance(1, check=False)
+    assert st == 0
 
 
 def test_tolerance_mode_converges(S, oracle_mod):
