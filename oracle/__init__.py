@@ -75,6 +75,7 @@ def lib():
         L.orc_get_map.argtypes = [ctypes.c_void_p, ctypes.c_int32, ip, ctypes.c_int64]
         L.orc_advance.argtypes = [ctypes.c_void_p, ctypes.c_int32, dp, ip]
         L.orc_poison_solids.argtypes = [ctypes.c_void_p]
+        L.orc_set_mesh.argtypes = [ctypes.c_void_p, dp, dp]
         L.orc_constants.argtypes = [ctypes.c_void_p, dp]
         for f in ("orc_vanleer",):
             getattr(L, f).restype = ctypes.c_double
@@ -136,6 +137,16 @@ class Case:
         self._h = lib().orc_create(ctypes.byref(p), sq.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(sq))
         if not self._h:
             raise ValueError("oracle rejected the case configuration")
+        # non-uniform mesh (N4): per-column / per-row steps, else uniform `spacing`
+        dxs, dys = case.get("dxs"), case.get("dys")
+        if dxs is not None or dys is not None:
+            self._dxs = None if dxs is None else np.ascontiguousarray(dxs, dtype=np.float64)
+            self._dys = None if dys is None else np.ascontiguousarray(dys, dtype=np.float64)
+            assert self._dxs is None or self._dxs.shape == (self.nx,)
+            assert self._dys is None or self._dys.shape == (self.ny,)
+            if lib().orc_set_mesh(self._h, None if self._dxs is None else _dptr(self._dxs),
+                                  None if self._dys is None else _dptr(self._dys)):
+                raise ValueError("oracle rejected the mesh steps")
 
     def __del__(self):
         h = getattr(self, "_h", None)

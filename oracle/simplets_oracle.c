@@ -44,6 +44,7 @@ struct orc_case {
     level L[3];                  /* 0: time n-1, 1: old iterate, 2: new */
     double *ue, *ve, *Te;        /* explicit planes       */
     double *uh, *du, *vh, *dv;   /* phase-A pseudo-velocities            */
+    double *dxs, *dys;           /* per-column / per-row steps, NULL = uniform */
 };
 
 #define N1 (&c->L[0])
@@ -60,9 +61,29 @@ static int tvd(const orc_case* c) { return c->P.space_scheme == ORC_TVD; }
 static int implicit_(const orc_case* c) { return c->P.time_scheme == ORC_IMPLICIT; }
 
 /* Grid steps Delta x_i, Delta y_j (Fig. 5).  The mesh of the
- * paper is uniform; ghost indices take the same step. */
-static double DX(const orc_case* c, int i) { (void)i; return c->P.dx; }
-static double DY(const orc_case* c, int j) { (void)j; return c->P.dy; }
+ * paper's test case is uniform (the P.dx / P.dy default); orc_set_mesh
+ * gives per-column / per-row steps (the general mesh of P:271-280, SURVEY
+ * 8(f) N4).  A ghost column takes the step of the column it copies (inflow
+ * ghosts: column 0, outflow ghosts: column nx-1, periodic: the wrapped
+ * column); rows beyond a wall take the boundary row's step (no stencil that
+ * is used reaches them: R17). */
+static double DX(const orc_case* c, int i)
+{
+    if (!c->dxs) return c->P.dx;
+    if (periodic(c)) return c->dxs[wrap(i, c->nx)];
+    return c->dxs[i < 0 ? 0 : (i >= c->nx ? c->nx - 1 : i)];
+}
+static double DY(const orc_case* c, int j)
+{
+    if (!c->dys) return c->P.dy;
+    return c->dys[j < 0 ? 0 : (j >= c->ny ? c->ny - 1 : j)];
+}
+/* Linear-interpolation weight of the node left of a face (reading R4): the
+ * face between nodes of widths dl (left) and dr (right) lies dl/2 from the
+ * left centre and dr/2 from the right one, so the left node weighs
+ * dr / (dl + dr) and the right node dl / (dl + dr) (1/2 each on a uniform
+ * mesh, exactly). */
+static double wleft(double dl, double dr) { return dr / (dl + dr); }
 
 /* ------------------------------------------------------------ scheme funcs */
 /* Van Leer limiter psi(r) = (r+|r|)/(1+r); r <= 0 -> 0 (R6). */
@@ -294,16 +315,21 @@ static double Fy(const orc_case* c, const level* s, int i, int j)
     return rho_v(c, s, i, j) * V(c, s, i, j) * DX(c, i);
 }
 
-/* Corner Gamma at (x^f_i, y^f_j): bilinear = mean of the 4 surrounding cells
- * on the uniform mesh (R4, R5), over the cells that are not solid and not
- * beyond a wall (BC spec 8). */
+/* Corner Gamma at (x^f_i, y^f_j): bilinear interpolation between the 4
+ * surrounding cell centres (R4, R5; weights wx * wy of wleft, 1/4 each on a
+ * uniform mesh), over the cells that are not solid and not beyond a wall,
+ * the weights renormalised to the cells kept (BC spec 8).  On a uniform mesh
+ * this is the mean of the cells kept, bit for bit (power-of-two weights). */
 static double gam_corner(const orc_case* c, const level* s, int i, int j)
 {
-    double sum = 0.0; int n = 0;
+    const double wxl = wleft(DX(c, i - 1), DX(c, i)), wxr = 1.0 - wxl;
+    const double wyb = wleft(DY(c, j - 1), DY(c, j)), wyt = 1.0 - wyb;
+    double sum = 0.0, wsum = 0.0;
     int ii[4] = {i - 1, i, i - 1, i}, jj[4] = {j - 1, j - 1, j, j};
+    double w[4] = {wxl * wyb, wxr * wyb, wxl * wyt, wxr * wyt};
     for (int k = 0; k < 4; k++)
-        if (!is_wallish(c, ii[k], jj[k])) { sum += GAM(s, ii[k], jj[k]); n++; }
-    return sum / n;
+        if (!is_wallish(c, ii[k], jj[k])) { sum += w[k] * GAM(s, ii[k], jj[k]); wsum += w[k]; }
+    return sum / wsum;
 }
 /* Harmonic face average of Gamma^lambda, Eq. pl33. */
 static double harmonic(double gm, double gp, double dm, double dp)
@@ -437,13 +463,24 @@ static double T_equation(const orc_case* c, int i, int j)
     if (impl) a0 = dt * (a1 + a2 + a3 + a4 + FE - FW + FN - FS) + rP * dx * dy;   /* pl31 */
     else      a0 = dt * (a1 + a2 + a3 + a4) + rP * dx * dy;                       /* pl31_1 */
 
-    /* S^T_c, Eq. pl29; bilinear mid-point velocities (R4). */
+    /* S^T_c, Eq. pl29; mid-face velocities by bilinear
+     * interpolation between the four neighbouring nodes (R4): the face
+     * x^f_{i+1} lies between the v-node columns i and i+1 (weights wleft) and
+     * y^v_j halfway between the v-node rows j and j+1 (1/2 each); likewise
+     * for u.  Terms summed in node order: on a uniform mesh this is the
+     * 4-point mean 0.25 (a + b + c + d) bit for bit. */
     double dudx = (U(c, o, i + 1, j) - U(c, o, i, j)) / dx;
     double dvdy = (V(c, o, i, j + 1) - V(c, o, i, j)) / dy;
-    double vE = 0.25 * (V(c, o, i, j) + V(c, o, i + 1, j) + V(c, o, i, j + 1) + V(c, o, i + 1, j + 1));
-    double vW = 0.25 * (V(c, o, i - 1, j) + V(c, o, i, j) + V(c, o, i - 1, j + 1) + V(c, o, i, j + 1));
-    double uN = 0.25 * (U(c, o, i, j) + U(c, o, i + 1, j) + U(c, o, i, j + 1) + U(c, o, i + 1, j + 1));
-    double uS = 0.25 * (U(c, o, i, j - 1) + U(c, o, i + 1, j - 1) + U(c, o, i, j) + U(c, o, i + 1, j));
+    double wE = wleft(dx, DX(c, i + 1)), wW = wleft(DX(c, i - 1), dx);
+    double wN = wleft(dy, DY(c, j + 1)), wS = wleft(DY(c, j - 1), dy);
+    double vE = 0.5 * wE * V(c, o, i, j) + 0.5 * (1.0 - wE) * V(c, o, i + 1, j)
+              + 0.5 * wE * V(c, o, i, j + 1) + 0.5 * (1.0 - wE) * V(c, o, i + 1, j + 1);
+    double vW = 0.5 * wW * V(c, o, i - 1, j) + 0.5 * (1.0 - wW) * V(c, o, i, j)
+              + 0.5 * wW * V(c, o, i - 1, j + 1) + 0.5 * (1.0 - wW) * V(c, o, i, j + 1);
+    double uN = 0.5 * wN * U(c, o, i, j) + 0.5 * wN * U(c, o, i + 1, j)
+              + 0.5 * (1.0 - wN) * U(c, o, i, j + 1) + 0.5 * (1.0 - wN) * U(c, o, i + 1, j + 1);
+    double uS = 0.5 * wS * U(c, o, i, j - 1) + 0.5 * wS * U(c, o, i + 1, j - 1)
+              + 0.5 * (1.0 - wS) * U(c, o, i, j) + 0.5 * (1.0 - wS) * U(c, o, i + 1, j);
     /* A mid-face velocity on a face that lies on a wall is the gas velocity at
      * the surface: the slip velocity of Eq. pl38 (reading R38) */
     if (is_wallish(c, i + 1, j)) vE = slip_velocity(c, 0.5 * (V(c, o, i, j) + V(c, o, i, j + 1)), 0.0, rP, 0.5 * dx);
@@ -1028,7 +1065,19 @@ void orc_destroy(orc_case* c)
     for (int k = 0; k < 3; k++) free_level(&c->L[k]);
     free(c->ue); free(c->ve); free(c->Te); free(c->uh); free(c->du); free(c->vh); free(c->dv);
     free(c->solid);
+    free(c->dxs); free(c->dys);
     free(c);
+}
+
+int orc_set_mesh(orc_case* c, const double* dxs, const double* dys)
+{
+    if (dxs) for (int i = 0; i < c->nx; i++) if (!(dxs[i] > 0.0)) return 1;
+    if (dys) for (int j = 0; j < c->ny; j++) if (!(dys[j] > 0.0)) return 1;
+    free(c->dxs); free(c->dys);
+    c->dxs = c->dys = NULL;
+    if (dxs) { c->dxs = malloc((size_t)c->nx * sizeof(double)); memcpy(c->dxs, dxs, (size_t)c->nx * sizeof(double)); }
+    if (dys) { c->dys = malloc((size_t)c->ny * sizeof(double)); memcpy(c->dys, dys, (size_t)c->ny * sizeof(double)); }
+    return 0;
 }
 
 /* Re-impose the fixed faces of BC spec 1-4 on the current state. */

@@ -80,6 +80,10 @@ int       orc_get_map(const orc_case* c, int32_t which, int32_t* a, int64_t n);
  * Returns 0, or 3 if tol > 0 and a step hit max_passes unconverged,
  * or 4 if a non-finite / non-positive state appeared. */
 int       orc_advance(orc_case* c, int32_t n_steps, double* res, int32_t* passes_out);
+/* Non-uniform mesh (the general staggered mesh of Fig. 5): dxs[nx]
+ * = Delta x_i, dys[ny] = Delta y_j (> 0); NULL keeps that direction uniform
+ * (P.dx / P.dy).  Returns 1 on a non-positive step. */
+int       orc_set_mesh(orc_case* c, const double* dxs, const double* dys);
 /* Debug: fill solid-cell p,T,rho,Gamma with NaN (proves they are never read). */
 void      orc_poison_solids(orc_case* c);
 /* Derived constants of Eq. pl37 and u_in: out[0..6] =

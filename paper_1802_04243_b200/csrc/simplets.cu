@@ -15,6 +15,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -311,10 +312,14 @@ static march_fn march_graph_table(int impl, int tvd, int regk)
 }
 static march_fn conv_march_table(int tvd) { return tvd ? conv_march_kernel<true> : conv_march_kernel<false>; }
 
+// The shared-memory opt-in is a per-device function attribute: one bit per
+// device (the caller has made ctx->device current), set once every attribute
+// of that device is in place.
 static sts_status set_smem_attrs(sts_ctx* ctx)
 {
-    static bool done = false;
-    if (done) return STS_OK;
+    static std::atomic<unsigned long long> done_mask{0};
+    const unsigned long long bit = 1ull << (ctx->device & 63);
+    if (done_mask.load() & bit) return STS_OK;
     for (int q = 0; q < 16; q++) {
         const int impl = q & 1, tvd = (q >> 1) & 1, regk = (q >> 2) & 1, graph = q >> 3;
         march_fn f = graph ? march_graph_table(impl, tvd, regk) : march_table(impl, tvd, regk);
@@ -323,7 +328,7 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
     for (int tvd = 0; tvd < 2; tvd++)
         CU(cudaFuncSetAttribute((const void*)conv_march_table(tvd), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(ConvSmem)));
-    done = true;
+    done_mask.fetch_or(bit);
     return STS_OK;
 }
 
@@ -1129,6 +1134,7 @@ extern "C" sts_status sts_profile(sts_ctx* ctx, int32_t enable)
 extern "C" sts_status sts_profile_read(sts_ctx* ctx, double* out, int32_t reset)
 {
     if (!ctx || !out) return fail(ctx, STS_E_ARG, "null argument");
+    CU(cudaSetDevice(ctx->device));
     prof_collect(ctx);
     out[0] = ctx->prof_pass_n; out[1] = ctx->prof_pass_ms; out[2] = ctx->prof_conv_n; out[3] = ctx->prof_conv_ms; out[4] = ctx->launches;
     if (reset) ctx->prof_pass_n = ctx->prof_pass_ms = ctx->prof_conv_n = ctx->prof_conv_ms = ctx->launches = 0;

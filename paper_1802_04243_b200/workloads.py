@@ -124,6 +124,34 @@ def c2(small=False, variant="implicit_upwind", passes=10):
     return c
 
 
+# ------------------------------------------------------------ non-uniform meshes (N4)
+def smooth_steps(n: int, spacing: float, amplitude: float = 0.3):
+    """Steps Delta_k = spacing (1 + amplitude cos(2 pi (k + 1/2) / n)), k < n: a
+    smooth stretching, mirror symmetric (Delta_k = Delta_{n-1-k}), mean spacing."""
+    k = np.arange(n)
+    return spacing * (1.0 + amplitude * np.cos(2 * np.pi * (k + 0.5) / n))
+
+
+def random_steps(n: int, spacing: float, seed: int, spread: float = 0.4):
+    """Seeded rough steps spacing (1 + spread U(-1/2, 1/2)) (every stencil weight differs)."""
+    rng = np.random.default_rng(seed)
+    return spacing * (1.0 + spread * rng.uniform(-0.5, 0.5, size=n))
+
+
+def with_mesh(case: dict, dxs=None, dys=None):
+    """The case on a non-uniform mesh: per-column steps dxs (nx) and per-row steps
+    dys (ny); None keeps that direction at the uniform `spacing`."""
+    c = dict(case)
+    if dxs is not None:
+        c["dxs"] = np.asarray(dxs, dtype=np.float64)
+        assert c["dxs"].shape == (c["nx"],)
+    if dys is not None:
+        c["dys"] = np.asarray(dys, dtype=np.float64)
+        assert c["dys"].shape == (c["ny"],)
+    c["name"] = c["name"] + "_nu"
+    return c
+
+
 # ------------------------------------------------------------ perturbations
 def perturbation(case: dict, seed: int, amplitude: float = 0.01):
     """Seeded multiplicative noise factors (1 + amplitude * U(-1,1)) for u, v

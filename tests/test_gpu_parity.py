@@ -75,17 +75,32 @@ def test_parity_c1(S, oracle_mod, variant):
     """BASELINE configs[0] at its stated length: C1 (120 x 40, Delta = 0.25,
     supersonic past one square), 200 steps x 10 passes from the free stream, every
     variant (explicit TVD at dt = 0.05 Delta, R39).  Implicit TVD's loop 2 does not
-    converge here (limiter switching, DESIGN 9), yet GPU and oracle stay within
-    1e-11 over the 2000 passes (tools/drift.py)."""
+    converge here (the limiter switches between passes, DESIGN 9), so the method
+    amplifies any rounding-level difference: two ORACLE runs whose T differs by one
+    ulp differ by 3e-12 after 40 steps and 8e-7 after 200.  For that variant the
+    1e-9 bar is tested at 40 steps, and at 200 steps the GPU-vs-oracle difference
+    must stay within the oracle's own one-ulp sensitivity (reading R40)."""
     case = W.c1(variant, passes=10)
-    steps = 200
     g = S.Solver(case)
     o = oracle_mod.Case(case)
-    g.advance(steps)
-    assert o.advance(steps)[0] == 0
     fluid = o.get_map(0) == 0
+    if variant != "implicit_tvd":
+        g.advance(200)
+        assert o.advance(200)[0] == 0
+        err = rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), fluid)
+        assert max(err.values()) <= TOL, err
+        return
+    o2 = oracle_mod.Case(case)
+    o2.set("T", np.nextafter(o2.get("T"), 2.0))
+    g.advance(40)
+    assert o.advance(40)[0] == 0 and o2.advance(40)[0] == 0
     err = rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), fluid)
     assert max(err.values()) <= TOL, err
+    g.advance(160)
+    assert o.advance(160)[0] == 0 and o2.advance(160)[0] == 0
+    e_gpu = max(rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), fluid).values())
+    e_ulp = max(rel_errors(o2.fields(), o.fields(), fluid).values())
+    assert e_gpu <= max(TOL, e_ulp), (e_gpu, e_ulp)
 
 
 def test_maps_bit_exact(S, oracle_mod):
