@@ -177,6 +177,17 @@ sts_status sts_set_field(sts_ctx* ctx, int32_t field, const double* host, int64_
 /* Same from a DEVICE buffer (global shape). */
 sts_status sts_set_field_device(sts_ctx* ctx, int32_t field, const double* dev, int64_t n);
 
+/* Non-uniform mesh (the general staggered mesh of Fig. 5, with the
+ * steps Delta x_i, Delta y_j that every coefficient of Eqs. pl8-pl33 carries;
+ * SURVEY 8(f) N4): dx = nx GLOBAL column widths, dy = ny row heights (host
+ * buffers, > 0; the caller keeps ownership).  NULL keeps that direction at the
+ * uniform sts_grid spacing.  Bilinear interpolation weights per reading R4.  The
+ * cell counts and the squares (in cell units) are those of sts_create; the
+ * state is kept.  Every point then runs the general-mesh instances of the
+ * kernels (no uniform shortcuts), which is slower than the uniform path.
+ * Returns STS_E_ARG on a size mismatch, STS_E_CONFIG on a step <= 0. */
+sts_status sts_set_mesh(sts_ctx* ctx, const double* dx, int64_t nx, const double* dy, int64_t ny);
+
 /* Loop 1 x loop 2 (Figs. 1-2, GPU columns): n_steps time steps. */
 sts_status sts_advance(sts_ctx* ctx, int32_t n_steps, sts_stats* out);
 

@@ -94,6 +94,10 @@ struct sts_ctx {
     int cur = 0;                           // index of the current state snapshot
     double *ue = nullptr, *ve = nullptr, *Te = nullptr;
     uint32_t* kind32 = nullptr;            // packed ck | uk << 8 | vk << 16, (ny+1) x pitch
+    // non-uniform mesh (sts_set_mesh): Delta x of every stored local
+    // column, Delta y of rows -PADY .. ny+PADY-1; nu = the NU kernel instances run
+    bool nu = false;
+    double *dxl = nullptr, *dyp = nullptr;
     std::vector<uint8_t> h_ck, h_uk, h_vk; // host copies of the local kind maps
     std::vector<uint8_t> h_solid;          // slab-local solid map, ny x sol_w (unwrapped columns from sol_lo)
     int sol_lo = 0, sol_w = 0;
@@ -291,9 +295,13 @@ __global__ void halo_unpack_kernel(int ny, int pitch, int c0, double* u, double*
 
 // ------------------------------------------------------------- kernel table
 typedef void (*march_fn)(MarchParams);
-// regk: the all-regular kernel (sts_march.cuh)
-static march_fn march_table(int impl, int tvd, int regk)
+// regk: the all-regular kernel (sts_march.cuh); nu: the non-uniform-mesh kernel
+static march_fn march_table(int impl, int tvd, int regk, int nu = 0)
 {
+    if (nu) {
+        if (impl) return tvd ? march_kernel<true, true, false, false, true> : march_kernel<true, false, false, false, true>;
+        return tvd ? march_kernel<false, true, false, false, true> : march_kernel<false, false, false, false, true>;
+    }
     if (regk) {
         if (impl) return tvd ? march_kernel<true, true, false, true> : march_kernel<true, false, false, true>;
         return tvd ? march_kernel<false, true, false, true> : march_kernel<false, false, false, true>;
@@ -301,8 +309,12 @@ static march_fn march_table(int impl, int tvd, int regk)
     if (impl) return tvd ? march_kernel<true, true> : march_kernel<true, false>;
     return tvd ? march_kernel<false, true> : march_kernel<false, false>;
 }
-static march_fn march_graph_table(int impl, int tvd, int regk)
+static march_fn march_graph_table(int impl, int tvd, int regk, int nu = 0)
 {
+    if (nu) {
+        if (impl) return tvd ? march_kernel<true, true, true, false, true> : march_kernel<true, false, true, false, true>;
+        return tvd ? march_kernel<false, true, true, false, true> : march_kernel<false, false, true, false, true>;
+    }
     if (regk) {
         if (impl) return tvd ? march_kernel<true, true, true, true> : march_kernel<true, false, true, true>;
         return tvd ? march_kernel<false, true, true, true> : march_kernel<false, false, true, true>;
@@ -310,7 +322,15 @@ static march_fn march_graph_table(int impl, int tvd, int regk)
     if (impl) return tvd ? march_kernel<true, true, true> : march_kernel<true, false, true>;
     return tvd ? march_kernel<false, true, true> : march_kernel<false, false, true>;
 }
-static march_fn conv_march_table(int tvd) { return tvd ? conv_march_kernel<true> : conv_march_kernel<false>; }
+static march_fn conv_march_table(int tvd, int nu = 0)
+{
+    if (nu) return tvd ? conv_march_kernel<true, true> : conv_march_kernel<false, true>;
+    return tvd ? conv_march_kernel<true> : conv_march_kernel<false>;
+}
+// dynamic shared memory of the march / conv kernels: the NU instances keep the
+// column widths of their ring columns behind the struct
+static size_t march_smem(const sts_ctx* c) { return sizeof(MarchSmem) + (c->nu ? RW * sizeof(double) : 0); }
+static size_t conv_smem(const sts_ctx* c) { return sizeof(ConvSmem) + (c->nu ? RW * sizeof(double) : 0); }
 
 // The shared-memory opt-in is a per-device function attribute: one bit per
 // device (the caller has made ctx->device current), set once every attribute
@@ -320,14 +340,16 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
     static std::atomic<unsigned long long> done_mask{0};
     const unsigned long long bit = 1ull << (ctx->device & 63);
     if (done_mask.load() & bit) return STS_OK;
-    for (int q = 0; q < 16; q++) {
-        const int impl = q & 1, tvd = (q >> 1) & 1, regk = (q >> 2) & 1, graph = q >> 3;
-        march_fn f = graph ? march_graph_table(impl, tvd, regk) : march_table(impl, tvd, regk);
-        CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));
+    for (int q = 0; q < 32; q++) {
+        const int impl = q & 1, tvd = (q >> 1) & 1, regk = (q >> 2) & 1, graph = (q >> 3) & 1, nu = q >> 4;
+        if (nu && regk) continue;
+        march_fn f = graph ? march_graph_table(impl, tvd, regk, nu) : march_table(impl, tvd, regk, nu);
+        CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(MarchSmem) + (nu ? RW * sizeof(double) : 0))));
     }
-    for (int tvd = 0; tvd < 2; tvd++)
-        CU(cudaFuncSetAttribute((const void*)conv_march_table(tvd), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(ConvSmem)));
+    for (int q = 0; q < 4; q++)
+        CU(cudaFuncSetAttribute((const void*)conv_march_table(q & 1, q >> 1), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(ConvSmem) + ((q >> 1) ? RW * sizeof(double) : 0))));
     done_mask.fetch_or(bit);
     return STS_OK;
 }
@@ -368,6 +390,8 @@ static MarchParams make_march(const sts_ctx* c, const Params& k)
     m.pw_a = c->gas.pw_form == PW_DPDT ? c->CT3 : 0.0;
     m.bad = c->bad;
     m.pass_key = 0xFFFFF;
+    m.dxl = c->dxl;
+    m.dyp = c->dyp;
     return m;
 }
 
@@ -390,15 +414,16 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     int dev_sms = 148, per_sm = 3;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
     int nb = 0;
-    const void* fn = (const void*)march_table(c->sch.time == STS_IMPLICIT, c->sch.space == STS_TVD_VANLEER, 1);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, MX, sizeof(MarchSmem)) == cudaSuccess && nb > 0)
+    const void* fn = (const void*)march_table(c->sch.time == STS_IMPLICIT, c->sch.space == STS_TVD_VANLEER, !c->nu, c->nu);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, MX, march_smem(c)) == cudaSuccess && nb > 0)
         per_sm = nb;
     const int strips = (c->nloc + MW - 1) / MW;
     const int slots = dev_sms * per_sm;
     const int ny = c->ny;
     double w_gen = 1.35, w_mix = 2.35;                  // warp costs relative to an all-regular warp
     if (const char* cv = getenv("STS_COST")) sscanf(cv, "%lf,%lf", &w_gen, &w_mix);   // tuning hook
-    const bool no_allreg = getenv("STS_NO_ALLREG") != nullptr;   // test hook: every CTA general
+    // every CTA general: test hook, or a non-uniform mesh (the NU kernel has general instances only)
+    const bool no_allreg = getenv("STS_NO_ALLREG") != nullptr || c->nu;
     int forced = 0;
     if (const char* sv = getenv("STS_SEG")) forced = std::max(0, atoi(sv));   // test hook: all heights
     // per (strip, row): cost of a row step and "all 128 points regular"
@@ -468,8 +493,12 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     if (forced > 0) { hg_c = {forced}; hr_c = {forced}; }
     else {
         hg_c = {8, 12, 16, 24, 32, 48};
-        // Hr: 8, 10, ..., 32, then ~6 % steps
-        for (int h = std::min(ny, 8); h <= ny; h = h < 32 ? h + 2 : std::max(h + 8, (int)(h * 1.06))) hr_c.push_back(h);
+        // Hr: 8, 10, ..., 64.  Longer regular CTAs look cheaper to the model (fewer
+        // warm-up rows) but measure slower: a slot is not a processor -- the CTAs
+        // resident on one SM share its issue rate, so a schedule of few long CTAs
+        // leaves SMs with 3 CTAs beside SMs with 4 and a long tail (C3: Hr 252,
+        // 501 CTAs 0.630 ms/pass; forced 48-row CTAs 0.606 ms, profiles/r02_summary.md)
+        for (int h = std::min(ny, 8); h <= std::min(ny, 64); h += 2) hr_c.push_back(h);
         if (hr_c.empty()) hr_c.push_back(std::max(1, ny));
     }
     for (int hg : hg_c)
@@ -529,7 +558,7 @@ static int launch_march(sts_ctx* c, const MarchParams& m, bool graph, cudaStream
                         int n_gen, int n_reg)
 {
     const int impl = c->sch.time == STS_IMPLICIT, tvd = c->sch.space == STS_TVD_VANLEER;
-    march_fn gen = graph ? march_graph_table(impl, tvd, 0) : march_table(impl, tvd, 0);
+    march_fn gen = graph ? march_graph_table(impl, tvd, 0, c->nu) : march_table(impl, tvd, 0, c->nu);
     march_fn reg = graph ? march_graph_table(impl, tvd, 1) : march_table(impl, tvd, 1);
     MarchParams mg = m, mr = m;
     mg.order = (const int4*)order;
@@ -537,14 +566,14 @@ static int launch_march(sts_ctx* c, const MarchParams& m, bool graph, cudaStream
     if (n_gen > 0 && n_reg > 0) {
         cudaEventRecord(c->ev_fork, st);
         cudaStreamWaitEvent(c->gstream, c->ev_fork, 0);
-        gen<<<n_gen, MX, sizeof(MarchSmem), c->gstream>>>(mg);
+        gen<<<n_gen, MX, march_smem(c), c->gstream>>>(mg);
         cudaEventRecord(c->ev_join, c->gstream);
-        reg<<<n_reg, MX, sizeof(MarchSmem), st>>>(mr);
+        reg<<<n_reg, MX, march_smem(c), st>>>(mr);
         cudaStreamWaitEvent(st, c->ev_join, 0);
         return 2;
     }
-    if (n_gen > 0) gen<<<n_gen, MX, sizeof(MarchSmem), st>>>(mg);
-    else if (n_reg > 0) reg<<<n_reg, MX, sizeof(MarchSmem), st>>>(mr);
+    if (n_gen > 0) gen<<<n_gen, MX, march_smem(c), st>>>(mg);
+    else if (n_reg > 0) reg<<<n_reg, MX, march_smem(c), st>>>(mr);
     return 1;
 }
 
@@ -899,6 +928,7 @@ extern "C" void sts_destroy(sts_ctx* ctx)
     for (int k = 0; k < 3; k++) { cudaFree(ctx->snap[k].u); cudaFree(ctx->snap[k].v); cudaFree(ctx->snap[k].p); cudaFree(ctx->snap[k].T); }
     cudaFree(ctx->ue); cudaFree(ctx->ve); cudaFree(ctx->Te); cudaFree(ctx->stage); cudaFree(ctx->halo);
     cudaFree(ctx->kind32); cudaFree(ctx->cta_order); cudaFree(ctx->cta_split); cudaFree(ctx->red);
+    cudaFree(ctx->dxl); cudaFree(ctx->dyp);
     if (ctx->h_red) cudaFreeHost(ctx->h_red);
     for (cudaGraphExec_t& g : ctx->tol_exec) if (g) cudaGraphExecDestroy(g);
     cudaFree(ctx->red2); cudaFree(ctx->d_ls);
@@ -1124,6 +1154,40 @@ extern "C" sts_status sts_constants(sts_ctx* ctx, double* out)
     return STS_OK;
 }
 
+// Non-uniform mesh (Fig. 5): per-column / per-row
+// steps of the global mesh.  The stored local columns take the steps of the
+// global columns they hold (periodic: wrapped; inflow / outflow ghosts: the
+// boundary column's, like their state), rows beyond a wall the wall row's.
+extern "C" sts_status sts_set_mesh(sts_ctx* ctx, const double* dx, int64_t nx, const double* dy, int64_t ny)
+{
+    if (!ctx) return fail(ctx, STS_E_ARG, "null ctx");
+    if ((dx && nx != ctx->nx) || (dy && ny != ctx->ny)) return fail(ctx, STS_E_ARG, "wrong mesh array size");
+    if (dx) for (int64_t i = 0; i < nx; i++) if (!(dx[i] > 0.0) || !std::isfinite(dx[i])) return fail(ctx, STS_E_CONFIG, "mesh step <= 0");
+    if (dy) for (int64_t j = 0; j < ny; j++) if (!(dy[j] > 0.0) || !std::isfinite(dy[j])) return fail(ctx, STS_E_CONFIG, "mesh step <= 0");
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaStreamSynchronize(ctx->stream));
+    std::vector<double> hx(ctx->pitch), hy(ctx->ny + 2 * PADY);
+    for (int l = 0; l < ctx->pitch; l++) {
+        int gi = ctx->gi0 - OFF + l;
+        gi = is_periodic(ctx) ? ((gi % ctx->nx) + ctx->nx) % ctx->nx : std::min(std::max(gi, 0), ctx->nx - 1);
+        hx[l] = dx ? dx[gi] : ctx->spacing;
+    }
+    for (int q = 0; q < ctx->ny + 2 * PADY; q++)
+        hy[q] = dy ? dy[std::min(std::max(q - PADY, 0), ctx->ny - 1)] : ctx->spacing;
+    if (!ctx->dxl && cudaMalloc(&ctx->dxl, hx.size() * sizeof(double)) != cudaSuccess) return fail(ctx, STS_E_OOM, "mesh");
+    if (!ctx->dyp && cudaMalloc(&ctx->dyp, hy.size() * sizeof(double)) != cudaSuccess) return fail(ctx, STS_E_OOM, "mesh");
+    CU(cudaMemcpy(ctx->dxl, hx.data(), hx.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->dyp, hy.data(), hy.size() * sizeof(double), cudaMemcpyHostToDevice));
+    ctx->nu = dx || dy;
+    // a new CTA schedule (the NU kernel has general instances only) and new graphs
+    std::vector<uint32_t> packed((size_t)(ctx->ny + 1) * ctx->pitch);
+    CU(cudaMemcpy(packed.data(), ctx->kind32, packed.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    choose_segments(ctx, packed);
+    for (cudaGraphExec_t& g : ctx->tol_exec)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    return STS_OK;
+}
+
 extern "C" sts_status sts_profile(sts_ctx* ctx, int32_t enable)
 {
     if (!ctx) return fail(ctx, STS_E_ARG, "null ctx");
@@ -1291,10 +1355,10 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
             mp.order = (const int4*)c->cta_order + (part ? c->n_gen : 0);
             void* args[] = {&mp};
             cudaKernelNodeParams kp = {};
-            kp.func = (void*)march_graph_table(impl, tvd, part);
+            kp.func = (void*)march_graph_table(impl, tvd, part, part ? 0 : c->nu);
             kp.gridDim = dim3(cnt);
             kp.blockDim = dim3(MX);
-            kp.sharedMemBytes = sizeof(MarchSmem);
+            kp.sharedMemBytes = march_smem(c);
             kp.kernelParams = args;
             e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
             if (e != cudaSuccess) return e;
@@ -1318,7 +1382,7 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
     if (!impl) {                                  // a1: explicit planes of this step
         Params q = k;
         q.ue_w = c->ue; q.ve_w = c->ve; q.Te_w = c->Te;
-        conv_march_table(tvd)<<<mgrid, MX, sizeof(ConvSmem), cap>>>(make_march(c, q));
+        conv_march_table(tvd, c->nu)<<<mgrid, MX, conv_smem(c), cap>>>(make_march(c, q));
     }
     CG(pass(n1, a, 0, cap));
     loop_check_kernel<<<1, 32, 0, cap>>>(c->red2, c->d_ls, h, mn, mx, tol);
@@ -1441,7 +1505,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 k.ue_w = c->ue; k.ve_w = c->ve; k.Te_w = c->Te;
                 prof_begin(c, 1);
                 const dim3 mgrid(c->n_gen + c->n_reg);                 // the conv kernel: every CTA of the schedule
-                conv_march_table(tvd)<<<mgrid, MX, sizeof(ConvSmem), st>>>(make_march(c, k));
+                conv_march_table(tvd, c->nu)<<<mgrid, MX, conv_smem(c), st>>>(make_march(c, k));
                 prof_end(c);
                 c->launches++;
                 CU(cudaGetLastError());
@@ -1488,8 +1552,8 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                     cudaStream_t as = overlap ? c->hstream : st;
                     if (overlap && it > 0) CU(cudaStreamWaitEvent(as, c->ev_b, 0));   // pass it-1 complete
                     prof_begin(c, 0);
-                    march_fn gen = gk ? march_graph_table(impl, tvd, 0) : march_table(impl, tvd, 0);
-                    gen<<<c->n_edge, MX, sizeof(MarchSmem), as>>>(ma);
+                    march_fn gen = gk ? march_graph_table(impl, tvd, 0, c->nu) : march_table(impl, tvd, 0, c->nu);
+                    gen<<<c->n_edge, MX, march_smem(c), as>>>(ma);
                     if (overlap) CU(cudaEventRecord(c->ev_a[it & 1], as));
                     c->launches += 1 + launch_march(c, mb, gk, st, c->cta_split + 4 * c->n_edge, c->n_split_gen,
                                                     c->n_split - c->n_edge - c->n_split_gen);

@@ -32,11 +32,15 @@ struct ConvSmem {
     unsigned long long mbar[RS];     // TMA completion barrier of each ring slot
 };
 
-template <bool TVD>
+// NU = true: non-uniform mesh -- general points only, the
+// limiters and fluxes in their general-mesh form (Eqs. pl15_1-pl15_2, pl15_11,
+// pl31_1); column widths behind ConvSmem, row heights from m.dyp.
+template <bool TVD, bool NU = false>
 __global__ void __launch_bounds__(MX, 5) conv_march_kernel(MarchParams m)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ConvSmem& s = *reinterpret_cast<ConvSmem*>(smem_raw);
+    double* const s_dx = reinterpret_cast<double*>(smem_raw + sizeof(ConvSmem));   // NU only: RW widths
     const Params& k = m.k;
     const int t = threadIdx.x;
     const int4 ce = m.order[blockIdx.x];
@@ -53,12 +57,15 @@ __global__ void __launch_bounds__(MX, 5) conv_march_kernel(MarchParams m)
         for (int q = 0; q < RS; q++) mbar_init(&s.mbar[q], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    if (NU)
+        for (int q = t; q < RW; q += MX) s_dx[q] = __ldg(m.dxl + min(max(c0 + q, 0), k.pitch - 1));
     __syncthreads();
     const int gi = I0 - 2 + t;
     const int J0 = ce.y, J1 = ce.z;
     const int js = J0 - 2;                              // 2 warm-up rows (carried TY, uY, vY, fluxes)
     const bool owner = t >= 2 && t < 2 + MW && gi < k.gi0 + k.nloc;
-    const double dx = k.dx, dy = k.dy;
+    const double dx = NU ? s_dx[lc] : k.dx;
+    auto X = [&](int o) { return s_dx[lc + o]; };     // Delta x at ring offset o (NU)
     // ring fed from the n-1 snapshot
     MarchParams mm = m;
     mm.k.u_o = k.u_1; mm.k.v_o = k.v_1; mm.k.p_o = k.p_1; mm.k.T_o = k.T_1;
@@ -73,7 +80,7 @@ __global__ void __launch_bounds__(MX, 5) conv_march_kernel(MarchParams m)
     int sj = slot(js);
 
     double TYc = 0.0, uYc = 0.0, vYc = 0.0;          // carried: TY(i,j), uY(i,y^f_j), vY(cell (i,j-1)) for v-face (i,j)
-    if (allreg) {
+    if (allreg && !NU) {
         constexpr bool ALLREG = true;
 #include "sts_conv_loop.inc"
     } else {

@@ -58,6 +58,20 @@ struct MarchParams {
     const int* done;             // graph-driven loop 2 (tolerance mode): loop finished -> the pass is a no-op
     unsigned long long* bad;     // sticky first-bad-state key of the advance call (bad_key)
     int pass_key;                // 0xFFFFF - pass index within the advance call
+    // non-uniform mesh (NU instances): Delta x of every stored local
+    // column (pitch entries, ghost rules applied by the host) and Delta y of rows
+    // -PADY .. ny+PADY-1 at dyp[j + PADY] (rows beyond a wall take the wall row's step)
+    const double* dxl;
+    const double* dyp;
+};
+constexpr int PADY = 4;
+
+// Mesh steps around a point of a non-uniform mesh: the column widths of the
+// CTA's ring columns (shared memory, ring column index) and the heights of
+// rows j-1 .. j+3 of the row step (Fig. 5).
+struct Geo {
+    const double* dxr;
+    double ym, y0, ya, yb, yc;
 };
 
 // fp64 reciprocal: MUFU.RCP64H seed (relative error <= 2^-19.9, measured) and
@@ -104,6 +118,37 @@ __device__ __forceinline__ double psi_f(double f1, double f2, double f3, double 
     const double q = fdiv(a, a + b);
     return up ? q : -q;
 }
+
+// psi_s of Eq. pl15_2 on a general mesh, Van Leer psi(r) = 2r/(1+r)
+// for r > 0 multiplied out: up (v > 0) 2 d2 a / ((d1 + d2) b + (d2 + d3) a),
+// a = f2 - f1; down -2 d3 a / ((d3 + d4) b + (d2 + d3) a), a = f4 - f3; b = f3 - f2.
+// Same guards as psi_f (R37, R6); equals psi_f's a / (a + b) on a uniform mesh.
+__device__ __forceinline__ double psi_s_nu(double f1, double f2, double f3, double f4,
+                                           double d1, double d2, double d3, double d4, double w)
+{
+    const double b = f3 - f2;
+    if (fabs(b) <= 1e-12 * (1.0 + fabs(f2) + fabs(f3))) return 0.0;   // R37
+    const bool up = w > 0.0;
+    const double a = up ? f2 - f1 : f4 - f3;
+    if (!(a * b > 0.0)) return 0.0;                                    // r <= 0 (R6)
+    const double q = fdiv(2.0 * (up ? d2 : d3) * a, (up ? d1 + d2 : d3 + d4) * b + (d2 + d3) * a);
+    return up ? q : -q;
+}
+// psi_c of Eq. pl15_1: up d2 a / (d1 b + d2 a), down -d2 a / (d3 b + d2 a).
+__device__ __forceinline__ double psi_c_nu(double f1, double f2, double f3, double f4,
+                                           double d1, double d2, double d3, double w)
+{
+    const double b = f3 - f2;
+    if (fabs(b) <= 1e-12 * (1.0 + fabs(f2) + fabs(f3))) return 0.0;   // R37
+    const bool up = w > 0.0;
+    const double a = up ? f2 - f1 : f4 - f3;
+    if (!(a * b > 0.0)) return 0.0;                                    // r <= 0 (R6)
+    const double q = fdiv(d2 * a, (up ? d1 : d3) * b + d2 * a);
+    return up ? q : -q;
+}
+// Linear-interpolation weight of the node left of a face between nodes of
+// widths dl, dr (reading R4): dr / (dl + dr).
+__device__ __forceinline__ double wleft(double dl, double dr) { return dr / (dl + dr); }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
 {
@@ -318,14 +363,20 @@ __device__ __forceinline__ void ring_issue_tma(SM& s, int sl, const MarchParams&
 #define STS_LINK(F, ps) (TVD ? max0(F) - (F) * (ps) : max0(F))
 
 // ================= stage A: row j+1 fluxes, link pieces =================
-template <bool IMPL, bool TVD, bool REG>
+// NU: the non-uniform-mesh instance (general points only): every step of the
+// uniform shortcuts is replaced by the printed general-mesh form (Eqs. pl8-pl16,
+// pl31-pl33, pl15_1-pl15_2; reading R4 for the corner Gamma).
+template <bool IMPL, bool TVD, bool REG, bool NU = false>
 __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
                                         const RingRow& R0, const RingRow& Ra, const RingRow& Rb,
                                         const RingRow& Rc, const FluxRow& Fc, FluxRow& Fn, const NM1& nm,
-                                        StepVars& v)
+                                        StepVars& v, const Geo& g)
 {
-    const double dx = m.k.dx, dy = m.k.dy;
+    static_assert(!(NU && REG), "non-uniform meshes run the general instances only");
+    const double dx = NU ? g.dxr[lc] : m.k.dx;
+    const double dya = NU ? g.ya : m.k.dy;           // Delta y of row j+1
     const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
+    auto X = [&](int o) { return g.dxr[lc + o]; };   // Delta x of the column at ring offset o (NU)
     // (p/T)^{n-1} of row j+1 (to shared memory in stage E)
     v.r1n = fdiv(nm.p1n, nm.T1n == 0.0 ? 1.0 : nm.T1n);
     // F^x, rho^u at u-face (i, j+1)  (Eqs. pl8, pl10, R1)
@@ -335,8 +386,9 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             const double w = Ra.U[lc], r1 = Ra.R[lc - 1], r2 = Ra.R[lc];
             ru = w > 0.0 ? r1 : r2;
             if (TVD && cF<REG>(Ra.KK[lc - 2]) && cF<REG>(Ra.KK[lc - 1]) && cF<REG>(kw1) && cF<REG>(Ra.KK[lc + 1]))
-                ru += psi_f(Ra.R[lc - 2], r1, r2, Ra.R[lc + 1], w) * (r2 - r1);
-            F = ru * w * dy;
+                ru += (NU ? psi_s_nu(Ra.R[lc - 2], r1, r2, Ra.R[lc + 1], X(-2), X(-1), X(0), X(1), w)
+                          : psi_f(Ra.R[lc - 2], r1, r2, Ra.R[lc + 1], w)) * (r2 - r1);
+            F = ru * w * dya;
         }
         Fn.RU[lc] = ru;
         Fn.FX[lc] = F;
@@ -349,7 +401,8 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             const double w = Ra.V[lc], r1 = R0.R[lc], r2 = Ra.R[lc];
             rv = w > 0.0 ? r1 : r2;
             if (TVD && cF<REG>(Rm.KK[lc]) && cF<REG>(kw0) && cF<REG>(kw1) && cF<REG>(Rb.KK[lc]))
-                rv += psi_f(Rm.R[lc], r1, r2, Rb.R[lc], w) * (r2 - r1);
+                rv += (NU ? psi_s_nu(Rm.R[lc], r1, r2, Rb.R[lc], g.ym, g.y0, g.ya, g.yb, w)
+                          : psi_f(Rm.R[lc], r1, r2, Rb.R[lc], w)) * (r2 - r1);
             F = rv * w * dx;
         }
         v.rv1 = rv;
@@ -364,10 +417,14 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         if (!cW<REG>(kl) && !cW<REG>(kw0)) {
             const double F = Fc.FX[lc];
             const double g1 = R0.G[lc - 1], g2 = R0.G[lc];
-            const double D = m.CT1_dydx * (2.0 * g1 * g2 * rcp(g1 + g2));
+            // NU: C^T1 Gamma|_{x^f_i} Delta y_j / (0.5 (Delta x_{i-1} + Delta x_i)) with the harmonic
+            // Gamma of Eq. pl33 = 2 C^T1 Delta y_j g1 g2 / (Delta x_{i-1} g2 + Delta x_i g1)
+            const double D = NU ? 2.0 * m.k.CT1 * g.y0 * g1 * g2 * rcp(X(-1) * g2 + dx * g1)
+                                : m.CT1_dydx * (2.0 * g1 * g2 * rcp(g1 + g2));
             double ps = 0.0;
             if (IMPL && TVD && cF<REG>(R0.KK[lc - 2]) && cF<REG>(kl) && cF<REG>(kw0) && cF<REG>(R0.KK[lc + 1]))
-                ps = psi_f(R0.T[lc - 2], R0.T[lc - 1], R0.T[lc], R0.T[lc + 1], R0.U[lc]);
+                ps = NU ? psi_s_nu(R0.T[lc - 2], R0.T[lc - 1], R0.T[lc], R0.T[lc + 1], X(-2), X(-1), X(0), X(1), R0.U[lc])
+                        : psi_f(R0.T[lc - 2], R0.T[lc - 1], R0.T[lc], R0.T[lc + 1], R0.U[lc]);
             pw = (IMPL ? STS_LINK(F, ps) : 0.0) + D;
         }
         s.XTW[lc] = pw;
@@ -378,10 +435,12 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
     if (!cW<REG>(kw0) && !cW<REG>(kw1)) {
         const double F = v.Fy1;
         const double g1 = R0.G[lc], g2 = Ra.G[lc];
-        const double D = m.CT1_dxdy * (2.0 * g1 * g2 * rcp(g1 + g2));
+        const double D = NU ? 2.0 * m.k.CT1 * dx * g1 * g2 * rcp(g.y0 * g2 + g.ya * g1)
+                            : m.CT1_dxdy * (2.0 * g1 * g2 * rcp(g1 + g2));
         double ps = 0.0;
         if (IMPL && TVD && cF<REG>(Rm.KK[lc]) && cF<REG>(kw0) && cF<REG>(kw1) && cF<REG>(Rb.KK[lc]))
-            ps = psi_f(Rm.T[lc], R0.T[lc], Ra.T[lc], Rb.T[lc], Ra.V[lc]);
+            ps = NU ? psi_s_nu(Rm.T[lc], R0.T[lc], Ra.T[lc], Rb.T[lc], g.ym, g.y0, g.ya, g.yb, Ra.V[lc])
+                    : psi_f(Rm.T[lc], R0.T[lc], Ra.T[lc], Rb.T[lc], Ra.V[lc]);
         v.ytSn = (IMPL ? STS_LINK(F, ps) : 0.0) + D;
         v.ytN = IMPL ? v.ytSn - F : v.ytSn;
     }
@@ -390,12 +449,14 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         double xe = 0.0, xw = 0.0, Fb = 0.0;
         if (cF<REG>(kw0)) {
             const double ub = 0.5 * (R0.U[lc] + R0.U[lc + 1]);
-            Fb = R0.R[lc] * ub * dy;
-            const double D = m.B43_dydx * R0.G[lc];
+            Fb = R0.R[lc] * ub * (NU ? g.y0 : m.k.dy);
+            // NU: 4/3 D^ux = 4/3 B Gamma_i Delta y_j / Delta x_i (transposed Eq. pl16)
+            const double D = NU ? 4.0 / 3.0 * m.k.B * R0.G[lc] * g.y0 * rcp(dx) : m.B43_dydx * R0.G[lc];
             double ps = 0.0;
             if (IMPL && TVD && uA<REG>(R0.KK[lc - 1]) && uA<REG>(kw0) && uA<REG>(R0.KK[lc + 1]) &&
                 uA<REG>(R0.KK[lc + 2]))
-                ps = psi_f(R0.U[lc - 1], R0.U[lc], R0.U[lc + 1], R0.U[lc + 2], ub);
+                ps = NU ? psi_c_nu(R0.U[lc - 1], R0.U[lc], R0.U[lc + 1], R0.U[lc + 2], X(-1), X(0), X(1), ub)
+                        : psi_f(R0.U[lc - 1], R0.U[lc], R0.U[lc + 1], R0.U[lc + 2], ub);
             xw = (IMPL ? STS_LINK(Fb, ps) : 0.0) + D;
             xe = IMPL ? xw - Fb : xw;
         }
@@ -408,8 +469,13 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
     v.upsi2 = 0.0;
     if (IMPL && TVD && uA<REG>(Rm.KK[lc]) && uA<REG>(kw0) && uA<REG>(kw1) && uA<REG>(Rb.KK[lc])) {
         const double f1 = Rm.U[lc], f2 = R0.U[lc], f3 = Ra.U[lc], f4 = Rb.U[lc];
-        v.upsi1 = psi_f(f1, f2, f3, f4, Ra.V[lc]);
-        v.upsi2 = psi_f(f1, f2, f3, f4, Ra.V[lc - 1]);
+        if (NU) {
+            v.upsi1 = psi_s_nu(f1, f2, f3, f4, g.ym, g.y0, g.ya, g.yb, Ra.V[lc]);
+            v.upsi2 = psi_s_nu(f1, f2, f3, f4, g.ym, g.y0, g.ya, g.yb, Ra.V[lc - 1]);
+        } else {
+            v.upsi1 = psi_f(f1, f2, f3, f4, Ra.V[lc]);
+            v.upsi2 = psi_f(f1, f2, f3, f4, Ra.V[lc - 1]);
+        }
     }
     // v-eq normal piece of cell (i, j+1): a^v_4 of v-face (i, j+1), a^v_3 of v-face (i, j+2)
     v.vcN = 0.0;
@@ -418,16 +484,28 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
     if (cF<REG>(kw1)) {
         const double vb = 0.5 * (Ra.V[lc] + Rb.V[lc]);
         v.FbN = Ra.R[lc] * vb * dx;
-        const double D = m.B43_dxdy * Ra.G[lc];
+        // NU: 4/3 D^vy_{i,j+2} = 4/3 B Gamma_{i,j+1} Delta x_i / Delta y_{j+1} (Eq. pl16)
+        const double D = NU ? 4.0 / 3.0 * m.k.B * Ra.G[lc] * dx * rcp(g.ya) : m.B43_dxdy * Ra.G[lc];
         double ps = 0.0;
         if (IMPL && TVD && vA<REG>(kw0) && vA<REG>(kw1) && vA<REG>(Rb.KK[lc]) && vA<REG>(Rc.KK[lc]))
-            ps = psi_f(R0.V[lc], Ra.V[lc], Rb.V[lc], Rc.V[lc], vb);
+            ps = NU ? psi_c_nu(R0.V[lc], Ra.V[lc], Rb.V[lc], Rc.V[lc], g.y0, g.ya, g.yb, vb)
+                    : psi_f(R0.V[lc], Ra.V[lc], Rb.V[lc], Rc.V[lc], vb);
         v.vcSn = (IMPL ? STS_LINK(v.FbN, ps) : 0.0) + D;
         v.vcN = IMPL ? v.vcSn - v.FbN : v.vcSn;
     }
     // corner Gamma at (x^f_i, y^f_{j+1}) (R4, R5; BC spec 8)
     if (REG) {
         v.gcN = 0.25 * (R0.G[lc - 1] + R0.G[lc] + Ra.G[lc - 1] + Ra.G[lc]);
+    } else if (NU) {
+        // bilinear weights of the four cell centres, renormalised to the cells kept
+        const double wxl = wleft(X(-1), dx), wxr = 1.0 - wxl;
+        const double wyb = wleft(g.y0, g.ya), wyt = 1.0 - wyb;
+        double sum = 0.0, ws = 0.0;
+        if (!wallish(ckind(R0.KK[lc - 1]))) { sum += wxl * wyb * R0.G[lc - 1]; ws += wxl * wyb; }
+        if (!wallish(ckind(kw0))) { sum += wxr * wyb * R0.G[lc]; ws += wxr * wyb; }
+        if (!wallish(ckind(Ra.KK[lc - 1]))) { sum += wxl * wyt * Ra.G[lc - 1]; ws += wxl * wyt; }
+        if (!wallish(ckind(kw1))) { sum += wxr * wyt * Ra.G[lc]; ws += wxr * wyt; }
+        v.gcN = ws > 0.0 ? sum / ws : 0.0;
     } else {
         double sum = 0.0;
         int n = 0;
@@ -445,10 +523,16 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         if (IMPL && TVD && vA<REG>(Ra.KK[lc - 2]) && vA<REG>(Ra.KK[lc - 1]) && vA<REG>(kw1) &&
             vA<REG>(Ra.KK[lc + 1])) {
             const double f1 = Ra.V[lc - 2], f2 = Ra.V[lc - 1], f3 = Ra.V[lc], f4 = Ra.V[lc + 1];
-            p1 = psi_f(f1, f2, f3, f4, Ra.U[lc]);
-            p2 = psi_f(f1, f2, f3, f4, R0.U[lc]);
+            if (NU) {
+                p1 = psi_s_nu(f1, f2, f3, f4, X(-2), X(-1), X(0), X(1), Ra.U[lc]);
+                p2 = psi_s_nu(f1, f2, f3, f4, X(-2), X(-1), X(0), X(1), R0.U[lc]);
+            } else {
+                p1 = psi_f(f1, f2, f3, f4, Ra.U[lc]);
+                p2 = psi_f(f1, f2, f3, f4, R0.U[lc]);
+            }
         }
-        const double D = m.B_dydx * v.gcN;
+        // NU: D^vx_{i,j+1} = B Gamma|_{x^f_i} (Delta y_j + Delta y_{j+1}) / (Delta x_{i-1} + Delta x_i) (Eq. pl16)
+        const double D = NU ? m.k.B * v.gcN * (g.y0 + g.ya) * rcp(X(-1) + dx) : m.B_dydx * v.gcN;
         v.FwSum = F1 + F2;
         v.xvW = (IMPL ? 0.5 * (STS_LINK(F1, p1) + STS_LINK(F2, p2)) : 0.0) + D;
         s.XVW[lc] = v.xvW;           // the E side of v-face (i-1, j+1) is XVW - (F^x(j) + F^x(j+1))/2
@@ -456,31 +540,61 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
 }
 
 // S^T_c pieces of a general (boundary) point.
-// dv/dx + du/dy from mid-face velocities: bilinear 4-point means (R4), or on a
-// face that lies on a wall the slip velocity of Eq. pl38 (R38).
+// dv/dx + du/dy from mid-face velocities: bilinear interpolation between the four
+// neighbouring nodes (R4 -- the 4-point mean on a uniform mesh), or on a face
+// that lies on a wall the slip velocity of Eq. pl38 (R38).
+template <bool NU>
 __device__ __forceinline__ double shear_general(const RingRow& R0, const RingRow& Ra, const RingRow& Rm, int lc,
-                                             double rP, const MarchParams& m)
+                                                double rP, const MarchParams& m, const Geo& g)
 {
     const Params& k = m.k;
+    const double dx = NU ? g.dxr[lc] : k.dx, dy = NU ? g.y0 : k.dy;
     const double zeta = 1.1466 * k.Kn * rcp(rP);
     auto slip = [&](double vP, double vw, double dn) { return (dn * vw + zeta * vP) * rcp(dn + zeta); };
     const double vs = R0.V[lc] + Ra.V[lc], us = R0.U[lc] + R0.U[lc + 1];
     const uint8_t kE = ckind(R0.KK[lc + 1]), kW = ckind(R0.KK[lc - 1]);
     const uint8_t kN = ckind(Ra.KK[lc]), kS = ckind(Rm.KK[lc]);
-    const double vE = wallish(kE) ? slip(0.5 * vs, 0.0, 0.5 * k.dx) : 0.25 * (vs + (R0.V[lc + 1] + Ra.V[lc + 1]));
-    const double vW = wallish(kW) ? slip(0.5 * vs, 0.0, 0.5 * k.dx) : 0.25 * ((R0.V[lc - 1] + Ra.V[lc - 1]) + vs);
-    const double uN = wallish(kN) ? slip(0.5 * us, kN == CK_WALLY ? k.u_wt : 0.0, 0.5 * k.dy)
-                                  : 0.25 * (us + (Ra.U[lc] + Ra.U[lc + 1]));
-    const double uS = wallish(kS) ? slip(0.5 * us, kS == CK_WALLY ? k.u_wb : 0.0, 0.5 * k.dy)
-                                  : 0.25 * ((Rm.U[lc] + Rm.U[lc + 1]) + us);
-    return (vE - vW) * m.inv_dx + (uN - uS) * m.inv_dy;
+    double vE, vW, uN, uS;
+    if (NU) {
+        // node order as the 4-point mean: (i, j), (i+1, j), (i, j+1), (i+1, j+1) etc.
+        const double wE = wleft(dx, g.dxr[lc + 1]), wW = wleft(g.dxr[lc - 1], dx);
+        const double wN = wleft(dy, g.ya), wS = wleft(g.ym, dy);
+        vE = 0.5 * wE * R0.V[lc] + 0.5 * (1.0 - wE) * R0.V[lc + 1] + 0.5 * wE * Ra.V[lc] + 0.5 * (1.0 - wE) * Ra.V[lc + 1];
+        vW = 0.5 * wW * R0.V[lc - 1] + 0.5 * (1.0 - wW) * R0.V[lc] + 0.5 * wW * Ra.V[lc - 1] + 0.5 * (1.0 - wW) * Ra.V[lc];
+        uN = 0.5 * wN * R0.U[lc] + 0.5 * wN * R0.U[lc + 1] + 0.5 * (1.0 - wN) * Ra.U[lc] + 0.5 * (1.0 - wN) * Ra.U[lc + 1];
+        uS = 0.5 * wS * Rm.U[lc] + 0.5 * wS * Rm.U[lc + 1] + 0.5 * (1.0 - wS) * R0.U[lc] + 0.5 * (1.0 - wS) * R0.U[lc + 1];
+        if (wallish(kE)) vE = slip(0.5 * vs, 0.0, 0.5 * dx);
+        if (wallish(kW)) vW = slip(0.5 * vs, 0.0, 0.5 * dx);
+        if (wallish(kN)) uN = slip(0.5 * us, kN == CK_WALLY ? k.u_wt : 0.0, 0.5 * dy);
+        if (wallish(kS)) uS = slip(0.5 * us, kS == CK_WALLY ? k.u_wb : 0.0, 0.5 * dy);
+    } else {
+        vE = wallish(kE) ? slip(0.5 * vs, 0.0, 0.5 * dx) : 0.25 * (vs + (R0.V[lc + 1] + Ra.V[lc + 1]));
+        vW = wallish(kW) ? slip(0.5 * vs, 0.0, 0.5 * dx) : 0.25 * ((R0.V[lc - 1] + Ra.V[lc - 1]) + vs);
+        uN = wallish(kN) ? slip(0.5 * us, kN == CK_WALLY ? k.u_wt : 0.0, 0.5 * dy)
+                         : 0.25 * (us + (Ra.U[lc] + Ra.U[lc + 1]));
+        uS = wallish(kS) ? slip(0.5 * us, kS == CK_WALLY ? k.u_wb : 0.0, 0.5 * dy)
+                         : 0.25 * ((Rm.U[lc] + Rm.U[lc + 1]) + us);
+    }
+    return NU ? (vE - vW) * rcp(dx) + (uN - uS) * rcp(dy) : (vE - vW) * m.inv_dx + (uN - uS) * m.inv_dy;
 }
 // Pressure gradient of the C^T3 Dp/Dt term (R9) at a general point: face
-// pressures = mean of the two cells, = p of the cell at a wall.
+// pressures = linear interpolation between the two cell centres (the mean on a
+// uniform mesh), = p of the cell at a wall.
+template <bool NU>
 __device__ __forceinline__ void dp_general(const RingRow& R0, const RingRow& Ra, const RingRow& Rm, int lc,
-                                        const MarchParams& m, double& dpx, double& dpy)
+                                           const MarchParams& m, const Geo& g, double& dpx, double& dpy)
 {
     const double pc = R0.P[lc];
+    if (NU) {
+        const double dx = g.dxr[lc], dxe = g.dxr[lc + 1], dxw = g.dxr[lc - 1];
+        const double pe = wallish(ckind(R0.KK[lc + 1])) ? pc : (dxe * pc + dx * R0.P[lc + 1]) / (dx + dxe);
+        const double pw = wallish(ckind(R0.KK[lc - 1])) ? pc : (dx * R0.P[lc - 1] + dxw * pc) / (dxw + dx);
+        const double pn = wallish(ckind(Ra.KK[lc])) ? pc : (g.ya * pc + g.y0 * Ra.P[lc]) / (g.y0 + g.ya);
+        const double ps = wallish(ckind(Rm.KK[lc])) ? pc : (g.y0 * Rm.P[lc] + g.ym * pc) / (g.ym + g.y0);
+        dpx = (pe - pw) * rcp(dx);
+        dpy = (pn - ps) * rcp(g.y0);
+        return;
+    }
     const double pe = wallish(ckind(R0.KK[lc + 1])) ? pc : 0.5 * (pc + R0.P[lc + 1]);
     const double pw = wallish(ckind(R0.KK[lc - 1])) ? pc : 0.5 * (R0.P[lc - 1] + pc);
     const double pn = wallish(ckind(Ra.KK[lc])) ? pc : 0.5 * (pc + Ra.P[lc]);
@@ -490,14 +604,17 @@ __device__ __forceinline__ void dp_general(const RingRow& R0, const RingRow& Ra,
 }
 
 // ================= stage C: T_{i,j}, u-hat_{i,j}, v-hat_{i,j+1} =================
-template <bool IMPL, bool TVD, bool REG>
+template <bool IMPL, bool TVD, bool REG, bool NU = false>
 __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
                                         const RingRow& R0, const RingRow& Ra, const RingRow& Rb,
                                         const FluxRow& Fc, const FluxRow& Fn, const NM1& nm, const Carry& c,
-                                        StepVars& v)
+                                        StepVars& v, const Geo& g)
 {
     const Params& k = m.k;
-    const double dt = k.dt, dx = k.dx, dy = k.dy;
+    const double dt = k.dt;
+    const double dx = NU ? g.dxr[lc] : k.dx, dy = NU ? g.y0 : k.dy;
+    const double dxw = NU ? g.dxr[lc - 1] : k.dx;                 // Delta x_{i-1}
+    const double dV = NU ? dx * dy : m.dV;
     const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
     const double rP = R0.R[lc], gP = R0.G[lc];
     // ---- energy (Eqs. pl30-pl33, pl28-pl29 / pl31_1)
@@ -525,12 +642,13 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
             if (wallish(kn)) { a4 = k.CT1 * gP * dx * rcp(0.5 * dy + tau); T4 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
             else { a4 = v.ytN; FNl = v.Fy1; T4 = Ra.T[lc]; }
         }
-        const double a0 = IMPL ? dt * (a1 + a2 + a3 + a4 + FE - FW + FNl - FSl) + rP * m.dV
-                               : dt * (a1 + a2 + a3 + a4) + rP * m.dV;
-        // S^T_c, Eq. pl29 (R4 bilinear = 4-point mean); a mid-face velocity on a
-        // wall face is the slip velocity of Eq. pl38 (R38)
-        const double dudx = (R0.U[lc + 1] - R0.U[lc]) * m.inv_dx;
-        const double dvdy = (Ra.V[lc] - R0.V[lc]) * m.inv_dy;
+        const double a0 = IMPL ? dt * (a1 + a2 + a3 + a4 + FE - FW + FNl - FSl) + rP * dV
+                               : dt * (a1 + a2 + a3 + a4) + rP * dV;
+        // S^T_c, Eq. pl29 (R4 bilinear = 4-point mean on a uniform mesh); a mid-face
+        // velocity on a wall face is the slip velocity of Eq. pl38 (R38)
+        const double rdx = NU ? rcp(dx) : m.inv_dx, rdy = NU ? rcp(dy) : m.inv_dy;
+        const double dudx = (R0.U[lc + 1] - R0.U[lc]) * rdx;
+        const double dvdy = (Ra.V[lc] - R0.V[lc]) * rdy;
         double shear;
         if (REG) {
             // dv/dx + du/dy from the bilinear face values (R4): v_E - v_W and u_N - u_S
@@ -538,14 +656,15 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
             shear = ((R0.V[lc + 1] + Ra.V[lc + 1]) - (R0.V[lc - 1] + Ra.V[lc - 1])) * m.q_dx
                   + ((Ra.U[lc] + Ra.U[lc + 1]) - (Rm.U[lc] + Rm.U[lc + 1])) * m.q_dy;
         } else {
-            shear = shear_general(R0, Ra, Rm, lc, rP, m);
+            shear = shear_general<NU>(R0, Ra, Rm, lc, rP, m, g);
         }
         const double div = dudx + dvdy;
         // pressure work (R9): C^T3 Dp/Dt of Eq. pl6 at the old iterate --
         // (p - p^{n-1}) / dt + ubar dp/dx + vbar dp/dy with face pressures p_f =
-        // mean of the two cells, = p of the cell at a wall -- or kappa p div(u);
-        // branch-free: pw_a = C^T3 or 0, pwk = 0 or kappa.  p^{n-1} = rho^{n-1} T^{n-1}
-        // (the (p/T)^{n-1} row times T^{n-1}, within 2 ulp of the stored p^{n-1})
+        // linear interpolation of the two cells, = p of the cell at a wall -- or
+        // kappa p div(u); branch-free: pw_a = C^T3 or 0, pwk = 0 or kappa.
+        // p^{n-1} = rho^{n-1} T^{n-1} (the (p/T)^{n-1} row times T^{n-1}, within
+        // 2 ulp of the stored p^{n-1})
         const double pc = R0.P[lc];
         const double p1 = s.R1[lc] * nm.T1c;
         double dpx, dpy;
@@ -553,20 +672,21 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
             dpx = (R0.P[lc + 1] - R0.P[lc - 1]) * m.h_dx;
             dpy = (Ra.P[lc] - Rm.P[lc]) * m.h_dy;
         } else {
-            dp_general(R0, Ra, Rm, lc, m, dpx, dpy);
+            dp_general<NU>(R0, Ra, Rm, lc, m, g, dpx, dpy);
         }
         const double ub = 0.5 * (R0.U[lc] + R0.U[lc + 1]), vb = 0.5 * (R0.V[lc] + Ra.V[lc]);
         const double pwork = m.pw_a * ((pc - p1) * m.inv_dt + ub * dpx + vb * dpy) + k.pwk * pc * div;
         const double Sc = (k.CT2 * gP * (2.0 * (dudx * dudx + dvdy * dvdy) + shear * shear - 2.0 / 3.0 * div * div)
-                           + pwork) * m.dV;
-        const double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + (IMPL ? Sc : Sc + nm.Tec)) + p1 * m.dV;
+                           + pwork) * dV;
+        const double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + (IMPL ? Sc : Sc + nm.Tec)) + p1 * dV;
         v.TN = rhs * rcp(a0);
     }
     // ---- u pseudo-velocity at u-face (i, j)
     {
         // N tangential link pieces at y^f_{j+1} (both sides; the S side is carried)
         const double F1 = v.Fy1, F2 = Fn.FY[lc - 1];
-        const double D = m.B_dxdy * v.gcN;
+        // NU: D^uy = B Gamma|_{corner} (Delta x_{i-1} + Delta x_i) / (Delta y_j + Delta y_{j+1})
+        const double D = NU ? k.B * v.gcN * (dxw + dx) * rcp(dy + g.ya) : m.B_dxdy * v.gcN;
         v.FsSumN = F1 + F2;
         v.utSn = (IMPL ? 0.5 * (STS_LINK(F1, v.upsi1) + STS_LINK(F2, v.upsi2)) : 0.0) + D;
         const double a4p = IMPL ? v.utSn - 0.5 * v.FsSumN : v.utSn;
@@ -584,26 +704,29 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
                 FsS = FnS = 0.0;
                 const double gadj = 0.5 * (gL + gR);
                 const double zeta = 1.1466 * k.Kn * rcp(0.5 * (rL + rR));     // Eq. pl38
+                const double L = NU ? 0.5 * (dxw + dx) : dx;                    // u-CV width
                 const uint8_t kl = ckind(Rm.KK[lc - 1]), kr = ckind(Rm.KK[lc]);
                 if (kl == CK_WALLY || (kl == CK_SOLID && kr == CK_SOLID)) {
-                    a3 = k.B * gadj * dx * rcp(0.5 * dy + zeta); uS = kl == CK_WALLY ? k.u_wb : 0.0;
+                    a3 = k.B * gadj * L * rcp(0.5 * dy + zeta); uS = kl == CK_WALLY ? k.u_wb : 0.0;
                 } else { a3 = c.utS; FsS = c.FsSum; uS = Rm.U[lc]; }
                 const uint8_t ml = ckind(Ra.KK[lc - 1]), mr = ckind(kw1);
                 if (ml == CK_WALLY || (ml == CK_SOLID && mr == CK_SOLID)) {
-                    a4 = k.B * gadj * dx * rcp(0.5 * dy + zeta); uN = ml == CK_WALLY ? k.u_wt : 0.0;
+                    a4 = k.B * gadj * L * rcp(0.5 * dy + zeta); uN = ml == CK_WALLY ? k.u_wt : 0.0;
                 } else { a4 = a4p; FnS = v.FsSumN; uN = Ra.U[lc]; }
             }
-            const double tterm = (rR + rL) * m.c_t;
+            // unsteady term (rho_i Delta x_i + rho_{i-1} Delta x_{i-1}) Delta y_j / (2 dt) (transposed pl15)
+            const double tterm = NU ? (rR * dx + rL * dxw) * dy * (0.5 * m.inv_dt) : (rR + rL) * m.c_t;
             const double a0 = IMPL ? a1 + a2 + a3 + a4 + FbE - FbW + 0.5 * (FnS - FsS) + tterm
                                    : a1 + a2 + a3 + a4 + tterm;
-            const double b = (s.R1[lc] + s.R1[lc - 1]) * m.c_t * nm.u1c
+            const double b = (NU ? (s.R1[lc] * dx + s.R1[lc - 1] * dxw) * dy * (0.5 * m.inv_dt)
+                                 : (s.R1[lc] + s.R1[lc - 1]) * m.c_t) * nm.u1c
                            + k.B * (v.gcN * (Ra.V[lc] - Ra.V[lc - 1]) - c.gcP * (R0.V[lc] - R0.V[lc - 1])
                                     - 2.0 / 3.0 * gR * (Ra.V[lc] - R0.V[lc])
                                     + 2.0 / 3.0 * gL * (Ra.V[lc - 1] - R0.V[lc - 1]))
-                           + k.g_x * (rR + rL) * m.half_dV;
+                           + (NU ? k.g_x * 0.5 * (rR * dx + rL * dxw) * dy : k.g_x * (rR + rL) * m.half_dV);
             const double r = rcp(a0);
             uhat = (a1 * R0.U[lc - 1] + a2 * R0.U[lc + 1] + a3 * uS + a4 * uN + (IMPL ? b : b + nm.uec)) * r;
-            du = m.A_dy * r;
+            du = (NU ? k.A * dy : m.A_dy) * r;
         }
         v.uhat = uhat;
         v.du = du;
@@ -615,6 +738,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
     v.dvN = 0.0;
     if (vA<REG>(kw1)) {
         const double rB = rP, rT = Ra.R[lc], gB = gP, gT = Ra.G[lc];
+        const double dyT = NU ? g.ya : k.dy;                           // Delta y_{j+1}
         double a1, a2, vW, vE, FwS, FeS;
         if (REG) {
             a1 = v.xvW; FwS = v.FwSum; vW = Ra.V[lc - 1];
@@ -623,17 +747,27 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
             FwS = FeS = 0.0;
             const double gadj = 0.5 * (gB + gT);
             const double zeta = 1.1466 * k.Kn * rcp(0.5 * (rB + rT));
+            const double L = NU ? 0.5 * (dy + dyT) : dy;                   // v-CV height
             if (ckind(R0.KK[lc - 1]) == CK_SOLID && ckind(Ra.KK[lc - 1]) == CK_SOLID) {
-                a1 = k.B * gadj * dy * rcp(0.5 * dx + zeta); vW = 0.0;
+                a1 = k.B * gadj * L * rcp(0.5 * dx + zeta); vW = 0.0;
             } else { a1 = v.xvW; FwS = v.FwSum; vW = Ra.V[lc - 1]; }
             if (ckind(R0.KK[lc + 1]) == CK_SOLID && ckind(Ra.KK[lc + 1]) == CK_SOLID) {
-                a2 = k.B * gadj * dy * rcp(0.5 * dx + zeta); vE = 0.0;
+                a2 = k.B * gadj * L * rcp(0.5 * dx + zeta); vE = 0.0;
             } else { FeS = Fn.FX[lc + 1] + Fc.FX[lc + 1]; a2 = IMPL ? s.XVW[lc + 1] - 0.5 * FeS : s.XVW[lc + 1]; vE = Ra.V[lc + 1]; }
         }
         // corner Gamma (i+1, j+1), recomputed with the same operations as its owner
         double gcE;
         if (REG) {
             gcE = 0.25 * (R0.G[lc] + R0.G[lc + 1] + Ra.G[lc] + Ra.G[lc + 1]);
+        } else if (NU) {
+            const double wxl = wleft(dx, g.dxr[lc + 1]), wxr = 1.0 - wxl;
+            const double wyb = wleft(dy, dyT), wyt = 1.0 - wyb;
+            double sum = 0.0, ws = 0.0;
+            if (!wallish(ckind(R0.KK[lc]))) { sum += wxl * wyb * R0.G[lc]; ws += wxl * wyb; }
+            if (!wallish(ckind(R0.KK[lc + 1]))) { sum += wxr * wyb * R0.G[lc + 1]; ws += wxr * wyb; }
+            if (!wallish(ckind(Ra.KK[lc]))) { sum += wxl * wyt * Ra.G[lc]; ws += wxl * wyt; }
+            if (!wallish(ckind(Ra.KK[lc + 1]))) { sum += wxr * wyt * Ra.G[lc + 1]; ws += wxr * wyt; }
+            gcE = ws > 0.0 ? sum / ws : 0.0;
         } else {
             double sum = 0.0;
             int n = 0;
@@ -644,28 +778,30 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
             gcE = n == 4 ? 0.25 * sum : (n > 0 ? sum / n : 0.0);
         }
         const double a3 = c.vcS, a4 = v.vcN;
-        const double tterm = (rT + rB) * m.c_t;
+        // unsteady term (rho_{j+1} Delta y_{j+1} + rho_j Delta y_j) Delta x_i / (2 dt) (Eq. pl15)
+        const double tterm = NU ? (rT * dyT + rB * dy) * dx * (0.5 * m.inv_dt) : (rT + rB) * m.c_t;
         const double a0 = IMPL ? a1 + a2 + a3 + a4 + 0.5 * (FeS - FwS) + v.FbN - c.FbS + tterm
                                : a1 + a2 + a3 + a4 + tterm;
-        const double b = (v.r1n + s.R1[lc]) * m.c_t * nm.v1n
+        const double b = (NU ? (v.r1n * dyT + s.R1[lc] * dy) * dx * (0.5 * m.inv_dt) : (v.r1n + s.R1[lc]) * m.c_t) * nm.v1n
                        + k.B * (gcE * (Ra.U[lc + 1] - R0.U[lc + 1]) - v.gcN * (Ra.U[lc] - R0.U[lc])
                                 - 2.0 / 3.0 * gT * (Ra.U[lc + 1] - Ra.U[lc])
                                 + 2.0 / 3.0 * gB * (R0.U[lc + 1] - R0.U[lc]))
-                       + k.g_y * (rT + rB) * m.half_dV;
+                       + (NU ? k.g_y * 0.5 * (rT * dyT + rB * dy) * dx : k.g_y * (rT + rB) * m.half_dV);
         const double r = rcp(a0);
         v.vhatN = (a1 * vW + a2 * vE + a3 * R0.V[lc] + a4 * Rb.V[lc] + (IMPL ? b : b + nm.ven)) * r;
-        v.dvN = m.A_dx * r;
+        v.dvN = (NU ? k.A * dx : m.A_dx) * r;
     }
 }
 
 // ================= stage D: p_{i,j} (Eqs. pl23-pl24) =================
-template <bool IMPL, bool TVD, bool REG>
+template <bool IMPL, bool TVD, bool REG, bool NU = false>
 __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
                                         const RingRow& R0, const RingRow& Ra, const FluxRow& Fc,
-                                        const FluxRow& Fn, const Carry& c, StepVars& v)
+                                        const FluxRow& Fn, const Carry& c, StepVars& v, const Geo& g)
 {
     const Params& k = m.k;
-    const double dt = k.dt, dx = k.dx, dy = k.dy;
+    const double dt = k.dt, dx = NU ? g.dxr[lc] : k.dx, dy = NU ? g.y0 : k.dy;
+    const double dV = NU ? dx * dy : m.dV;
     const uint32_t kw0 = R0.KK[lc];
     double pn = R0.P[lc];
     if (cF<REG>(kw0)) {
@@ -698,8 +834,8 @@ __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int 
         }
         // a^p_0 = dV / T_new + dt sum a^p (Eq. pl24, R28); multiplied through by T_new
         // so one reciprocal serves: p = T_new (dt sum + b^p) / (dV + T_new dt sum a^p)
-        const double bp = s.R1[lc] * m.dV - (bpE - bpW + bpN - bpS) * dt;
-        pn = v.TN * (sum * dt + bp) * rcp(fma(v.TN * dt, apW + apE + apS + apN, m.dV));
+        const double bp = s.R1[lc] * dV - (bpE - bpW + bpN - bpS) * dt;
+        pn = v.TN * (sum * dt + bp) * rcp(fma(v.TN * dt, apW + apE + apS + apN, dV));
     }
     v.pn = pn;
     s.PN[lc] = pn;
@@ -778,11 +914,16 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
 // has a register allocation of its own.  REGK = false: every other CTA, with
 // the per-point choice between the instances.  A regular point runs the same
 // instance code in both kernels, so the split never changes a bit.
-template <bool IMPL, bool TVD, bool GRAPH = false, bool REGK = false>
+// NU = true: the non-uniform-mesh kernel: every point runs the
+// general instances in their general-mesh form; the column widths of the ring
+// columns sit behind MarchSmem in shared memory, the row heights come from m.dyp.
+template <bool IMPL, bool TVD, bool GRAPH = false, bool REGK = false, bool NU = false>
 __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
 {
+    static_assert(!(NU && REGK), "non-uniform meshes run the general kernel only");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MarchSmem& s = *reinterpret_cast<MarchSmem*>(smem_raw);
+    double* const s_dx = reinterpret_cast<double*>(smem_raw + sizeof(MarchSmem));   // NU only: RW widths
     const Params& k = m.k;
     if (GRAPH && *(volatile const int*)m.done) return;  // converged earlier in this graph launch (CTA-uniform)
     if (*(volatile const unsigned long long*)m.bad) return;   // a bad state earlier in this advance call
@@ -801,6 +942,8 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
         for (int q = 0; q < RS; q++) mbar_init(&s.mbar[q], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    if (NU)
+        for (int q = t; q < RW; q += MX) s_dx[q] = __ldg(m.dxl + min(max(c0 + q, 0), k.pitch - 1));
     __syncthreads();
     const int gi = I0 - 2 + t;                          // this thread's global column
     const int J0 = ce.y, J1 = ce.z;

@@ -28,7 +28,7 @@ FIELDS = {"u": 0, "v": 1, "p": 2, "T": 3, "rho": 4, "uexp": 6, "vexp": 7, "Texp"
 EXPORTS = ["sts_create", "sts_destroy", "sts_last_error", "sts_set_stream", "sts_init_freestream",
            "sts_set_field", "sts_set_field_device", "sts_advance", "sts_advance_group", "sts_get_field", "sts_get_field_device",
            "sts_get_map", "sts_shape", "sts_constants", "sts_profile", "sts_profile_read", "sts_nccl_unique_id",
-           "sts_plan"]
+           "sts_plan", "sts_set_mesh"]
 
 
 class StsError(RuntimeError):
@@ -122,6 +122,8 @@ def lib():
         L.sts_profile_read.argtypes = [vp, dp, ctypes.c_int32]
         L.sts_nccl_unique_id.restype = st
         L.sts_nccl_unique_id.argtypes = [vp]
+        L.sts_set_mesh.restype = st
+        L.sts_set_mesh.argtypes = [vp, dp, ctypes.c_int64, dp, ctypes.c_int64]
         L.sts_plan.restype = st
         L.sts_plan.argtypes = [ctypes.POINTER(sts_grid), ctypes.POINTER(sts_square), ctypes.c_int32,
                                ctypes.POINTER(sts_gas), ctypes.c_int32, ctypes.c_int32,
@@ -206,6 +208,8 @@ class Solver:
         self.rank, self.world = rank, world
         if stream is not None:
             self.set_stream(stream)
+        if case.get("dxs") is not None or case.get("dys") is not None:
+            self.set_mesh(case.get("dxs"), case.get("dys"))
 
     # --- lifecycle
     def close(self):
@@ -222,6 +226,14 @@ class Solver:
     # --- ABI calls (same names without the prefix)
     def set_stream(self, stream_ptr: int):
         _check(lib().sts_set_stream(self._h, ctypes.c_void_p(stream_ptr)), self._h)
+
+    def set_mesh(self, dxs=None, dys=None):
+        """Non-uniform mesh steps (global dx[nx], dy[ny]; None = uniform spacing)."""
+        self._dxs = None if dxs is None else np.ascontiguousarray(dxs, dtype=np.float64)
+        self._dys = None if dys is None else np.ascontiguousarray(dys, dtype=np.float64)
+        dptr = lambda a: None if a is None else a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        _check(lib().sts_set_mesh(self._h, dptr(self._dxs), 0 if self._dxs is None else self._dxs.size,
+                                  dptr(self._dys), 0 if self._dys is None else self._dys.size), self._h)
 
     def init_freestream(self):
         _check(lib().sts_init_freestream(self._h), self._h)
