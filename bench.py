@@ -158,13 +158,14 @@ def run_reference(args):
     case = W.c3(200, args.variant, passes=args.ref_passes)
     o = oracle.Case(case)
     nfv = W.n_fv(case)
-    for _ in range(args.warmup if args.ref_warmup else 0):
-        o.advance(1)
     times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        o.advance(1)
-        times.append(time.perf_counter() - t0)
+    with _Pinned():
+        for _ in range(args.warmup if args.ref_warmup else 0):
+            o.advance(1)
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            o.advance(1)
+            times.append(time.perf_counter() - t0)
     tot = sum(times)
     value = nfv * args.ref_passes * args.steps / tot
     line = {
@@ -174,7 +175,8 @@ def run_reference(args):
         "data": "synthetic (paper geometry, free-stream IC)",
         "config": {"workload": case["name"] + "_" + args.variant, "nx": case["nx"], "ny": case["ny"],
                    "passes_per_step": args.ref_passes},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu": _cpu_model(),
+                         "nproc": os.cpu_count(), "pinned": "sched_setaffinity to one core",
                          "sample": f"{case['name']} full mesh, {args.ref_passes} loop-2 passes of one time step per bench step, single thread"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -182,18 +184,49 @@ def run_reference(args):
     return 0
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class _Pinned:
+    """Pin this process to one host core (the oracle runs on 1 core,
+    like taskset -c 0) for the duration of a block; restores the affinity."""
+
+    def __enter__(self):
+        self.old = None
+        try:
+            self.old = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, {min(self.old)})
+        except (AttributeError, OSError):
+            pass
+        return self
+
+    def __exit__(self, *a):
+        if self.old is not None:
+            os.sched_setaffinity(0, self.old)
+
+
 def cpu_baseline(variant, seconds_hint=20.0):
-    """Oracle (single thread) on a bounded sample of the bench workload: the full
-    C3 4032 x 4000 mesh, one time step of ONE loop-2 pass."""
+    """Oracle (single thread, pinned to one core) on a bounded sample of the bench
+    workload: the full C3 4032 x 4000 mesh, one time step of ONE loop-2 pass."""
     import oracle
     from paper_1802_04243_b200 import workloads as W
     oracle.build()
     case = W.c3(200, variant, passes=1)
     o = oracle.Case(case)
-    t0 = time.perf_counter()
-    o.advance(1)
-    dt = time.perf_counter() - t0
+    with _Pinned():
+        t0 = time.perf_counter()
+        o.advance(1)
+        dt = time.perf_counter() - t0
     return {"value": W.n_fv(case) / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu": _cpu_model(), "nproc": os.cpu_count(), "pinned": "sched_setaffinity to one core (taskset -c equivalent)",
             "sample": f"{case['name']} full mesh (16.1 M FVs), 1 time step x 1 loop-2 pass, {dt:.1f} s, single thread"}
 
 
@@ -211,6 +244,10 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: every rank on one device (a 2-process check of the N > 1 code path on a
+    # 1-GPU box; the numbers of such a run mean nothing); torch's process group on gloo
+    if os.environ.get("STS_BENCH_ONE_DEVICE"):
+        local = 0
     if world != args.gpus:
         if rank == 0:
             print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
@@ -218,28 +255,51 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     nccl_id = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(S.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tolist())
+        if os.environ.get("STS_BENCH_ONE_DEVICE"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+        if args.halo == "nccl":
+            idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(S.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(idt, 0)
+            nccl_id = bytes(idt.cpu().numpy().tolist())
+
+    def make_solver(case, stream_ptr=None):
+        """One rank's solver; N > 1: the fused halo over peer memory (N1, default)
+        -- blobs of CUDA IPC handles exchanged over the process group -- or NCCL."""
+        g = S.Solver(case, rank=rank, world=world, device=local, nccl_id=nccl_id, stream=stream_ptr)
+        if world > 1 and args.halo == "peer":
+            blobs = [None] * world
+            dist.all_gather_object(blobs, g.peer_export())
+            g.peer_connect(blobs)
+        return g
 
     case = bench_case(args, world)
     stream = torch.cuda.current_stream(dev)
     torch.cuda.synchronize(dev)
     free0 = torch.cuda.mem_get_info(dev)[0]
-    g = S.Solver(case, rank=rank, world=world, device=local, nccl_id=nccl_id, stream=stream.cuda_stream)
+    g = make_solver(case, stream.cuda_stream)
     torch.cuda.synchronize(dev)
     lib_bytes = free0 - torch.cuda.mem_get_info(dev)[0]      # device memory the library holds for this rank
     nfv_rank = g.shape("p")[2] * case["ny"]
     passes = case["max_passes"]
     kind = "implicit" if case["time"] == W.IMPLICIT else "explicit"
 
+    def allmax(x):
+        """max over ranks of a host float (device-timed per rank)"""
+        if world == 1:
+            return float(x)
+        one = os.environ.get("STS_BENCH_ONE_DEVICE")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if one else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     def barrier():
         torch.cuda.synchronize(dev)
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier() if os.environ.get("STS_BENCH_ONE_DEVICE") else dist.barrier(device_ids=[local])
             torch.cuda.synchronize(dev)
 
     # warm-up
@@ -258,10 +318,7 @@ def run_ours(args):
     ms = ev0.elapsed_time(ev1)
     prof = g.profile_read(reset=True)
     g.profile(False)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = allmax(ms)
     total_fvu = nfv_rank * world * passes * args.steps
     value = total_fvu / (ms_max / 1e3)
 
@@ -287,51 +344,58 @@ def run_ours(args):
                 "pass_share_of_step": prof["pass_ms"] / ms if ms > 0 else None,
                 "fp64_pipe_active_ncu": fp64_active}
 
-    # e2e: through the public API with host (pinned) buffers, every step:
-    # H2D of the step's input state (u, v, p, T) + advance + D2H of the residual maxima.
-    # The inputs are double-buffered: the H2D copy of step s+1 runs on a copy
-    # stream while step s computes (the copy of step 0 is inside the timed region too).
+    # e2e: through the public C ABI with HOST buffers, every step: sts_set_field of
+    # the step's input state (u, v, p, T) from pinned host memory (H2D inside the
+    # call), sts_advance (one time step: conv + loop 2), sts_get_field of the new
+    # state (u, v, p, T) into pinned host memory (D2H) -- what a user's time loop
+    # does.  Each call synchronises the stream; nothing overlaps.
     e2e = None
     if not args.no_e2e:
+        import ctypes
         names = ("u", "v", "p", "T")
-        host = {k: torch.from_numpy(g.get_field(k)).pin_memory() for k in names}
-        devb = [{k: torch.empty_like(host[k], device=dev) for k in names} for _ in range(2)]
-        h2d = sum(h.numel() * 8 for h in host.values())
+        L = S.lib()
+        dp = lambda t: ctypes.cast(t.data_ptr(), ctypes.POINTER(ctypes.c_double))
+        hin = {k: torch.from_numpy(g.get_field(k)).pin_memory() for k in names}      # this rank's slab
+        hout = {k: torch.empty_like(hin[k]).pin_memory() for k in names}
+        h2d = sum(h.numel() * 8 for h in hin.values())
         e_steps = max(2, min(args.steps, 6))
-        cstream = torch.cuda.Stream(dev)
-        copied = [torch.cuda.Event() for _ in range(2)]
-        consumed = [torch.cuda.Event() for _ in range(2)]
-
-        def h2d_copy(b):
-            with torch.cuda.stream(cstream):
-                for k in names:
-                    devb[b][k].copy_(host[k], non_blocking=True)
-                copied[b].record(cstream)
-
         barrier()
+        t0 = time.perf_counter()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        cstream.wait_event(e0)
-        h2d_copy(0)
-        for s in range(e_steps):
-            b = s % 2
-            stream.wait_event(copied[b])
+        for _ in range(e_steps):
             for k in names:
-                g.set_field_device(k, devb[b][k].data_ptr(), devb[b][k].numel())
-            consumed[b].record(stream)
-            if s + 1 < e_steps:
-                cstream.wait_event(consumed[1 - b]) if s >= 1 else None
-                h2d_copy(1 - b)
-            g.advance(1)          # reads back the 9 residual slots (72 B) to the host
+                S._check(L.sts_set_field(g._h, S.FIELDS[k], dp(hin[k]), hin[k].numel()), g._h)
+            g.advance(1)
+            for k in names:
+                S._check(L.sts_get_field(g._h, S.FIELDS[k], dp(hout[k]), hout[k].numel()), g._h)
         e1.record(stream)
         barrier()
         ems = e0.elapsed_time(e1)
-        te = torch.tensor([ems], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": nfv_rank * world * passes * e_steps / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": 72 * world, "steps": e_steps,
-               "inputs": "pinned host state copied every step, double-buffered (copy of step s+1 overlaps step s)"}
+        e2e = {"value": nfv_rank * world * passes * e_steps / (allmax(ems) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": h2d * world, "steps": e_steps,
+               "wall_s": time.perf_counter() - t0,
+               "path": "sts_set_field (pinned host -> device) x4, sts_advance(1), sts_get_field (device -> pinned host) x4"}
+
+    # N > 1: built-in decomposition check -- the same transport on a small channel
+    # (C1 geometry stretched to 96 columns per rank), every rank's slab against a
+    # single-slab run on rank 0, bit for bit (DESIGN 7: a cell's arithmetic does
+    # not depend on which slab owns it)
+    decomp = None
+    if world > 1:
+        small = W.channel(96 * world, 40, spacing=0.25, variant=args.variant, passes=4,
+                          squares=[(22 + 96 * q, 18, 4, 4) for q in range(world)])
+        gs = make_solver(small)
+        ref = S.Solver(small, device=local) if rank == 0 else None
+        gs.advance(3)
+        parts = [None] * world
+        dist.all_gather_object(parts, {f: gs.get_field(f) for f in ("u", "v", "p", "T")})
+        if ref is not None:
+            ref.advance(3)
+            decomp = all(np.array_equal(ref.get_field(f), np.concatenate([p_[f] for p_ in parts], axis=1))
+                         for f in ("u", "v", "p", "T"))
+            ref.close()
+        gs.close()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -345,9 +409,11 @@ def run_ours(args):
             "config": {"workload": f"{case['name']}_{args.variant}", "nx": case["nx"], "ny": case["ny"],
                        "fv_per_gpu": nfv_rank, "passes_per_step": passes, "dt": case["dt"],
                        "parallelism": f"x-slabs{world}" if world > 1 else "single",
+                       "halo": (args.halo if world > 1 else None),
                        "l2": "inputs larger than L2 (>= 1.5 GB working set per GPU)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(prof["launches"]), "clocks": clk.summary(),
+            "decomp_bitwise": decomp,
             "hbm_gbs_algorithmic_step": value / world * BYTES_PER_FVU[kind] / 1e9,
             # resident device memory per FV (the paper: 5.9 M FVs per GB, P:708 = 169 B/FV)
             "memory": {"device_bytes_per_gpu": int(lib_bytes), "bytes_per_fv": lib_bytes / nfv_rank,
@@ -376,7 +442,13 @@ def main():
     ap.add_argument("--ref-warmup", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    # N > 1 halo transport: the fused peer-memory path (N1, default) or NCCL send/recv
+    ap.add_argument("--halo", default="peer", choices=["peer", "nccl"])
     args = ap.parse_args()
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # communicator lines in the log (which ranks / devices / transports NCCL set up)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         if args.steps > 5:
             args.steps = 5     # each reference step is ~20 s of single-core work

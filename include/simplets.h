@@ -227,6 +227,27 @@ sts_status sts_constants(sts_ctx* ctx, double* out7);
 sts_status sts_profile(sts_ctx* ctx, int32_t enable);
 sts_status sts_profile_read(sts_ctx* ctx, double* out5, int32_t reset);
 
+/* Fused halo transport: instead of
+ * pack -> NCCL send/recv -> unpack after every pass, the pass kernel's epilogue
+ * (and the explicit-plane kernel's) stores this slab's first / last 4 owned
+ * columns straight into the neighbours' ghost columns of the same snapshot
+ * through peer-mapped memory (NVLink P2P / CUDA IPC), ordered by stream-side
+ * flag writes and waits (cuStreamWriteValue64 / cuStreamWaitValue64); the
+ * residual maxima go to every rank by system-scope atomicMax.  No NCCL call.
+ *  - sts_peer_export: an opaque description of this rank (CUDA IPC handles of
+ *    its snapshots, planes, flag and residual words); blob == NULL returns the
+ *    size in *nbytes.  The caller moves the blobs between processes.
+ *  - sts_peer_connect: blobs = world blobs of nbytes_each bytes, in rank
+ *    order (this rank's own included); for contexts created with world > 1 and
+ *    no nccl_id (one process per rank).  Afterwards sts_advance and
+ *    sts_set_field are collective over the ranks, like the NCCL path.
+ *  - sts_peer_connect_group: the same transport for in-process slab contexts of
+ *    one device (sts_advance_group), with plain device pointers.
+ * Results are bit-identical to the NCCL path and to one slab. */
+sts_status sts_peer_export(sts_ctx* ctx, void* blob, int64_t* nbytes);
+sts_status sts_peer_connect(sts_ctx* ctx, const void* blobs, int64_t nbytes_each);
+sts_status sts_peer_connect_group(sts_ctx** ctxs, int32_t n);
+
 /* rank 0: make the 128-byte NCCL unique id (multi-GPU bootstrap). */
 sts_status sts_nccl_unique_id(void* out128);
 

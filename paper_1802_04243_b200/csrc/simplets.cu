@@ -11,6 +11,7 @@
 #include "sts_march.cuh"
 #include "sts_conv.cuh"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -22,6 +23,7 @@
 #include <cstring>
 #include <string>
 #include <functional>
+#include <mutex>
 #include <queue>
 #include <vector>
 
@@ -132,6 +134,19 @@ struct sts_ctx {
     cudaStream_t stream = nullptr;
     // multi-GPU
     nccl_comm comm = nullptr;
+    // fused halo transport (sts_peer_connect / sts_peer_connect_group):
+    // peer-mapped pointers to the left [0] / right [1] neighbour's snapshots and
+    // explicit planes, and stream-ordered flags instead of pack / NCCL / unpack
+    bool peer = false;
+    Snapshot nb_snap[2][3];
+    double* nb_pl[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};   // ue, ve, Te
+    int nb_pitch[2] = {0, 0}, nb_shift[2] = {0, 0};
+    unsigned long long* flags = nullptr;       // [2 world]: [q] last halo phase of rank q, [world+q] its last residual push
+    std::vector<unsigned long long*> peer_flags;   // every rank's `flags` (peer-mapped; own at [rank])
+    unsigned long long* red_all = nullptr;     // [2][10] residual maxima pushed by every rank (step parity)
+    unsigned long long** d_peer_red = nullptr; // device array: every rank's red_all
+    unsigned long long seq = 0, rseq = 0;      // halo phases / residual pushes issued so far
+    std::vector<void*> ipc_mapped;             // IPC mappings to close
     bool local_group = false;              // world > 1 without NCCL: in-process slabs (sts_advance_group)
     // stats / profiling
     sts_stats stats{};
@@ -291,6 +306,34 @@ __global__ void halo_unpack_kernel(int ny, int pitch, int c0, double* u, double*
         int rows = f == 1 ? ny + 1 : ny;
         if (j < rows) dst[(long long)j * pitch + c0 + i] = buf[e];
     }
+}
+
+// Fused-halo push (N1) of a whole snapshot outside a pass (slab-shaped field
+// input): columns [c0, c0+OFF) of u, v, p, T straight into the neighbour's
+// columns [c0 + shift, ...) of its copy (peer-mapped pointers, pitch npitch).
+__global__ void halo_push_kernel(int ny, int pitch, int c0, const double* u, const double* v, const double* p,
+                                 const double* T, int npitch, int shift, double* nu, double* nv, double* np, double* nT)
+{
+    const int per = OFF * (ny + 1);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 4 * per; e += gridDim.x * blockDim.x) {
+        int f = e / per, r = e - f * per, j = r / OFF, i = r - j * OFF;
+        if (j >= (f == 1 ? ny + 1 : ny)) continue;
+        const double* src = f == 0 ? u : f == 1 ? v : f == 2 ? p : T;
+        double* dst = f == 0 ? nu : f == 1 ? nv : f == 2 ? np : nT;
+        dst[(long long)j * npitch + c0 + i + shift] = src[(long long)j * pitch + c0 + i];
+    }
+}
+// Residual maxima of one pass (9 u64 slots + the sticky bad key) pushed into
+// every rank's red_all by system-scope atomicMax (exact, order-independent:
+// the u64 bit patterns of non-negative doubles order like the doubles).
+__global__ void red_push_kernel(const unsigned long long* slot, const unsigned long long* bad,
+                                unsigned long long** dst, int world, int par)
+{
+    const int q = threadIdx.x;
+    if (q >= world) return;
+    unsigned long long* d = dst[q] + 10 * par;
+    for (int e = 0; e < 9; e++) atomicMax_system(d + e, slot[e]);
+    atomicMax_system(d + 9, *bad);
 }
 
 // ------------------------------------------------------------- kernel table
@@ -668,7 +711,7 @@ static Snapshot pick(sts_ctx* c, int which)
 }
 static sts_status exchange_group(sts_ctx** cs, int n, const int* which, cudaStream_t st)
 {
-    if (cs[0]->world == 1 && !cs[0]->comm) return STS_OK;
+    if ((cs[0]->world == 1 && !cs[0]->comm) || cs[0]->peer) return STS_OK;   // peers: stored in the epilogues
     for (int r = 0; r < n; r++) { sts_status e = halo_pack(cs[r], pick(cs[r], which[r]), st); if (e) return e; }
     if (n == 1) {
         sts_status e = halo_nccl(cs[0], st);
@@ -684,6 +727,113 @@ static sts_status exchange_group(sts_ctx** cs, int n, const int* which, cudaStre
     }
     for (int r = 0; r < n; r++) { sts_status e = halo_unpack(cs[r], pick(cs[r], which[r]), st); if (e) return e; }
     return STS_OK;
+}
+
+// ------------------------------------------------------------- fused halo (N1)
+// Stream-ordered flags over peer memory: every halo phase
+// (explicit planes, loop-2 pass) gets a number q.  Before a phase stores into
+// its neighbours' ghost columns it waits, on its own stream, until both
+// neighbours have finished phase q-1: that covers the neighbour's writes into
+// my ghosts (read now) and its reads of the ghosts I am about to overwrite
+// (both happened in phase q-1 or earlier; interior strips touch no ghost
+// column).  After the phase's edge work the stream writes q into the
+// neighbours' flag word for this rank; the write carries a memory barrier, so
+// the peer stores of the phase are visible first.  No SM waits, no kernel
+// is added, no NCCL call is made.
+typedef CUresult (*pfn_memop64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+static pfn_memop64 g_write64 = nullptr, g_wait64 = nullptr;
+static bool memops_load()
+{
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q1 = cudaDriverEntryPointSymbolNotFound, q2 = cudaDriverEntryPointSymbolNotFound;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", (void**)&g_write64, cudaEnableDefault, &q1) != cudaSuccess ||
+            q1 != cudaDriverEntryPointSuccess)
+            g_write64 = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue64", (void**)&g_wait64, cudaEnableDefault, &q2) != cudaSuccess ||
+            q2 != cudaDriverEntryPointSuccess)
+            g_wait64 = nullptr;
+    });
+    return g_write64 && g_wait64;
+}
+static sts_status peer_wait_rank(sts_ctx* c, int q, int slot_base, unsigned long long v, cudaStream_t s)
+{
+    if (v == 0) return STS_OK;
+    if (g_wait64((CUstream)s, (CUdeviceptr)(c->flags + slot_base + q), v, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        return fail(c, STS_E_COMM, "cuStreamWaitValue64 failed");
+    return STS_OK;
+}
+static sts_status peer_signal_rank(sts_ctx* c, int q, int slot_base, unsigned long long v, cudaStream_t s)
+{
+    if (g_write64((CUstream)s, (CUdeviceptr)(c->peer_flags[q] + slot_base + c->rank), v, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+        return fail(c, STS_E_COMM, "cuStreamWriteValue64 failed");
+    return STS_OK;
+}
+// wait until both neighbours finished halo phase v
+static sts_status peer_wait(sts_ctx* c, unsigned long long v, cudaStream_t s)
+{
+    const int l = left_of(c), r = right_of(c);
+    if (l >= 0) { sts_status e = peer_wait_rank(c, l, 0, v, s); if (e) return e; }
+    if (r >= 0 && r != l) { sts_status e = peer_wait_rank(c, r, 0, v, s); if (e) return e; }
+    return STS_OK;
+}
+// tell both neighbours that this rank finished halo phase v
+static sts_status peer_signal(sts_ctx* c, unsigned long long v, cudaStream_t s)
+{
+    const int l = left_of(c), r = right_of(c);
+    if (l >= 0) { sts_status e = peer_signal_rank(c, l, 0, v, s); if (e) return e; }
+    if (r >= 0 && r != l) { sts_status e = peer_signal_rank(c, r, 0, v, s); if (e) return e; }
+    return STS_OK;
+}
+// The neighbour pointers of one march / conv launch: snapshot `which` of the
+// neighbours (0..2), or their explicit planes (3); none on a physical boundary.
+static void peer_params(const sts_ctx* c, int which, MarchParams& m)
+{
+    for (int sd = 0; sd < 2; sd++) {
+        const int nb = sd == 0 ? left_of(c) : right_of(c);
+        const bool on = c->peer && nb >= 0;
+        if (which == 3) {
+            m.nb_u[sd] = on ? c->nb_pl[sd][0] : nullptr; m.nb_v[sd] = on ? c->nb_pl[sd][1] : nullptr;
+            m.nb_p[sd] = nullptr; m.nb_T[sd] = on ? c->nb_pl[sd][2] : nullptr;
+        } else {
+            m.nb_u[sd] = on ? c->nb_snap[sd][which].u : nullptr; m.nb_v[sd] = on ? c->nb_snap[sd][which].v : nullptr;
+            m.nb_p[sd] = on ? c->nb_snap[sd][which].p : nullptr; m.nb_T[sd] = on ? c->nb_snap[sd][which].T : nullptr;
+        }
+        m.nb_pitch[sd] = c->nb_pitch[sd];
+        m.nb_shift[sd] = c->nb_shift[sd];
+    }
+}
+// A state write outside a pass (sts_set_field, sts_init_freestream) on a
+// peer-connected rank is a halo phase of its own: the neighbours' next pushes
+// into my ghost columns must come after it (they wait for this phase), and
+// mine after theirs.  Every rank makes the same calls (they are collective).
+static sts_status peer_fence(sts_ctx* c)
+{
+    if (!c->peer) return STS_OK;
+    return peer_signal(c, ++c->seq, c->stream);
+}
+// One collective push of a whole snapshot (slab-shaped field input on a
+// peer-connected rank): my edge columns into both neighbours' ghosts, then
+// wait until both neighbours have pushed theirs into mine.
+static sts_status peer_exchange(sts_ctx* ctx, int which, cudaStream_t st)
+{
+    sts_ctx* const c = ctx;
+    const unsigned long long q = ++c->seq;
+    sts_status e = peer_wait(c, q - 1, st);
+    if (e) return e;
+    const Snapshot& s = c->snap[which];
+    const int per = 4 * OFF * (c->ny + 1), blocks = (per + 255) / 256;
+    for (int sd = 0; sd < 2; sd++) {
+        if ((sd == 0 ? left_of(c) : right_of(c)) < 0) continue;
+        const Snapshot& n = c->nb_snap[sd][which];
+        halo_push_kernel<<<blocks, 256, 0, st>>>(c->ny, c->pitch, sd == 0 ? OFF : c->nloc, s.u, s.v, s.p, s.T,
+                                                 c->nb_pitch[sd], c->nb_shift[sd], n.u, n.v, n.p, n.T);
+        c->launches++;
+    }
+    CU(cudaGetLastError());
+    e = peer_signal(c, q, st);
+    if (!e) e = peer_wait(c, q, st);
+    return e;
 }
 
 // ------------------------------------------------------------- ABI
@@ -929,6 +1079,8 @@ extern "C" void sts_destroy(sts_ctx* ctx)
     cudaFree(ctx->ue); cudaFree(ctx->ve); cudaFree(ctx->Te); cudaFree(ctx->stage); cudaFree(ctx->halo);
     cudaFree(ctx->kind32); cudaFree(ctx->cta_order); cudaFree(ctx->cta_split); cudaFree(ctx->red);
     cudaFree(ctx->dxl); cudaFree(ctx->dyp);
+    for (void* p : ctx->ipc_mapped) cudaIpcCloseMemHandle(p);
+    cudaFree(ctx->flags); cudaFree(ctx->red_all); cudaFree(ctx->d_peer_red);
     if (ctx->h_red) cudaFreeHost(ctx->h_red);
     for (cudaGraphExec_t& g : ctx->tol_exec) if (g) cudaGraphExecDestroy(g);
     cudaFree(ctx->red2); cudaFree(ctx->d_ls);
@@ -1023,10 +1175,10 @@ static sts_status set_field_any(sts_ctx* ctx, int field, const double* src, int6
     for (int k = 0; k < 3; k++)
         if (k != ctx->cur)
             CU(cudaMemcpyAsync(field_ptr(ctx->snap[k], field), dst, (size_t)rows * dp, cudaMemcpyDeviceToDevice, ctx->stream));
-    if (slab && ctx->world > 1 && ctx->comm) {
+    if (slab && ctx->world > 1 && (ctx->comm || ctx->peer)) {
         const int which = ctx->cur;
         sts_ctx* one[1] = {ctx};
-        sts_status e = exchange_group(one, 1, &which, ctx->stream);
+        sts_status e = ctx->peer ? peer_exchange(ctx, which, ctx->stream) : exchange_group(one, 1, &which, ctx->stream);
         if (e) return e;
         for (int k = 0; k < 3; k++)        // the exchanged ghost columns into the other snapshots too
             if (k != ctx->cur)
@@ -1035,7 +1187,7 @@ static sts_status set_field_any(sts_ctx* ctx, int field, const double* src, int6
                                        (size_t)(f2 == STS_V ? ctx->ny + 1 : ctx->ny) * dp, cudaMemcpyDeviceToDevice,
                                        ctx->stream));
     }
-    return STS_OK;
+    return peer_fence(ctx);
 }
 
 extern "C" sts_status sts_set_field(sts_ctx* ctx, int32_t field, const double* host, int64_t n)
@@ -1064,6 +1216,8 @@ extern "C" sts_status sts_init_freestream(sts_ctx* ctx)
     CU(cudaMemsetAsync(ctx->ue, 0, cell_elems(ctx) * sizeof(double), ctx->stream));
     CU(cudaMemsetAsync(ctx->ve, 0, v_elems(ctx) * sizeof(double), ctx->stream));
     CU(cudaMemsetAsync(ctx->Te, 0, cell_elems(ctx) * sizeof(double), ctx->stream));
+    sts_status e = peer_fence(ctx);
+    if (e) return e;
     CU(cudaStreamSynchronize(ctx->stream));
     ctx->cur = 0;
     return STS_OK;
@@ -1188,6 +1342,146 @@ extern "C" sts_status sts_set_mesh(sts_ctx* ctx, const double* dx, int64_t nx, c
     return STS_OK;
 }
 
+// ------------------------------------------------------------- fused-halo setup (N1)
+// Opaque per-rank description for sts_peer_connect: the slab geometry and CUDA
+// IPC handles of the three snapshots (u, v, p, T), the explicit planes, the flag
+// words and the pushed residual slots.
+struct PeerBlob {
+    uint32_t magic, version;
+    int32_t rank, world, nloc, pitch, gi0, ny, device, pad;
+    cudaIpcMemHandle_t h[17];
+};
+static constexpr uint32_t PEER_MAGIC = 0x53545331u;   // "STS1"
+
+static sts_status peer_alloc(sts_ctx* ctx)
+{
+    sts_ctx* const c = ctx;
+    if (!memops_load()) return fail(c, STS_E_CUDA, "cuStreamWriteValue64 / cuStreamWaitValue64 unavailable");
+    if (!c->flags) {
+        CU(cudaMalloc(&c->flags, 2 * (size_t)c->world * sizeof(unsigned long long)));
+        CU(cudaMemset(c->flags, 0, 2 * (size_t)c->world * sizeof(unsigned long long)));
+    }
+    if (!c->red_all) {
+        CU(cudaMalloc(&c->red_all, 20 * sizeof(unsigned long long)));
+        CU(cudaMemset(c->red_all, 0, 20 * sizeof(unsigned long long)));
+    }
+    return STS_OK;
+}
+static sts_status peer_finish(sts_ctx* ctx, const std::vector<unsigned long long*>& reds)
+{
+    sts_ctx* const c = ctx;
+    CU(cudaMalloc(&c->d_peer_red, reds.size() * sizeof(unsigned long long*)));
+    CU(cudaMemcpy(c->d_peer_red, reds.data(), reds.size() * sizeof(unsigned long long*), cudaMemcpyHostToDevice));
+    c->peer = true;
+    c->local_group = false;
+    c->seq = c->rseq = 0;
+    // the edge / interior split of every pass (edge strips first, ~15 % shorter)
+    // needs a schedule with edge strips: choose_segments made it at creation
+    return STS_OK;
+}
+
+extern "C" sts_status sts_peer_export(sts_ctx* ctx, void* blob, int64_t* nbytes)
+{
+    if (!ctx || !nbytes) return fail(ctx, STS_E_ARG, "null argument");
+    if (!blob) { *nbytes = (int64_t)sizeof(PeerBlob); return STS_OK; }
+    if (*nbytes < (int64_t)sizeof(PeerBlob)) return fail(ctx, STS_E_ARG, "blob buffer too small");
+    if (ctx->world < 2) return fail(ctx, STS_E_ARG, "peer transport needs world >= 2");
+    CU(cudaSetDevice(ctx->device));
+    sts_status e = peer_alloc(ctx);
+    if (e) return e;
+    PeerBlob b{};
+    b.magic = PEER_MAGIC; b.version = 1;
+    b.rank = ctx->rank; b.world = ctx->world; b.nloc = ctx->nloc; b.pitch = ctx->pitch; b.gi0 = ctx->gi0;
+    b.ny = ctx->ny; b.device = ctx->device;
+    void* ptrs[17];
+    for (int k = 0; k < 3; k++) { ptrs[4 * k] = ctx->snap[k].u; ptrs[4 * k + 1] = ctx->snap[k].v; ptrs[4 * k + 2] = ctx->snap[k].p; ptrs[4 * k + 3] = ctx->snap[k].T; }
+    ptrs[12] = ctx->ue; ptrs[13] = ctx->ve; ptrs[14] = ctx->Te; ptrs[15] = ctx->flags; ptrs[16] = ctx->red_all;
+    for (int q = 0; q < 17; q++) CU(cudaIpcGetMemHandle(&b.h[q], ptrs[q]));
+    memcpy(blob, &b, sizeof b);
+    *nbytes = (int64_t)sizeof b;
+    return STS_OK;
+}
+
+extern "C" sts_status sts_peer_connect(sts_ctx* ctx, const void* blobs, int64_t nbytes_each)
+{
+    if (!ctx || !blobs) return fail(ctx, STS_E_ARG, "null argument");
+    if (nbytes_each != (int64_t)sizeof(PeerBlob)) return fail(ctx, STS_E_ARG, "wrong blob size");
+    if (ctx->world < 2 || ctx->comm) return fail(ctx, STS_E_ARG, "peer transport: world >= 2 and no NCCL communicator");
+    CU(cudaSetDevice(ctx->device));
+    sts_status e = peer_alloc(ctx);
+    if (e) return e;
+    std::vector<PeerBlob> bl(ctx->world);
+    for (int q = 0; q < ctx->world; q++) {
+        memcpy(&bl[q], (const char*)blobs + (size_t)q * sizeof(PeerBlob), sizeof(PeerBlob));
+        if (bl[q].magic != PEER_MAGIC || bl[q].rank != q || bl[q].world != ctx->world || bl[q].ny != ctx->ny)
+            return fail(ctx, STS_E_ARG, "peer blobs must be ranks 0..world-1 of this decomposition");
+    }
+    auto open = [&](const cudaIpcMemHandle_t& h, void** p) -> sts_status {
+        cudaError_t err = cudaIpcOpenMemHandle(p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (err != cudaSuccess) return fail(ctx, STS_E_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(err));
+        ctx->ipc_mapped.push_back(*p);
+        return STS_OK;
+    };
+    ctx->peer_flags.assign(ctx->world, nullptr);
+    std::vector<unsigned long long*> reds(ctx->world, nullptr);
+    for (int q = 0; q < ctx->world; q++) {
+        if (q == ctx->rank) { ctx->peer_flags[q] = ctx->flags; reds[q] = ctx->red_all; continue; }
+        void* p = nullptr;
+        if ((e = open(bl[q].h[15], &p))) return e;
+        ctx->peer_flags[q] = (unsigned long long*)p;
+        if ((e = open(bl[q].h[16], &p))) return e;
+        reds[q] = (unsigned long long*)p;
+    }
+    for (int sd = 0; sd < 2; sd++) {
+        const int nb = sd == 0 ? left_of(ctx) : right_of(ctx);
+        if (nb < 0) continue;
+        if (nb == ctx->rank) return fail(ctx, STS_E_ARG, "a rank cannot be its own neighbour");
+        // the neighbour's element of my local column l: l + shift (DESIGN 7)
+        ctx->nb_pitch[sd] = bl[nb].pitch;
+        ctx->nb_shift[sd] = sd == 0 ? bl[nb].nloc : -ctx->nloc;
+        if (sd == 1 && nb == left_of(ctx)) {       // 2-rank ring: both sides are the same rank
+            ctx->nb_snap[1][0] = ctx->nb_snap[0][0]; ctx->nb_snap[1][1] = ctx->nb_snap[0][1]; ctx->nb_snap[1][2] = ctx->nb_snap[0][2];
+            for (int f = 0; f < 3; f++) ctx->nb_pl[1][f] = ctx->nb_pl[0][f];
+            continue;
+        }
+        void* p[15];
+        for (int q = 0; q < 15; q++) if ((e = open(bl[nb].h[q], &p[q]))) return e;
+        for (int k = 0; k < 3; k++)
+            ctx->nb_snap[sd][k] = Snapshot{(double*)p[4 * k], (double*)p[4 * k + 1], (double*)p[4 * k + 2], (double*)p[4 * k + 3]};
+        for (int f = 0; f < 3; f++) ctx->nb_pl[sd][f] = (double*)p[12 + f];
+    }
+    return peer_finish(ctx, reds);
+}
+
+extern "C" sts_status sts_peer_connect_group(sts_ctx** ctxs, int32_t n)
+{
+    sts_ctx* ctx = nullptr;
+    if (!ctxs || n < 2) return fail(ctx, STS_E_ARG, "bad argument");
+    for (int r = 0; r < n; r++)
+        if (!ctxs[r] || ctxs[r]->world != n || ctxs[r]->rank != r || !ctxs[r]->local_group || ctxs[r]->device != ctxs[0]->device)
+            return fail(ctxs[r], STS_E_ARG, "group must be ranks 0..n-1 of one in-process decomposition on one device");
+    CU(cudaSetDevice(ctxs[0]->device));
+    for (int r = 0; r < n; r++) { sts_status e = peer_alloc(ctxs[r]); if (e) return e; }
+    std::vector<unsigned long long*> reds(n), flags(n);
+    for (int r = 0; r < n; r++) { reds[r] = ctxs[r]->red_all; flags[r] = ctxs[r]->flags; }
+    for (int r = 0; r < n; r++) {
+        sts_ctx* c = ctxs[r];
+        c->peer_flags = flags;
+        for (int sd = 0; sd < 2; sd++) {
+            const int nb = sd == 0 ? left_of(c) : right_of(c);
+            if (nb < 0) continue;
+            c->nb_pitch[sd] = ctxs[nb]->pitch;
+            c->nb_shift[sd] = sd == 0 ? ctxs[nb]->nloc : -c->nloc;
+            for (int k = 0; k < 3; k++) c->nb_snap[sd][k] = ctxs[nb]->snap[k];
+            c->nb_pl[sd][0] = ctxs[nb]->ue; c->nb_pl[sd][1] = ctxs[nb]->ve; c->nb_pl[sd][2] = ctxs[nb]->Te;
+        }
+        sts_status e = peer_finish(c, reds);
+        if (e) return e;
+        c->local_group = true;                      // still driven by sts_advance_group
+    }
+    return STS_OK;
+}
+
 extern "C" sts_status sts_profile(sts_ctx* ctx, int32_t enable)
 {
     if (!ctx) return fail(ctx, STS_E_ARG, "null ctx");
@@ -1239,6 +1533,23 @@ static sts_status gather_red(sts_ctx** cs, int n, int it, unsigned long long* ou
 {
     sts_ctx* ctx = cs[0];
     for (int q = 0; q < 10; q++) out[q] = 0;
+    if (n == 1 && ctx->peer) {
+        // fused path (N1): push my maxima into every rank's slots (system-scope
+        // atomicMax over peer memory), signal every rank, wait for every rank's
+        // push, read my slots; slots alternate by parity, zeroed after reading
+        const int par = (int)(ctx->rseq & 1);
+        const unsigned long long q = ++ctx->rseq;
+        red_push_kernel<<<1, 32, 0, st>>>(ctx->red + (size_t)it * 9, ctx->bad, ctx->d_peer_red, ctx->world, par);
+        ctx->launches++;
+        CU(cudaGetLastError());
+        for (int r = 0; r < ctx->world; r++) { sts_status e = peer_signal_rank(ctx, r, ctx->world, q, st); if (e) return e; }
+        for (int r = 0; r < ctx->world; r++) { sts_status e = peer_wait_rank(ctx, r, ctx->world, q, st); if (e) return e; }
+        CU(cudaMemcpyAsync(ctx->h_red, ctx->red_all + 10 * par, 10 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CU(cudaMemsetAsync(ctx->red_all + 10 * par, 0, 10 * sizeof(unsigned long long), st));
+        CU(cudaStreamSynchronize(st));
+        for (int q2 = 0; q2 < 10; q2++) out[q2] = ctx->h_red[q2];
+        return STS_OK;
+    }
     if (n == 1 && ctx->comm) {
         unsigned long long* slot = ctx->red + (size_t)it * 9;
         if (g_nccl.AllReduce(slot, slot, 9, NCCL_UINT64, NCCL_MAX, ctx->comm, st)) return fail(ctx, STS_E_COMM, "ncclAllReduce");
@@ -1505,7 +1816,16 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                 k.ue_w = c->ue; k.ve_w = c->ve; k.Te_w = c->Te;
                 prof_begin(c, 1);
                 const dim3 mgrid(c->n_gen + c->n_reg);                 // the conv kernel: every CTA of the schedule
-                conv_march_table(tvd, c->nu)<<<mgrid, MX, conv_smem(c), st>>>(make_march(c, k));
+                MarchParams mc = make_march(c, k);
+                unsigned long long q = 0;
+                if (c->peer) {                                         // fused halo: planes stored into the neighbours
+                    q = ++c->seq;
+                    sts_status e = peer_wait(c, q - 1, st);
+                    if (e) return e;
+                    peer_params(c, 3, mc);
+                }
+                conv_march_table(tvd, c->nu)<<<mgrid, MX, conv_smem(c), st>>>(mc);
+                if (c->peer) { sts_status e = peer_signal(c, q, st); if (e) return e; }
                 prof_end(c);
                 c->launches++;
                 CU(cudaGetLastError());
@@ -1524,7 +1844,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
         // slab groups launch the same two CTA sets one after the other.
         const bool split = (ctx->world > 1 || ctx->comm) && ctx->n_edge > 0 &&
                            ctx->n_edge < ctx->n_split && !getenv("STS_NO_SPLIT");
-        const bool overlap = split && n == 1 && ctx->comm;
+        const bool overlap = split && n == 1 && (ctx->comm || ctx->peer);
         if (overlap) {
             if (!ctx->hstream) {
                 int lo = 0, hi = 0;
@@ -1552,8 +1872,16 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                     cudaStream_t as = overlap ? c->hstream : st;
                     if (overlap && it > 0) CU(cudaStreamWaitEvent(as, c->ev_b, 0));   // pass it-1 complete
                     prof_begin(c, 0);
+                    unsigned long long q = 0;
+                    if (c->peer) {              // fused halo: the edge strips store into the neighbours
+                        q = ++c->seq;
+                        sts_status e = peer_wait(c, q - 1, as);
+                        if (e) return e;
+                        peer_params(c, nw[r], ma);
+                    }
                     march_fn gen = gk ? march_graph_table(impl, tvd, 0, c->nu) : march_table(impl, tvd, 0, c->nu);
                     gen<<<c->n_edge, MX, march_smem(c), as>>>(ma);
+                    if (c->peer) { sts_status e = peer_signal(c, q, as); if (e) return e; }
                     if (overlap) CU(cudaEventRecord(c->ev_a[it & 1], as));
                     c->launches += 1 + launch_march(c, mb, gk, st, c->cta_split + 4 * c->n_edge, c->n_split_gen,
                                                     c->n_split - c->n_edge - c->n_split_gen);
@@ -1561,10 +1889,12 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                         CU(cudaStreamWaitEvent(st, c->ev_a[it & 1], 0));   // the pass ends with both sets
                         prof_end(c);
                         CU(cudaEventRecord(c->ev_b, st));
-                        sts_status e = halo_pack(c, c->snap[nw[r]], as);
-                        if (!e) e = halo_nccl(c, as);
-                        if (!e) e = halo_unpack(c, c->snap[nw[r]], as);
-                        if (e) return e;
+                        if (!c->peer) {
+                            sts_status e = halo_pack(c, c->snap[nw[r]], as);
+                            if (!e) e = halo_nccl(c, as);
+                            if (!e) e = halo_unpack(c, c->snap[nw[r]], as);
+                            if (e) return e;
+                        }
                     } else {
                         prof_end(c);
                     }
@@ -1573,7 +1903,15 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                     MarchParams mk = make_march(c, k);
                     mk.pass_key = pkey;
                     if (gk) mk.done = &c->d_ls->done;
+                    unsigned long long q = 0;
+                    if (c->peer) {              // no edge / interior split (narrow slab): the whole pass
+                        q = ++c->seq;
+                        sts_status e = peer_wait(c, q - 1, st);
+                        if (e) return e;
+                        peer_params(c, nw[r], mk);
+                    }
                     c->launches += launch_march(c, mk, gk, st, c->cta_order, c->n_gen, c->n_reg);
+                    if (c->peer) { sts_status e = peer_signal(c, q, st); if (e) return e; }
                     prof_end(c);
                 }
                 CU(cudaGetLastError());

@@ -63,8 +63,36 @@ struct MarchParams {
     // -PADY .. ny+PADY-1 at dyp[j + PADY] (rows beyond a wall take the wall row's step)
     const double* dxl;
     const double* dyp;
+    // fused halo: the pass epilogue also stores this slab's first /
+    // last OFF owned columns of u, v, p, T (the conv kernel: u^exp, v^exp, T^exp)
+    // straight into the ghost columns of the left [0] / right [1] neighbour's copy of
+    // the same snapshot -- peer-mapped pointers (NVLink P2P, CUDA IPC, or the same
+    // device for in-process slabs), null = no such neighbour.  Neighbour element of
+    // local (row j, column l): j * nb_pitch + l + nb_shift.
+    double* nb_u[2];
+    double* nb_v[2];
+    double* nb_p[2];
+    double* nb_T[2];
+    int nb_pitch[2], nb_shift[2];
 };
 constexpr int PADY = 4;
+
+// Store one point's new values into the neighbours' ghost columns (fused halo):
+// the first OFF owned columns go left, the last OFF right (both when the slab is
+// narrower than 2 OFF).  Cells that are not fluid keep their p, T everywhere.
+__device__ __forceinline__ void halo_store(const MarchParams& m, int j, int col, bool fluid,
+                                           double u, double v, double p, double T)
+{
+#pragma unroll
+    for (int sd = 0; sd < 2; sd++) {
+        if (m.nb_u[sd] && (sd == 0 ? col < 2 * OFF : col >= m.k.nloc)) {
+            const long long id = (long long)j * m.nb_pitch[sd] + col + m.nb_shift[sd];
+            m.nb_u[sd][id] = u;
+            m.nb_v[sd][id] = v;
+            if (fluid) { m.nb_p[sd][id] = p; m.nb_T[sd][id] = T; }
+        }
+    }
+}
 
 // Mesh steps around a point of a non-uniform mesh: the column widths of the
 // CTA's ring columns (shared memory, ring column index) and the heights of
@@ -853,7 +881,7 @@ __host__ __device__ __forceinline__ unsigned long long bad_key(int pass_key, lon
 }
 
 // ================= stage E: corrections, writes, residuals =================
-template <bool IMPL, bool TVD, bool REG>
+template <bool IMPL, bool TVD, bool REG, bool HALO = false>
 __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int lc, int gi, int j,
                                         const RingRow& R0, const Carry& c, const StepVars& v, Resid& rs)
 {
@@ -889,6 +917,7 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
         rs.nanv |= vn != vn;
     }
     k.v_w[id] = vn;
+    if (HALO) halo_store(m, j, gi - k.gi0 + OFF, fluid, un, vn, v.pn, v.TN);   // fused halo (N1)
     if (!REG && k.xbc == 0 && gi == k.nx - 1) {
         k.u_w[id + 1] = R0.U[lc];                    // outlet face: u_old(nx-1), BC spec 3
         const double pv = fluid ? v.pn : R0.P[lc];

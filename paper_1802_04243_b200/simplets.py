@@ -28,7 +28,7 @@ FIELDS = {"u": 0, "v": 1, "p": 2, "T": 3, "rho": 4, "uexp": 6, "vexp": 7, "Texp"
 EXPORTS = ["sts_create", "sts_destroy", "sts_last_error", "sts_set_stream", "sts_init_freestream",
            "sts_set_field", "sts_set_field_device", "sts_advance", "sts_advance_group", "sts_get_field", "sts_get_field_device",
            "sts_get_map", "sts_shape", "sts_constants", "sts_profile", "sts_profile_read", "sts_nccl_unique_id",
-           "sts_plan", "sts_set_mesh"]
+           "sts_plan", "sts_set_mesh", "sts_peer_export", "sts_peer_connect", "sts_peer_connect_group"]
 
 
 class StsError(RuntimeError):
@@ -124,6 +124,12 @@ def lib():
         L.sts_nccl_unique_id.argtypes = [vp]
         L.sts_set_mesh.restype = st
         L.sts_set_mesh.argtypes = [vp, dp, ctypes.c_int64, dp, ctypes.c_int64]
+        L.sts_peer_export.restype = st
+        L.sts_peer_export.argtypes = [vp, vp, i64p]
+        L.sts_peer_connect.restype = st
+        L.sts_peer_connect.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
+        L.sts_peer_connect_group.restype = st
+        L.sts_peer_connect_group.argtypes = [ctypes.POINTER(vp), ctypes.c_int32]
         L.sts_plan.restype = st
         L.sts_plan.argtypes = [ctypes.POINTER(sts_grid), ctypes.POINTER(sts_square), ctypes.c_int32,
                                ctypes.POINTER(sts_gas), ctypes.c_int32, ctypes.c_int32,
@@ -145,6 +151,13 @@ def advance_group(solvers, n_steps):
     st = sts_stats()
     _check(lib().sts_advance_group(arr, n, int(n_steps), ctypes.byref(st)), solvers[0]._h)
     return {"steps_done": st.steps_done, "passes_done": st.passes_done, "res": list(st.res), "converged": st.converged}
+
+
+def peer_connect_group(solvers):
+    """Fused halo (N1) for in-process slab contexts: the pass epilogues store the
+    edge columns straight into the neighbours' ghost columns (same device)."""
+    arr = (ctypes.c_void_p * len(solvers))(*[s._h for s in solvers])
+    _check(lib().sts_peer_connect_group(arr, len(solvers)), solvers[0]._h)
 
 
 def _structs(case: dict):
@@ -234,6 +247,19 @@ class Solver:
         dptr = lambda a: None if a is None else a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         _check(lib().sts_set_mesh(self._h, dptr(self._dxs), 0 if self._dxs is None else self._dxs.size,
                                   dptr(self._dys), 0 if self._dys is None else self._dys.size), self._h)
+
+    def peer_export(self) -> bytes:
+        """This rank's description for the fused halo transport (CUDA IPC handles)."""
+        n = ctypes.c_int64(0)
+        _check(lib().sts_peer_export(self._h, None, ctypes.byref(n)), self._h)
+        buf = ctypes.create_string_buffer(n.value)
+        _check(lib().sts_peer_export(self._h, buf, ctypes.byref(n)), self._h)
+        return buf.raw[:n.value]
+
+    def peer_connect(self, blobs):
+        """Attach to the other ranks (blobs of ranks 0..world-1 from peer_export)."""
+        size = len(blobs[0])
+        _check(lib().sts_peer_connect(self._h, b"".join(blobs), size), self._h)
 
     def init_freestream(self):
         _check(lib().sts_init_freestream(self._h), self._h)

@@ -185,3 +185,55 @@ def test_allreg_loop_bitwise(S, variant):
     for f in FIELDS:
         assert np.array_equal(out[0][f], out[1][f]), f
         assert np.array_equal(out[0][f], out[2][f]), f
+
+
+def _peer_group(S, case, k, steps, seed=3):
+    """k in-process slabs with the fused halo transport (N1): global fields."""
+    ref = S.Solver(case)
+    st = W.perturbed_state({f: ref.get_field(f) for f in FIELDS}, W.perturbation(case, seed), vscale=0.05)
+    group = [S.Solver(case, rank=r, world=k) for r in range(k)]
+    S.peer_connect_group(group)
+    for g in [ref] + group:
+        for f in ("p", "T", "u", "v"):
+            g.set_field(f, st[f])
+    ref.advance(steps)
+    S.advance_group(group, steps)
+    return ref, {f: np.concatenate([g.get_field(f) for g in group], axis=1) for f in FIELDS}, group
+
+
+@pytest.mark.parametrize("variant", list(W.VARIANTS))
+@pytest.mark.parametrize("k", [2, 3])
+def test_peer_group_bitwise(S, variant, k):
+    """Fused halo: the pass and explicit-plane epilogues store the
+    edge columns straight into the neighbours' ghost columns (in-process slabs on
+    one device: plain device pointers, the same stream-ordered flags as across
+    processes).  Bit-identical to one slab, with no pack / copy / unpack launch."""
+    case = W.c1(variant, passes=4)
+    ref, got, group = _peer_group(S, case, k, steps=3)
+    for f in FIELDS:
+        assert np.array_equal(ref.get_field(f), got[f]), (f, np.abs(ref.get_field(f) - got[f]).max())
+
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_peer_group_periodic_bitwise(S, k):
+    """The same on a periodic channel (ring neighbours; k = 2: both neighbours are
+    the same rank)."""
+    case = W.c2(small=True, variant="explicit_tvd", passes=4)
+    ref, got, _ = _peer_group(S, case, k, steps=3)
+    for f in FIELDS:
+        assert np.array_equal(ref.get_field(f), got[f]), f
+
+
+def test_peer_group_no_halo_launches(S):
+    """The fused transport adds no kernel launch per pass: the launches of a peer
+    group equal the march launches alone (edge + interior sets per slab)."""
+    case = W.c1("implicit_upwind", passes=4)
+    group = [S.Solver(case, rank=r, world=2) for r in range(2)]
+    S.peer_connect_group(group)
+    for g in group:
+        g.profile(True)
+        g.profile_read(reset=True)
+    S.advance_group(group, 2)
+    for g in group:
+        prof = g.profile_read(reset=True)
+        assert prof["launches"] <= 3 * prof["pass_launches"], prof     # edge + general + regular sets only
