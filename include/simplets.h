@@ -99,13 +99,20 @@ typedef struct {
 
 /* Scheme and loop-2 control (Figs. 1-2): time step dt > 0; per time step
  * loop 2 runs until the four residuals (DESIGN R35) are < tol after at least
- * min_passes passes, or exactly max_passes passes when tol <= 0. */
+ * min_passes passes, or exactly max_passes passes when tol <= 0.
+ * loop3: energy / pressure sweeps per loop-2 pass -- 0 or 1 is the GPU column
+ * of Figs. 1-2; k > 1 adds the CPU column's loop 3 ("calculate the
+ * coupled equations for energy and pressure") as
+ * k-1 Jacobi sweeps over the T-p coupled terms (reading R41, DESIGN 3.6).
+ * loop3 > 1 runs on single-rank, uniform-mesh contexts (else STS_E_CONFIG). */
 typedef struct {
     int32_t time;                /* sts_time_scheme  */
     int32_t space;               /* sts_space_scheme */
     double dt;
     int32_t min_passes, max_passes;
     double tol;
+    int32_t loop3;               /* T-p sweeps per pass (N3); 0 / 1 = off */
+    int32_t reserved;            /* must be 0 */
 } sts_scheme;
 
 /* Multi-GPU: one process per GPU; the channel is split into slabs along x

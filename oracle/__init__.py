@@ -53,6 +53,7 @@ class Params(ctypes.Structure):
         ("dt", ctypes.c_double),
         ("min_passes", ctypes.c_int32), ("max_passes", ctypes.c_int32),
         ("tol", ctypes.c_double),
+        ("loop3", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
 
@@ -131,6 +132,7 @@ class Case:
         p.dt = case["dt"]
         p.min_passes, p.max_passes = case.get("min_passes", 1), case["max_passes"]
         p.tol = case.get("tol", 0.0)
+        p.loop3 = int(case.get("loop3", 1))
         self.nx, self.ny = p.nx, p.ny
         sq = np.ascontiguousarray(np.asarray(case.get("squares", []), dtype=np.int32).reshape(-1, 4))
         self._sq = sq

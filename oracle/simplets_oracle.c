@@ -45,11 +45,17 @@ struct orc_case {
     double *ue, *ve, *Te;        /* explicit planes       */
     double *uh, *du, *vh, *dv;   /* phase-A pseudo-velocities            */
     double *dxs, *dys;           /* per-column / per-row steps, NULL = uniform */
+    level L3;                    /* loop 3 (N3): the previous T-p iterate of the pass */
+    const level* it3;            /* the level the coupled T-p terms read: OLD, or &L3 */
 };
 
 #define N1 (&c->L[0])
 #define OLD (&c->L[1])
 #define NEW (&c->L[2])
+/* The T-p coupled quantities of the energy and pressure equations (reading R41):
+ * the old iterate in the GPU column, the previous loop-3 iterate in
+ * the CPU column's loop 3. */
+#define TP3 (c->it3 ? c->it3 : OLD)
 
 /* ---------------------------------------------------------------- indices */
 static int IC(const orc_case* c, int i, int j) { return j * c->nx + i; }
@@ -378,13 +384,14 @@ static double face_interp(double fa, double fb, double da, double db)
 static double pressure_work(const orc_case* c, int i, int j, double div)
 {
     const level* o = OLD;
-    const double pc = PP(o, i, j);
+    const level* q = TP3;                          /* pressure of the T-p iterate (R41) */
+    const double pc = PP(q, i, j);
     if (c->P.pw_form != ORC_PW_DPDT) return c->PWK * pc * div;
     const double dx = DX(c, i), dy = DY(c, j);
-    double pe = is_wallish(c, i + 1, j) ? pc : face_interp(pc, PP(o, i + 1, j), dx, DX(c, i + 1));
-    double pw = is_wallish(c, i - 1, j) ? pc : face_interp(PP(o, i - 1, j), pc, DX(c, i - 1), dx);
-    double pn = is_wallish(c, i, j + 1) ? pc : face_interp(pc, PP(o, i, j + 1), dy, DY(c, j + 1));
-    double ps = is_wallish(c, i, j - 1) ? pc : face_interp(PP(o, i, j - 1), pc, DY(c, j - 1), dy);
+    double pe = is_wallish(c, i + 1, j) ? pc : face_interp(pc, PP(q, i + 1, j), dx, DX(c, i + 1));
+    double pw = is_wallish(c, i - 1, j) ? pc : face_interp(PP(q, i - 1, j), pc, DX(c, i - 1), dx);
+    double pn = is_wallish(c, i, j + 1) ? pc : face_interp(pc, PP(q, i, j + 1), dy, DY(c, j + 1));
+    double ps = is_wallish(c, i, j - 1) ? pc : face_interp(PP(q, i, j - 1), pc, DY(c, j - 1), dy);
     double ub = 0.5 * (U(c, o, i, j) + U(c, o, i + 1, j));
     double vb = 0.5 * (V(c, o, i, j) + V(c, o, i, j + 1));
     double dpdt = (pc - PP(N1, i, j)) / c->P.dt;
@@ -418,6 +425,7 @@ static double T_equation(const orc_case* c, int i, int j)
     const level* n1 = N1;
     const int impl = implicit_(c);
     const double dx = DX(c, i), dy = DY(c, j), dt = c->P.dt;
+    const level* q = TP3;                       /* T-p coupled values (R41): old iterate, or loop 3 */
     const double gP = GAM(o, i, j), rP = RHO(o, i, j);
     double a1, a2, a3, a4, T1, T2, T3, T4;
     double FW = 0, FE = 0, FS = 0, FN = 0;
@@ -429,7 +437,7 @@ static double T_equation(const orc_case* c, int i, int j)
         FW = Fx(c, o, i, j);
         double D = c->CT1 * harmonic(GAM(o, i - 1, j), gP, DX(c, i - 1), dx) * dy / (0.5 * (dx + DX(c, i - 1)));
         a1 = (impl ? max0(FW) - FW * psis_cell_x(c, o, C_T, i, j, U(c, o, i, j)) : 0.0) + D;
-        T1 = TT(o, i - 1, j);
+        T1 = TT(q, i - 1, j);
     }
     /* a^T_2: east, D^Tx_{i+1,j} */
     if (is_wallish(c, i + 1, j)) {
@@ -438,7 +446,7 @@ static double T_equation(const orc_case* c, int i, int j)
         FE = Fx(c, o, i + 1, j);
         double D = c->CT1 * harmonic(gP, GAM(o, i + 1, j), dx, DX(c, i + 1)) * dy / (0.5 * (DX(c, i + 1) + dx));
         a2 = (impl ? max0(-FE) - FE * psis_cell_x(c, o, C_T, i + 1, j, U(c, o, i + 1, j)) : 0.0) + D;
-        T2 = TT(o, i + 1, j);
+        T2 = TT(q, i + 1, j);
     }
     /* a^T_3: south, D^Ty_{i,j} */
     if (is_wallish(c, i, j - 1)) {
@@ -447,7 +455,7 @@ static double T_equation(const orc_case* c, int i, int j)
         FS = Fy(c, o, i, j);
         double D = c->CT1 * harmonic(GAM(o, i, j - 1), gP, DY(c, j - 1), dy) * dx / (0.5 * (dy + DY(c, j - 1)));
         a3 = (impl ? max0(FS) - FS * psis_cell_y(c, o, C_T, i, j, V(c, o, i, j)) : 0.0) + D;
-        T3 = TT(o, i, j - 1);
+        T3 = TT(q, i, j - 1);
     }
     /* a^T_4: north, D^Ty_{i,j+1} */
     if (is_wallish(c, i, j + 1)) {
@@ -456,12 +464,13 @@ static double T_equation(const orc_case* c, int i, int j)
         FN = Fy(c, o, i, j + 1);
         double D = c->CT1 * harmonic(gP, GAM(o, i, j + 1), dy, DY(c, j + 1)) * dx / (0.5 * (DY(c, j + 1) + dy));
         a4 = (impl ? max0(-FN) - FN * psis_cell_y(c, o, C_T, i, j + 1, V(c, o, i, j + 1)) : 0.0) + D;
-        T4 = TT(o, i, j + 1);
+        T4 = TT(q, i, j + 1);
     }
 
     double a0;
-    if (impl) a0 = dt * (a1 + a2 + a3 + a4 + FE - FW + FN - FS) + rP * dx * dy;   /* pl31 */
-    else      a0 = dt * (a1 + a2 + a3 + a4) + rP * dx * dy;                       /* pl31_1 */
+    const double rq = RHO(q, i, j);             /* rho of the unsteady term: p/T of the T-p iterate */
+    if (impl) a0 = dt * (a1 + a2 + a3 + a4 + FE - FW + FN - FS) + rq * dx * dy;   /* pl31 */
+    else      a0 = dt * (a1 + a2 + a3 + a4) + rq * dx * dy;                       /* pl31_1 */
 
     /* S^T_c, Eq. pl29; mid-face velocities by bilinear
      * interpolation between the four neighbouring nodes (R4): the face
@@ -861,10 +870,11 @@ static double p_equation(const orc_case* c, int i, int j)
     double bp = PP(n1, i, j) / TT(n1, i, j) * dx * dy - (bpE - bpW + bpN - bpS) * dt;
     /* neighbour p_old only through active faces (BC spec 9: a^p = 0 elsewhere) */
     double sum = 0.0;
-    if (kw == F_ACTIVE) sum += apW * PP(o, i - 1, j);
-    if (ke == F_ACTIVE) sum += apE * PP(o, i + 1, j);
-    if (vkind(c, i, j) == F_ACTIVE) sum += apS * PP(o, i, j - 1);
-    if (vkind(c, i, j + 1) == F_ACTIVE) sum += apN * PP(o, i, j + 1);
+    const level* q = TP3;                       /* neighbour pressures: old iterate, or loop 3 (R41) */
+    if (kw == F_ACTIVE) sum += apW * PP(q, i - 1, j);
+    if (ke == F_ACTIVE) sum += apE * PP(q, i + 1, j);
+    if (vkind(c, i, j) == F_ACTIVE) sum += apS * PP(q, i, j - 1);
+    if (vkind(c, i, j + 1) == F_ACTIVE) sum += apN * PP(q, i, j + 1);
     return (sum * dt + bp) / a0;
 }
 
@@ -897,6 +907,28 @@ static int one_pass(orc_case* c, double* res)
     for (int j = 0; j < ny; j++)
         for (int i = 0; i < nx; i++)
             nw->p[IC(c, i, j)] = is_fluid(c, i, j) ? p_equation(c, i, j) : o->p[IC(c, i, j)];
+    /* loop 3 of the CPU column (Figs. 1-2, reading R41):
+     * sweeps k = 2 .. loop3 repeat the coupled energy / pressure pair with the
+     * T-p terms at the previous sweep's iterate (Jacobi): the energy equation's
+     * neighbour temperatures, unsteady density p/T and pressure work, and the
+     * pressure equation's neighbour pressures; every other coefficient (fluxes,
+     * limiters, links, Gamma, viscous heating, u-hat, d) stays the old iterate's. */
+    for (int k = 2; k <= c->P.loop3; k++) {
+        const size_t nc = (size_t)nx * ny;
+        for (size_t e = 0; e < nc; e++) {
+            c->L3.p[e] = nw->p[e];
+            c->L3.T[e] = nw->T[e];
+            c->L3.rho[e] = c->solid[e] ? o->rho[e] : nw->p[e] / nw->T[e];
+        }
+        c->it3 = &c->L3;
+        for (int j = 0; j < ny; j++)
+            for (int i = 0; i < nx; i++)
+                if (is_fluid(c, i, j)) nw->T[IC(c, i, j)] = T_equation(c, i, j);
+        for (int j = 0; j < ny; j++)
+            for (int i = 0; i < nx; i++)
+                if (is_fluid(c, i, j)) nw->p[IC(c, i, j)] = p_equation(c, i, j);
+        c->it3 = NULL;
+    }
     /* phase C: velocity correction (pl18, pl19), EOS (pl5), Gamma (pl37) */
     for (int j = 0; j < ny; j++)
         for (int i = 0; i <= nx; i++) {
@@ -1022,7 +1054,8 @@ static void free_level(level* l)
 orc_case* orc_create(const orc_params* prm, const int32_t* squares, int32_t n_sq)
 {
     if (!prm || prm->nx < 1 || prm->ny < 1 || !(prm->dx > 0) || !(prm->dy > 0) || !(prm->Kn > 0) ||
-        !(prm->dt > 0) || prm->max_passes < 1 || prm->pw_form < ORC_PW_DPDT || prm->pw_form > ORC_PW_GAMMA)
+        !(prm->dt > 0) || prm->max_passes < 1 || prm->pw_form < ORC_PW_DPDT || prm->pw_form > ORC_PW_GAMMA ||
+        prm->loop3 < 0)
         return NULL;
     orc_case* c = calloc(1, sizeof *c);
     c->P = *prm;
@@ -1051,6 +1084,7 @@ orc_case* orc_create(const orc_params* prm, const int32_t* squares, int32_t n_sq
             for (int i = i0; i < i0 + ni; i++) c->solid[IC(c, i, j)] = 1;
     }
     for (int k = 0; k < 3; k++) alloc_level(c, &c->L[k]);
+    if (prm->loop3 > 1) alloc_level(c, &c->L3);
     size_t nu = (size_t)(c->nx + 1) * c->ny, nv = (size_t)c->nx * (c->ny + 1), nc = (size_t)c->nx * c->ny;
     c->ue = calloc(nu, sizeof(double)); c->ve = calloc(nv, sizeof(double)); c->Te = calloc(nc, sizeof(double));
     c->uh = calloc(nu, sizeof(double)); c->du = calloc(nu, sizeof(double));
@@ -1063,6 +1097,7 @@ void orc_destroy(orc_case* c)
 {
     if (!c) return;
     for (int k = 0; k < 3; k++) free_level(&c->L[k]);
+    free_level(&c->L3);
     free(c->ue); free(c->ve); free(c->Te); free(c->uh); free(c->du); free(c->vh); free(c->dv);
     free(c->solid);
     free(c->dxs); free(c->dys);

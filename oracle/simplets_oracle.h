@@ -58,6 +58,10 @@ typedef struct {
     double  dt;               /* time step                                     */
     int32_t min_passes, max_passes;
     double  tol;              /* <= 0 -> exactly max_passes per step           */
+    int32_t loop3;            /* T-p sweeps per pass (loop 3 of the CPU column,
+                                 Figs. 1-2, reading R41); 0 or 1 =
+                                 the GPU column (one energy / pressure pair)    */
+    int32_t reserved;
 } orc_params;
 
 typedef struct orc_case orc_case;

@@ -147,6 +147,10 @@ struct sts_ctx {
     unsigned long long** d_peer_red = nullptr; // device array: every rank's red_all
     unsigned long long seq = 0, rseq = 0;      // halo phases / residual pushes issued so far
     std::vector<void*> ipc_mapped;             // IPC mappings to close
+    // loop 3 (N3, sch.loop3 > 1): T-p sweep iterates (ping-pong), a junk target for
+    // the u, v of the non-final sweeps, junk residual slots + bad key
+    double *l3p[2] = {nullptr, nullptr}, *l3T[2] = {nullptr, nullptr}, *l3junk = nullptr;
+    unsigned long long* l3red = nullptr;
     bool local_group = false;              // world > 1 without NCCL: in-process slabs (sts_advance_group)
     // stats / profiling
     sts_stats stats{};
@@ -339,8 +343,16 @@ __global__ void red_push_kernel(const unsigned long long* slot, const unsigned l
 // ------------------------------------------------------------- kernel table
 typedef void (*march_fn)(MarchParams);
 // regk: the all-regular kernel (sts_march.cuh); nu: the non-uniform-mesh kernel
-static march_fn march_table(int impl, int tvd, int regk, int nu = 0)
+static march_fn march_table(int impl, int tvd, int regk, int nu = 0, int l3 = 0)
 {
+    if (l3) {                                    // loop-3 sweeps k >= 2 (N3)
+        if (regk) {
+            if (impl) return tvd ? march_kernel<true, true, false, true, false, true> : march_kernel<true, false, false, true, false, true>;
+            return tvd ? march_kernel<false, true, false, true, false, true> : march_kernel<false, false, false, true, false, true>;
+        }
+        if (impl) return tvd ? march_kernel<true, true, false, false, false, true> : march_kernel<true, false, false, false, false, true>;
+        return tvd ? march_kernel<false, true, false, false, false, true> : march_kernel<false, false, false, false, false, true>;
+    }
     if (nu) {
         if (impl) return tvd ? march_kernel<true, true, false, false, true> : march_kernel<true, false, false, false, true>;
         return tvd ? march_kernel<false, true, false, false, true> : march_kernel<false, false, false, false, true>;
@@ -383,10 +395,12 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
     static std::atomic<unsigned long long> done_mask{0};
     const unsigned long long bit = 1ull << (ctx->device & 63);
     if (done_mask.load() & bit) return STS_OK;
-    for (int q = 0; q < 32; q++) {
-        const int impl = q & 1, tvd = (q >> 1) & 1, regk = (q >> 2) & 1, graph = (q >> 3) & 1, nu = q >> 4;
-        if (nu && regk) continue;
-        march_fn f = graph ? march_graph_table(impl, tvd, regk, nu) : march_table(impl, tvd, regk, nu);
+    for (int q = 0; q < 40; q++) {
+        const int impl = q & 1, tvd = (q >> 1) & 1, regk = (q >> 2) & 1, graph = (q >> 3) & 1, nu = (q >> 4) & 1;
+        const int l3 = q >= 32;                  // q 32..39: the loop-3 instances (no graph, no NU)
+        if ((nu && regk) || (l3 && (graph || nu))) continue;
+        march_fn f = l3 ? march_table(impl, tvd, regk, 0, 1)
+                        : graph ? march_graph_table(impl, tvd, regk, nu) : march_table(impl, tvd, regk, nu);
         CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(MarchSmem) + (nu ? RW * sizeof(double) : 0))));
     }
@@ -598,11 +612,11 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
 // (fork / join by events; the same calls build the dependencies inside a graph
 // capture).  Returns the number of launches.
 static int launch_march(sts_ctx* c, const MarchParams& m, bool graph, cudaStream_t st, const int* order,
-                        int n_gen, int n_reg)
+                        int n_gen, int n_reg, bool l3 = false)
 {
     const int impl = c->sch.time == STS_IMPLICIT, tvd = c->sch.space == STS_TVD_VANLEER;
-    march_fn gen = graph ? march_graph_table(impl, tvd, 0, c->nu) : march_table(impl, tvd, 0, c->nu);
-    march_fn reg = graph ? march_graph_table(impl, tvd, 1) : march_table(impl, tvd, 1);
+    march_fn gen = l3 ? march_table(impl, tvd, 0, 0, 1) : graph ? march_graph_table(impl, tvd, 0, c->nu) : march_table(impl, tvd, 0, c->nu);
+    march_fn reg = l3 ? march_table(impl, tvd, 1, 0, 1) : graph ? march_graph_table(impl, tvd, 1) : march_table(impl, tvd, 1);
     MarchParams mg = m, mr = m;
     mg.order = (const int4*)order;
     mr.order = (const int4*)order + n_gen;
@@ -962,6 +976,8 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
         return fail(ctx, STS_E_ARG, "bad scheme enum");
     if (!(scheme->dt > 0) || scheme->max_passes < 1 || scheme->min_passes < 0) return fail(ctx, STS_E_CONFIG, "bad dt / passes");
     const int world = dist ? dist->world : 1, rank = dist ? dist->rank : 0;
+    if (scheme->loop3 < 0 || scheme->reserved != 0 || (scheme->loop3 > 1 && world > 1))
+        return fail(ctx, STS_E_CONFIG, "loop3 must be >= 0, and > 1 only on a single-rank context");
     ctx = new sts_ctx();
     {
         sts_status st0 = plan_host(grid, squares, n_squares, gas, world, rank, ctx);
@@ -1009,6 +1025,14 @@ extern "C" sts_status sts_create(const sts_grid* grid, const sts_square* squares
         ALLOC(ctx->snap[k].u, nce); ALLOC(ctx->snap[k].v, nve); ALLOC(ctx->snap[k].p, nce); ALLOC(ctx->snap[k].T, nce);
     }
     ALLOC(ctx->ue, nce); ALLOC(ctx->ve, nve); ALLOC(ctx->Te, nce);
+    if (scheme->loop3 > 1) {                  // loop 3 (N3): sweep iterates and junk targets
+        for (int q = 0; q < 2; q++) { ALLOC(ctx->l3p[q], nce); ALLOC(ctx->l3T[q], nce); }
+        ALLOC(ctx->l3junk, nve);
+        if (cudaMalloc(&ctx->l3red, 10 * sizeof(unsigned long long)) != cudaSuccess) {
+            sts_destroy(ctx);
+            return fail(nullptr, STS_E_OOM, "device allocation failed");
+        }
+    }
     ctx->stage_elems = (size_t)ctx->nloc * ny;          // slab-shaped scratch (rho read-back)
     ALLOC(ctx->stage, ctx->stage_elems);
     if (world > 1 || (dist && dist->nccl_id && gas->xbc == STS_X_PERIODIC)) {
@@ -1081,6 +1105,8 @@ extern "C" void sts_destroy(sts_ctx* ctx)
     cudaFree(ctx->dxl); cudaFree(ctx->dyp);
     for (void* p : ctx->ipc_mapped) cudaIpcCloseMemHandle(p);
     cudaFree(ctx->flags); cudaFree(ctx->red_all); cudaFree(ctx->d_peer_red);
+    for (int q = 0; q < 2; q++) { cudaFree(ctx->l3p[q]); cudaFree(ctx->l3T[q]); }
+    cudaFree(ctx->l3junk); cudaFree(ctx->l3red);
     if (ctx->h_red) cudaFreeHost(ctx->h_red);
     for (cudaGraphExec_t& g : ctx->tol_exec) if (g) cudaGraphExecDestroy(g);
     cudaFree(ctx->red2); cudaFree(ctx->d_ls);
@@ -1316,6 +1342,7 @@ extern "C" sts_status sts_set_mesh(sts_ctx* ctx, const double* dx, int64_t nx, c
 {
     if (!ctx) return fail(ctx, STS_E_ARG, "null ctx");
     if ((dx && nx != ctx->nx) || (dy && ny != ctx->ny)) return fail(ctx, STS_E_ARG, "wrong mesh array size");
+    if (ctx->sch.loop3 > 1) return fail(ctx, STS_E_CONFIG, "loop 3 (loop3 > 1) runs on uniform meshes");
     if (dx) for (int64_t i = 0; i < nx; i++) if (!(dx[i] > 0.0) || !std::isfinite(dx[i])) return fail(ctx, STS_E_CONFIG, "mesh step <= 0");
     if (dy) for (int64_t j = 0; j < ny; j++) if (!(dy[j] > 0.0) || !std::isfinite(dy[j])) return fail(ctx, STS_E_CONFIG, "mesh step <= 0");
     CU(cudaSetDevice(ctx->device));
@@ -1614,7 +1641,7 @@ __global__ void loop_check_kernel(unsigned long long* slot, LoopState* ls, cudaG
 
 static bool tol_graph_ok(const sts_ctx* c)
 {
-    return c->sch.tol > 0 && c->world == 1 && !c->comm && !c->profiling && !getenv("STS_NO_GRAPH");
+    return c->sch.tol > 0 && c->world == 1 && !c->comm && !c->profiling && c->sch.loop3 <= 1 && !getenv("STS_NO_GRAPH");
 }
 
 #define CG(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
@@ -1898,6 +1925,33 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                     } else {
                         prof_end(c);
                     }
+                } else if (c->sch.loop3 > 1) {
+                    // loop 3 (N3, reading R41): sweeps 1 .. L3-1 write T, p into the sweep
+                    // iterates (u, v, residuals, bad key into junk); sweep k >= 2 reads the
+                    // previous sweep's T, p for the coupled terms; the last sweep writes the
+                    // new state, the velocity correction and the residuals as usual
+                    prof_begin(c, 0);
+                    const int L = c->sch.loop3;
+                    const size_t cb = cell_elems(c) * sizeof(double);
+                    for (int q2 = 0; q2 < 2 && q2 < L - 1; q2++) {   // ghost columns / solid cells: the old iterate's
+                        CU(cudaMemcpyAsync(c->l3p[q2], c->snap[old[r]].p, cb, cudaMemcpyDeviceToDevice, st));
+                        CU(cudaMemcpyAsync(c->l3T[q2], c->snap[old[r]].T, cb, cudaMemcpyDeviceToDevice, st));
+                    }
+                    for (int kk = 1; kk <= L; kk++) {
+                        Params q = k;
+                        const bool last = kk == L;
+                        if (!last) {
+                            q.p_w = c->l3p[(kk - 1) & 1]; q.T_w = c->l3T[(kk - 1) & 1];
+                            q.u_w = c->l3junk; q.v_w = c->l3junk; q.red = c->l3red;
+                            CU(cudaMemsetAsync(c->l3red, 0, 10 * sizeof(unsigned long long), st));
+                        }
+                        MarchParams mk = make_march(c, q);
+                        mk.pass_key = pkey;
+                        if (!last) mk.bad = c->l3red + 9;
+                        if (kk >= 2) { mk.p3 = c->l3p[(kk - 2) & 1]; mk.T3 = c->l3T[(kk - 2) & 1]; }
+                        c->launches += launch_march(c, mk, false, st, c->cta_order, c->n_gen, c->n_reg, kk >= 2);
+                    }
+                    prof_end(c);
                 } else {
                     prof_begin(c, 0);
                     MarchParams mk = make_march(c, k);

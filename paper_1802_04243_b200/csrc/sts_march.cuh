@@ -74,6 +74,19 @@ struct MarchParams {
     double* nb_p[2];
     double* nb_T[2];
     int nb_pitch[2], nb_shift[2];
+    // loop 3 (L3 instances, reading R41): the previous T-p sweep's
+    // pressure and temperature (local layout) -- the energy equation's neighbour
+    // T, unsteady density p/T and pressure work, the pressure equation's neighbour p
+    const double* p3;
+    const double* T3;
+};
+// A point's view of the loop-3 iterate: element id = j pitch + local column.
+struct Tp3 {
+    const double* p;
+    const double* T;
+    int id, pitch;
+    __device__ __forceinline__ double P(int o) const { return __ldg(p + id + o); }
+    __device__ __forceinline__ double Tt(int o) const { return __ldg(T + id + o); }
 };
 constexpr int PADY = 4;
 
@@ -608,10 +621,21 @@ __device__ __forceinline__ double shear_general(const RingRow& R0, const RingRow
 // Pressure gradient of the C^T3 Dp/Dt term (R9) at a general point: face
 // pressures = linear interpolation between the two cell centres (the mean on a
 // uniform mesh), = p of the cell at a wall.
-template <bool NU>
+template <bool NU, bool L3 = false>
 __device__ __forceinline__ void dp_general(const RingRow& R0, const RingRow& Ra, const RingRow& Rm, int lc,
-                                           const MarchParams& m, const Geo& g, double& dpx, double& dpy)
+                                           const MarchParams& m, const Geo& g, double& dpx, double& dpy,
+                                           const Tp3& q3 = Tp3{})
 {
+    if (L3) {                                      // loop 3: the pressures of the previous sweep
+        const double pc = q3.P(0);
+        const double pe = wallish(ckind(R0.KK[lc + 1])) ? pc : 0.5 * (pc + q3.P(1));
+        const double pw = wallish(ckind(R0.KK[lc - 1])) ? pc : 0.5 * (q3.P(-1) + pc);
+        const double pn = wallish(ckind(Ra.KK[lc])) ? pc : 0.5 * (pc + q3.P(q3.pitch));
+        const double ps = wallish(ckind(Rm.KK[lc])) ? pc : 0.5 * (q3.P(-q3.pitch) + pc);
+        dpx = (pe - pw) * m.inv_dx;
+        dpy = (pn - ps) * m.inv_dy;
+        return;
+    }
     const double pc = R0.P[lc];
     if (NU) {
         const double dx = g.dxr[lc], dxe = g.dxr[lc + 1], dxw = g.dxr[lc - 1];
@@ -632,12 +656,13 @@ __device__ __forceinline__ void dp_general(const RingRow& R0, const RingRow& Ra,
 }
 
 // ================= stage C: T_{i,j}, u-hat_{i,j}, v-hat_{i,j+1} =================
-template <bool IMPL, bool TVD, bool REG, bool NU = false>
+template <bool IMPL, bool TVD, bool REG, bool NU = false, bool L3 = false>
 __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
                                         const RingRow& R0, const RingRow& Ra, const RingRow& Rb,
                                         const FluxRow& Fc, const FluxRow& Fn, const NM1& nm, const Carry& c,
-                                        StepVars& v, const Geo& g)
+                                        StepVars& v, const Geo& g, const Tp3& q3 = Tp3{})
 {
+    static_assert(!(NU && L3), "loop 3 runs on uniform meshes");
     const Params& k = m.k;
     const double dt = k.dt;
     const double dx = NU ? g.dxr[lc] : k.dx, dy = NU ? g.y0 : k.dy;
@@ -649,29 +674,36 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
     v.TN = 0.0;
     if (cF<REG>(kw0)) {
         double a1, a2, a3, a4, T1, T2, T3, T4, FW, FE, FSl, FNl;
+        // neighbour temperatures: the old iterate, or (loop 3) the previous sweep's
+        auto TW = [&] { return L3 ? q3.Tt(-1) : R0.T[lc - 1]; };
+        auto TE = [&] { return L3 ? q3.Tt(1) : R0.T[lc + 1]; };
+        auto TS = [&] { return L3 ? q3.Tt(-q3.pitch) : Rm.T[lc]; };
+        auto TN = [&] { return L3 ? q3.Tt(q3.pitch) : Ra.T[lc]; };
         if (REG) {
-            a1 = s.XTW[lc]; FW = Fc.FX[lc]; T1 = R0.T[lc - 1];
-            FE = Fc.FX[lc + 1]; a2 = IMPL ? s.XTW[lc + 1] - FE : s.XTW[lc + 1]; T2 = R0.T[lc + 1];
-            a3 = c.ytS; FSl = c.FS; T3 = Rm.T[lc];
-            a4 = v.ytN; FNl = v.Fy1; T4 = Ra.T[lc];
+            a1 = s.XTW[lc]; FW = Fc.FX[lc]; T1 = TW();
+            FE = Fc.FX[lc + 1]; a2 = IMPL ? s.XTW[lc + 1] - FE : s.XTW[lc + 1]; T2 = TE();
+            a3 = c.ytS; FSl = c.FS; T3 = TS();
+            a4 = v.ytN; FNl = v.Fy1; T4 = TN();
         } else {
             FW = FE = FSl = FNl = 0.0;
             const double tau = 2.1904 * k.Kn * rcp(rP);   // Eq. pl39
             uint8_t kn = ckind(R0.KK[lc - 1]);
             if (wallish(kn)) { a1 = k.CT1 * gP * dy * rcp(0.5 * dx + tau); T1 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { a1 = s.XTW[lc]; FW = Fc.FX[lc]; T1 = R0.T[lc - 1]; }
+            else { a1 = s.XTW[lc]; FW = Fc.FX[lc]; T1 = TW(); }
             kn = ckind(R0.KK[lc + 1]);
             if (wallish(kn)) { a2 = k.CT1 * gP * dy * rcp(0.5 * dx + tau); T2 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { FE = Fc.FX[lc + 1]; a2 = IMPL ? s.XTW[lc + 1] - FE : s.XTW[lc + 1]; T2 = R0.T[lc + 1]; }
+            else { FE = Fc.FX[lc + 1]; a2 = IMPL ? s.XTW[lc + 1] - FE : s.XTW[lc + 1]; T2 = TE(); }
             kn = ckind(Rm.KK[lc]);
             if (wallish(kn)) { a3 = k.CT1 * gP * dx * rcp(0.5 * dy + tau); T3 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { a3 = c.ytS; FSl = c.FS; T3 = Rm.T[lc]; }
+            else { a3 = c.ytS; FSl = c.FS; T3 = TS(); }
             kn = ckind(kw1);
             if (wallish(kn)) { a4 = k.CT1 * gP * dx * rcp(0.5 * dy + tau); T4 = kn == CK_WALLY ? k.T_wall : k.T_sq; }
-            else { a4 = v.ytN; FNl = v.Fy1; T4 = Ra.T[lc]; }
+            else { a4 = v.ytN; FNl = v.Fy1; T4 = TN(); }
         }
-        const double a0 = IMPL ? dt * (a1 + a2 + a3 + a4 + FE - FW + FNl - FSl) + rP * dV
-                               : dt * (a1 + a2 + a3 + a4) + rP * dV;
+        // unsteady density: old iterate, or (loop 3) p / T of the previous sweep
+        const double rq = L3 ? fdiv(q3.P(0), q3.Tt(0)) : rP;
+        const double a0 = IMPL ? dt * (a1 + a2 + a3 + a4 + FE - FW + FNl - FSl) + rq * dV
+                               : dt * (a1 + a2 + a3 + a4) + rq * dV;
         // S^T_c, Eq. pl29 (R4 bilinear = 4-point mean on a uniform mesh); a mid-face
         // velocity on a wall face is the slip velocity of Eq. pl38 (R38)
         const double rdx = NU ? rcp(dx) : m.inv_dx, rdy = NU ? rcp(dy) : m.inv_dy;
@@ -693,14 +725,14 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         // kappa p div(u); branch-free: pw_a = C^T3 or 0, pwk = 0 or kappa.
         // p^{n-1} = rho^{n-1} T^{n-1} (the (p/T)^{n-1} row times T^{n-1}, within
         // 2 ulp of the stored p^{n-1})
-        const double pc = R0.P[lc];
+        const double pc = L3 ? q3.P(0) : R0.P[lc];
         const double p1 = s.R1[lc] * nm.T1c;
         double dpx, dpy;
         if (REG) {
-            dpx = (R0.P[lc + 1] - R0.P[lc - 1]) * m.h_dx;
-            dpy = (Ra.P[lc] - Rm.P[lc]) * m.h_dy;
+            dpx = L3 ? (q3.P(1) - q3.P(-1)) * m.h_dx : (R0.P[lc + 1] - R0.P[lc - 1]) * m.h_dx;
+            dpy = L3 ? (q3.P(q3.pitch) - q3.P(-q3.pitch)) * m.h_dy : (Ra.P[lc] - Rm.P[lc]) * m.h_dy;
         } else {
-            dp_general<NU>(R0, Ra, Rm, lc, m, g, dpx, dpy);
+            dp_general<NU, L3>(R0, Ra, Rm, lc, m, g, dpx, dpy, q3);
         }
         const double ub = 0.5 * (R0.U[lc] + R0.U[lc + 1]), vb = 0.5 * (R0.V[lc] + Ra.V[lc]);
         const double pwork = m.pw_a * ((pc - p1) * m.inv_dt + ub * dpx + vb * dpy) + k.pwk * pc * div;
@@ -822,10 +854,11 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
 }
 
 // ================= stage D: p_{i,j} (Eqs. pl23-pl24) =================
-template <bool IMPL, bool TVD, bool REG, bool NU = false>
+template <bool IMPL, bool TVD, bool REG, bool NU = false, bool L3 = false>
 __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
                                         const RingRow& R0, const RingRow& Ra, const FluxRow& Fc,
-                                        const FluxRow& Fn, const Carry& c, StepVars& v, const Geo& g)
+                                        const FluxRow& Fn, const Carry& c, StepVars& v, const Geo& g,
+                                        const Tp3& q3 = Tp3{})
 {
     const Params& k = m.k;
     const double dt = k.dt, dx = NU ? g.dxr[lc] : k.dx, dy = NU ? g.y0 : k.dy;
@@ -834,30 +867,35 @@ __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int 
     double pn = R0.P[lc];
     if (cF<REG>(kw0)) {
         double apW = 0.0, apE = 0.0, apS = 0.0, apN = 0.0, bpW = 0.0, bpE = 0.0, bpS = 0.0, bpN = 0.0, sum = 0.0;
+        // neighbour pressures: the old iterate, or (loop 3) the previous sweep's
+        auto PW = [&] { return L3 ? q3.P(-1) : R0.P[lc - 1]; };
+        auto PE = [&] { return L3 ? q3.P(1) : R0.P[lc + 1]; };
+        auto PS = [&] { return L3 ? q3.P(-q3.pitch) : Rm.P[lc]; };
+        auto PN = [&] { return L3 ? q3.P(q3.pitch) : Ra.P[lc]; };
         if (REG) {
             const double rw = Fc.RU[lc], re = Fc.RU[lc + 1], rs = c.rvS, rn = v.rv1;
             apW = rw * v.du * dy; bpW = rw * v.uhat * dy;
             apE = re * s.DU[lc + 1] * dy; bpE = re * s.UH[lc + 1] * dy;
             apS = rs * c.dvP * dx; bpS = rs * c.vhatP * dx;
             apN = rn * v.dvN * dx; bpN = rn * v.vhatN * dx;
-            sum = apW * R0.P[lc - 1] + apE * R0.P[lc + 1] + apS * Rm.P[lc] + apN * Ra.P[lc];
+            sum = apW * PW() + apE * PE() + apS * PS() + apN * PN();
         } else {
             const uint8_t kwf = ukind(kw0), kef = ukind(R0.KK[lc + 1]);
             if (kwf == FK_ACTIVE) {
                 const double r = Fc.RU[lc];
-                apW = r * v.du * dy; bpW = r * v.uhat * dy; sum += apW * R0.P[lc - 1];
+                apW = r * v.du * dy; bpW = r * v.uhat * dy; sum += apW * PW();
             } else if (kwf == FK_INLET) bpW = Fc.RU[lc] * k.u_in * dy;
             if (kef == FK_ACTIVE) {
                 const double r = Fc.RU[lc + 1];
-                apE = r * s.DU[lc + 1] * dy; bpE = r * s.UH[lc + 1] * dy; sum += apE * R0.P[lc + 1];
+                apE = r * s.DU[lc + 1] * dy; bpE = r * s.UH[lc + 1] * dy; sum += apE * PE();
             } else if (kef == FK_OUTLET) bpE = Fc.RU[lc + 1] * R0.U[lc] * dy;
             if (vkind(kw0) == FK_ACTIVE) {
                 const double r = c.rvS;
-                apS = r * c.dvP * dx; bpS = r * c.vhatP * dx; sum += apS * Rm.P[lc];
+                apS = r * c.dvP * dx; bpS = r * c.vhatP * dx; sum += apS * PS();
             }
             if (vkind(Ra.KK[lc]) == FK_ACTIVE) {
                 const double r = v.rv1;
-                apN = r * v.dvN * dx; bpN = r * v.vhatN * dx; sum += apN * Ra.P[lc];
+                apN = r * v.dvN * dx; bpN = r * v.vhatN * dx; sum += apN * PN();
             }
         }
         // a^p_0 = dV / T_new + dt sum a^p (Eq. pl24, R28); multiplied through by T_new
@@ -946,10 +984,11 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
 // NU = true: the non-uniform-mesh kernel: every point runs the
 // general instances in their general-mesh form; the column widths of the ring
 // columns sit behind MarchSmem in shared memory, the row heights come from m.dyp.
-template <bool IMPL, bool TVD, bool GRAPH = false, bool REGK = false, bool NU = false>
+template <bool IMPL, bool TVD, bool GRAPH = false, bool REGK = false, bool NU = false, bool L3 = false>
 __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
 {
     static_assert(!(NU && REGK), "non-uniform meshes run the general kernel only");
+    static_assert(!(NU && L3), "loop 3 runs on uniform meshes");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MarchSmem& s = *reinterpret_cast<MarchSmem*>(smem_raw);
     double* const s_dx = reinterpret_cast<double*>(smem_raw + sizeof(MarchSmem));   // NU only: RW widths

@@ -57,7 +57,8 @@ class sts_gas(ctypes.Structure):
 
 class sts_scheme(ctypes.Structure):
     _fields_ = [("time", ctypes.c_int32), ("space", ctypes.c_int32), ("dt", ctypes.c_double),
-                ("min_passes", ctypes.c_int32), ("max_passes", ctypes.c_int32), ("tol", ctypes.c_double)]
+                ("min_passes", ctypes.c_int32), ("max_passes", ctypes.c_int32), ("tol", ctypes.c_double),
+                ("loop3", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class sts_dist(ctypes.Structure):
@@ -210,7 +211,8 @@ class Solver:
         self.case = dict(case)
         grid, arr, nsq, gas = _structs(case)
         sch = sts_scheme(int(case["time"]), int(case["space"]), float(case["dt"]),
-                         int(case.get("min_passes", 1)), int(case["max_passes"]), float(case.get("tol", 0.0)))
+                         int(case.get("min_passes", 1)), int(case["max_passes"]), float(case.get("tol", 0.0)),
+                         int(case.get("loop3", 1)), 0)
         self._idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         dist = sts_dist(rank, world, device, ctypes.cast(self._idbuf, ctypes.c_void_p) if self._idbuf else None)
         h = ctypes.c_void_p()
