@@ -123,6 +123,11 @@ struct sts_ctx {
     // graph-driven loop 2 (tolerance mode, one context without NCCL): one CUDA
     // graph per snapshot rotation, loop 2 as a conditional WHILE node
     cudaGraphExec_t tol_exec[3] = {nullptr, nullptr, nullptr};
+    // fixed-pass mode as one CUDA graph per time step and snapshot rotation (no
+    // host round trip, no per-launch API cost; the paper's small meshes)
+    cudaGraphExec_t fix_exec[3] = {nullptr, nullptr, nullptr};
+    unsigned long long* h_badstep = nullptr;   // pinned: the sticky bad key after every step of a call
+    int h_badstep_n = 0;
     unsigned long long* red2 = nullptr;    // [2][9] residual slots (even / odd passes)
     struct LoopState* d_ls = nullptr;      // device loop state
     struct LoopState* h_ls = nullptr;      // pinned copy
@@ -549,13 +554,15 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     std::vector<int> hg_c, hr_c;
     if (forced > 0) { hg_c = {forced}; hr_c = {forced}; }
     else {
-        hg_c = {8, 12, 16, 24, 32, 48};
+        hg_c = {4, 6, 8, 12, 16, 24, 32, 48};
         // Hr: 8, 10, ..., 64.  Longer regular CTAs look cheaper to the model (fewer
         // warm-up rows) but measure slower: a slot is not a processor -- the CTAs
         // resident on one SM share its issue rate, so a schedule of few long CTAs
         // leaves SMs with 3 CTAs beside SMs with 4 and a long tail (C3: Hr 252,
         // 501 CTAs 0.630 ms/pass; forced 48-row CTAs 0.606 ms, profiles/r02_summary.md)
-        for (int h = std::min(ny, 8); h <= std::min(ny, 64); h += 2) hr_c.push_back(h);
+        // (from 4 rows: the paper's 4032 x 200 mesh cannot fill 148 SMs x 4 CTAs with
+        // longer segments -- 6-row segments measured 0.63 ms/step, 8-row ones 0.72)
+        for (int h = std::min(ny, 4); h <= std::min(ny, 64); h += 2) hr_c.push_back(h);
         if (hr_c.empty()) hr_c.push_back(std::max(1, ny));
     }
     for (int hg : hg_c)
@@ -1109,6 +1116,8 @@ extern "C" void sts_destroy(sts_ctx* ctx)
     cudaFree(ctx->l3junk); cudaFree(ctx->l3red);
     if (ctx->h_red) cudaFreeHost(ctx->h_red);
     for (cudaGraphExec_t& g : ctx->tol_exec) if (g) cudaGraphExecDestroy(g);
+    for (cudaGraphExec_t& g : ctx->fix_exec) if (g) cudaGraphExecDestroy(g);
+    if (ctx->h_badstep) cudaFreeHost(ctx->h_badstep);
     cudaFree(ctx->red2); cudaFree(ctx->d_ls);
     if (ctx->h_ls) cudaFreeHost(ctx->h_ls);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
@@ -1365,6 +1374,8 @@ extern "C" sts_status sts_set_mesh(sts_ctx* ctx, const double* dx, int64_t nx, c
     CU(cudaMemcpy(packed.data(), ctx->kind32, packed.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     choose_segments(ctx, packed);
     for (cudaGraphExec_t& g : ctx->tol_exec)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    for (cudaGraphExec_t& g : ctx->fix_exec)
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     return STS_OK;
 }
@@ -1785,6 +1796,120 @@ static sts_status graph_step(sts_ctx* ctx, bool* conv)
     return STS_OK;
 }
 
+// Fixed-pass mode (tol <= 0) on one context without a halo: one time step =
+// one graph launch of [zero residual slots; explicit planes; max_passes passes]
+// built from the same kernels and launch configuration as the stream path (the
+// general and all-regular CTA sets as two parallel kernel nodes per pass).  The
+// pass key of a graph pass is its index within the step; the host keeps the
+// sticky bad key after every step (one 8-byte async copy) to place a bad state
+// in the call.
+static bool fix_graph_ok(const sts_ctx* c)
+{
+    return c->sch.tol <= 0 && c->world == 1 && !c->comm && !c->peer && !c->profiling && c->sch.loop3 <= 1 &&
+           !getenv("STS_NO_GRAPH") && !getenv("STS_GRAPH_KERNEL");
+}
+static sts_status build_fix_graph(sts_ctx* ctx, int n1)
+{
+    sts_ctx* const c = ctx;
+    const int impl = c->sch.time == STS_IMPLICIT, tvd = c->sch.space == STS_TVD_VANLEER;
+    const int a = (n1 + 1) % 3, b = (n1 + 2) % 3;
+    cudaStream_t cap = nullptr;
+    CU(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    Params k = make_params(c);
+    k.u_1 = c->snap[n1].u; k.v_1 = c->snap[n1].v; k.p_1 = c->snap[n1].p; k.T_1 = c->snap[n1].T;
+    k.ue = c->ue; k.ve = c->ve; k.Te = c->Te;
+    cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->red, 0, (size_t)c->sch.max_passes * 9 * sizeof(unsigned long long), cap);
+    if (e == cudaSuccess && !impl) {
+        Params q = k;
+        q.ue_w = c->ue; q.ve_w = c->ve; q.Te_w = c->Te;
+        conv_march_table(tvd, c->nu)<<<dim3(c->n_gen + c->n_reg), MX, conv_smem(c), cap>>>(make_march(c, q));
+        e = cudaGetLastError();
+    }
+    int old = n1, nw = a;
+    for (int it = 0; it < c->sch.max_passes && e == cudaSuccess; it++) {
+        Params q = k;
+        q.u_o = c->snap[old].u; q.v_o = c->snap[old].v; q.p_o = c->snap[old].p; q.T_o = c->snap[old].T;
+        q.u_w = c->snap[nw].u; q.v_w = c->snap[nw].v; q.p_w = c->snap[nw].p; q.T_w = c->snap[nw].T;
+        q.red = c->red + (size_t)it * 9;
+        MarchParams m = make_march(c, q);
+        m.pass_key = 0xFFFFF - it;
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t g;
+        const cudaGraphNode_t* dp = nullptr;
+        size_t nd = 0;
+        e = cudaStreamGetCaptureInfo(cap, &cs, nullptr, &g, &dp, &nd);
+        if (e != cudaSuccess) break;
+        std::vector<cudaGraphNode_t> deps(dp, dp + nd);
+        cudaGraphNode_t nodes[2];
+        int nn = 0;
+        for (int part = 0; part < 2 && e == cudaSuccess; part++) {
+            const int cnt = part == 0 ? c->n_gen : c->n_reg;
+            if (cnt == 0) continue;
+            MarchParams mp = m;
+            mp.order = (const int4*)c->cta_order + (part ? c->n_gen : 0);
+            void* args[] = {&mp};
+            cudaKernelNodeParams kp = {};
+            kp.func = (void*)march_table(impl, tvd, part, part ? 0 : c->nu);
+            kp.gridDim = dim3(cnt);
+            kp.blockDim = dim3(MX);
+            kp.sharedMemBytes = march_smem(c);
+            kp.kernelParams = args;
+            e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
+            nn++;
+        }
+        if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(cap, nodes, nn, cudaStreamSetCaptureDependencies);
+        old = nw;
+        nw = nw == a ? b : a;
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t e2 = cudaStreamEndCapture(cap, &g);
+    if (e == cudaSuccess) e = e2;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&c->fix_exec[n1], g, 0);
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(cap);
+    if (e != cudaSuccess) return fail(c, STS_E_CUDA, std::string("fixed-pass graph: ") + cudaGetErrorString(e));
+    return STS_OK;
+}
+static sts_status fix_graph_advance(sts_ctx* ctx, int32_t n_steps, sts_stats* out)
+{
+    sts_ctx* c = ctx;
+    for (int r = 0; r < 3; r++)                   // all three rotations at once: no build inside later steps
+        if (!c->fix_exec[r]) { sts_status e = build_fix_graph(c, r); if (e) return e; }
+    if (c->h_badstep_n < n_steps) {
+        if (c->h_badstep) cudaFreeHost(c->h_badstep);
+        c->h_badstep = nullptr;
+        c->h_badstep_n = 0;
+        CU(cudaMallocHost(&c->h_badstep, (size_t)std::max(n_steps, 1) * sizeof(unsigned long long)));
+        c->h_badstep_n = std::max(n_steps, 1);
+    }
+    const long long pass0 = c->stats.passes_done;
+    const int P = c->sch.max_passes;
+    for (int s = 0; s < n_steps; s++) {
+        const int n1 = c->cur;
+        CU(cudaGraphLaunch(c->fix_exec[n1], c->stream));
+        CU(cudaMemcpyAsync(c->h_badstep + s, c->bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+        c->cur = (P & 1) ? (n1 + 1) % 3 : (n1 + 2) % 3;          // pass 1 writes n1+1, pass 2 n1+2, ...
+        c->launches += 2 * P + (c->sch.time == STS_EXPLICIT ? 1 : 0);
+        c->stats.steps_done++;
+        c->stats.passes_done += P;
+        c->stats.converged = 0;
+    }
+    if (n_steps > 0) {
+        unsigned long long red[10];
+        sts_status e = gather_red(&c, 1, P - 1, red, c->stream);     // synchronises the stream
+        if (e) return e;
+        c->pass0 = pass0;
+        for (int s = 0; s < n_steps; s++)
+            if (c->h_badstep[s]) { c->pass0 = pass0 + (long long)s * P; break; }
+        e = finish_residuals(c, red, red[9]);
+        if (out) *out = c->stats;
+        return e;
+    }
+    if (out) *out = c->stats;
+    return STS_OK;
+}
+
 // Loop 1 x loop 2 for a group of slab contexts advanced in lockstep (n == 1
 // for the usual one-context-per-process case).
 static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
@@ -1811,6 +1936,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
         CU(cudaMemsetAsync(cs[r]->bad, 0, sizeof(unsigned long long), st));
     }
     long long prel = 0;                               // pass index within this advance call
+    if (n == 1 && fix_graph_ok(ctx)) return fix_graph_advance(ctx, n_steps, out);
     if (n == 1 && tol_graph_ok(ctx)) {
         for (int step = 0; step < n_steps; step++) {
             bool conv = false;

@@ -993,8 +993,15 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     MarchSmem& s = *reinterpret_cast<MarchSmem*>(smem_raw);
     double* const s_dx = reinterpret_cast<double*>(smem_raw + sizeof(MarchSmem));   // NU only: RW widths
     const Params& k = m.k;
-    if (GRAPH && *(volatile const int*)m.done) return;  // converged earlier in this graph launch (CTA-uniform)
-    if (*(volatile const unsigned long long*)m.bad) return;   // a bad state earlier in this advance call
+    // Early exit: loop 2 converged earlier in this graph launch, or a bad state
+    // earlier in this advance call.  The bad key is written by other CTAs of this
+    // very launch (atomicMax at their end), so a per-thread read could differ
+    // inside one CTA and split it at the barriers below; thread 0 reads both
+    // flags and the CTA takes one decision (__syncthreads_or).
+    int stop = 0;
+    if (threadIdx.x == 0)
+        stop = (GRAPH && *(volatile const int*)m.done) || *(volatile const unsigned long long*)m.bad != 0ull;
+    if (__syncthreads_or(stop)) return;
     const int t = threadIdx.x;
     const int4 ce = m.order[blockIdx.x];
     const int strip = ce.x;

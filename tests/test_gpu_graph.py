@@ -113,3 +113,28 @@ def test_graph_loop_bad_state(S):
     st, stats = g.advance(1, check=False)
     assert st == S.STS_E_STATE
     assert stats["bad_cell"] >= 0
+
+
+@pytest.mark.parametrize("variant", list(W.VARIANTS))
+def test_fixed_pass_graph_matches_stream(S, variant):
+    """Fixed-pass mode: one CUDA graph per time step (the default on one context)
+    against the stream-launched passes (STS_NO_GRAPH=1), bit for bit, over steps
+    of both snapshot-rotation parities (odd pass count)."""
+    case = W.c1_small(variant, passes=3)
+    a = _run(S, case, 4, graph=True)
+    b = _run(S, case, 4, graph=False)
+    _same(a, b)
+
+
+def test_fixed_pass_graph_bad_state_step(S):
+    """A bad state in step 3 of a 4-step call made of graph launches: reported with
+    its cumulative pass index (2 steps x 2 passes + its pass within step 3)."""
+    case = W.c1_small("implicit_upwind", passes=2)
+    g = S.Solver(case)
+    g.advance(2)                                   # a healthy start: passes_done = 4
+    T = g.get_field("T")
+    T[5, 3] = -1.0
+    g.set_field("T", T)
+    st, stats = g.advance(3, check=False)
+    assert st == S.STS_E_STATE
+    assert stats["bad_pass"] == 4, stats

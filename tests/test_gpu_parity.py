@@ -294,11 +294,17 @@ def test_parity_implicit_tvd_paper_mesh_conditioning(S, oracle_mod):
 
 def test_parity_c2_full(S, oracle_mod):
     """BASELINE configs[1] against the oracle: C2 (4096 x 256, 1 M FVs, periodic
-    slip Poiseuille, implicit upwind), 20 steps x 10 passes (~6 min of oracle time)
-    from the closed-form profile scaled by 1.05 with smooth p and T modes.  (Cell-wise
-    random noise is not a usable start here: 10 fixed passes per step do not
-    converge on it at dt = 0.002 and the oracle itself diverges within 5 steps.)"""
+    slip Poiseuille, implicit upwind), 20 steps x 10 passes from the closed-form
+    profile scaled by 1.05 with smooth p and T modes.  (Cell-wise random noise is
+    not a usable start here: 10 fixed passes per step do not converge on it at
+    dt = 0.002 and the oracle itself diverges within 5 steps.)  Even from the
+    smooth start the fixed-pass scheme amplifies a perturbation ~3.7x per step
+    here (two oracle runs 1 ulp of T apart: 3e-15 after 3 steps, 3e-11 after 10),
+    so, as for implicit TVD (R40), the 1e-9 bar holds through 8 steps and at 20
+    steps the GPU must stay within the oracle's own one-ulp sensitivity (x10).
+    The two oracle runs go in parallel threads (ctypes releases the GIL)."""
     import math
+    from concurrent.futures import ThreadPoolExecutor
     case = W.c2(small=False, variant="implicit_upwind", passes=10)
     H, N, Kn, gx, nx = 1.0, case["ny"], case["Kn"], case["g_x"], case["nx"]
     B = 5.0 * math.sqrt(math.pi) / 16.0 * Kn
@@ -307,13 +313,23 @@ def test_parity_c2_full(S, oracle_mod):
     prof = (gx / (2 * B)) * (y * (H - y) + 1.1466 * Kn * H)
     g = S.Solver(case)
     o = oracle_mod.Case(case)
+    o2 = oracle_mod.Case(case)
     st = {"u": np.repeat(1.05 * prof[:, None], nx + 1, axis=1), "v": np.zeros((N + 1, nx)),
           "p": 1 + 1e-3 * np.sin(2 * np.pi * x)[None, :] * np.ones((N, 1)),
           "T": 1 + 5e-4 * np.outer(np.sin(np.pi * y), np.cos(2 * np.pi * x))}
     for k in ("p", "T", "u", "v"):
         g.set_field(k, st[k])
         o.set(k, st[k])
-    g.advance(20)
-    assert o.advance(20)[0] == 0
-    err = rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), o.get_map(0) == 0)
-    assert max(err.values()) <= TOL, err
+        o2.set(k, np.nextafter(st[k], 2.0) if k == "T" else st[k])
+    fluid = o.get_map(0) == 0
+    with ThreadPoolExecutor(2) as ex:
+        for steps in (8, 12):
+            g.advance(steps)
+            r1, r2 = ex.submit(o.advance, steps), ex.submit(o2.advance, steps)
+            assert r1.result()[0] == 0 and r2.result()[0] == 0
+            err = rel_errors({k: g.get_field(k) for k in FIELDS}, o.fields(), fluid)
+            if steps == 8:
+                assert max(err.values()) <= TOL, err
+            else:
+                e_ulp = max(rel_errors(o2.fields(), o.fields(), fluid).values())
+                assert max(err.values()) <= max(TOL, 10 * e_ulp), (err, e_ulp)
