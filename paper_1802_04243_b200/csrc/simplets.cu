@@ -1615,6 +1615,19 @@ static sts_status gather_red(sts_ctx** cs, int n, int it, unsigned long long* ou
 // second pass of a body iteration is a no-op when the first one converged.  The
 // check applies exactly the host's test (finish_residuals + the tol comparison,
 // same fp64 operations), so both drivers take identical pass counts.
+// The general CTAs of a pass (walls, squares, inlet / outlet strips: the long
+// critical path of the schedule) run on a high-priority stream on the stream
+// path; inside a graph the same priority is a kernel-node attribute.
+static cudaError_t graph_node_high_priority(cudaGraphNode_t node)
+{
+    int lo = 0, hi = 0;
+    cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (e != cudaSuccess) return e;
+    cudaKernelNodeAttrValue v = {};
+    v.priority = hi;
+    return cudaGraphKernelNodeSetAttribute(node, cudaKernelNodeAttributePriority, &v);
+}
+
 struct LoopState {
     int passes, done, conv, checked;
     unsigned long long red[9];   // residual slots of the last checked pass
@@ -1710,6 +1723,8 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
             kp.sharedMemBytes = march_smem(c);
             kp.kernelParams = args;
             e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
+            if (e != cudaSuccess) return e;
+            if (part == 0) e = graph_node_high_priority(nodes[nn]);   // general CTAs first, as on the stream path
             if (e != cudaSuccess) return e;
             nn++;
         }
@@ -1856,6 +1871,7 @@ static sts_status build_fix_graph(sts_ctx* ctx, int n1)
             kp.sharedMemBytes = march_smem(c);
             kp.kernelParams = args;
             e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
+            if (e == cudaSuccess && part == 0) e = graph_node_high_priority(nodes[nn]);
             nn++;
         }
         if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(cap, nodes, nn, cudaStreamSetCaptureDependencies);
