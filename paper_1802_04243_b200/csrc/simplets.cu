@@ -348,6 +348,16 @@ __global__ void red_push_kernel(const unsigned long long* slot, const unsigned l
 // ------------------------------------------------------------- kernel table
 typedef void (*march_fn)(MarchParams);
 // regk: the all-regular kernel (sts_march.cuh); nu: the non-uniform-mesh kernel
+// the edge strips of a peer-connected rank: general kernel with the fused halo stores (N1)
+static march_fn march_halo_table(int impl, int tvd, int nu)
+{
+    if (nu) {
+        if (impl) return tvd ? march_kernel<true, true, false, false, true, false, true> : march_kernel<true, false, false, false, true, false, true>;
+        return tvd ? march_kernel<false, true, false, false, true, false, true> : march_kernel<false, false, false, false, true, false, true>;
+    }
+    if (impl) return tvd ? march_kernel<true, true, false, false, false, false, true> : march_kernel<true, false, false, false, false, false, true>;
+    return tvd ? march_kernel<false, true, false, false, false, false, true> : march_kernel<false, false, false, false, false, false, true>;
+}
 static march_fn march_table(int impl, int tvd, int regk, int nu = 0, int l3 = 0)
 {
     if (l3) {                                    // loop-3 sweeps k >= 2 (N3)
@@ -407,6 +417,11 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
         march_fn f = l3 ? march_table(impl, tvd, regk, 0, 1)
                         : graph ? march_graph_table(impl, tvd, regk, nu) : march_table(impl, tvd, regk, nu);
         CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(MarchSmem) + (nu ? RW * sizeof(double) : 0))));
+    }
+    for (int q = 0; q < 8; q++) {
+        const int impl = q & 1, tvd = (q >> 1) & 1, nu = q >> 2;
+        CU(cudaFuncSetAttribute((const void*)march_halo_table(impl, tvd, nu), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(MarchSmem) + (nu ? RW * sizeof(double) : 0))));
     }
     for (int q = 0; q < 4; q++)
@@ -638,7 +653,7 @@ static int launch_march(sts_ctx* c, const MarchParams& m, bool graph, cudaStream
     }
     if (n_gen > 0) gen<<<n_gen, MX, march_smem(c), st>>>(mg);
     else if (n_reg > 0) reg<<<n_reg, MX, march_smem(c), st>>>(mr);
-    return 1;
+    return (n_gen > 0 || n_reg > 0) ? 1 : 0;
 }
 
 // ------------------------------------------------------------- profiling
@@ -2011,8 +2026,11 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
         // pass stream and need only pass p-1 (edge + interior), never the halo, so
         // the exchange of pass p overlaps the interior of pass p+1.  In-process
         // slab groups launch the same two CTA sets one after the other.
+        // a peer-connected rank always splits (its edge strips carry the fused halo
+        // stores, which the all-regular kernel does not compile in), even when
+        // every strip is an edge strip (an empty interior set)
         const bool split = (ctx->world > 1 || ctx->comm) && ctx->n_edge > 0 &&
-                           ctx->n_edge < ctx->n_split && !getenv("STS_NO_SPLIT");
+                           (ctx->peer || (ctx->n_edge < ctx->n_split && !getenv("STS_NO_SPLIT")));
         const bool overlap = split && n == 1 && (ctx->comm || ctx->peer);
         if (overlap) {
             if (!ctx->hstream) {
@@ -2048,7 +2066,8 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                         if (e) return e;
                         peer_params(c, nw[r], ma);
                     }
-                    march_fn gen = gk ? march_graph_table(impl, tvd, 0, c->nu) : march_table(impl, tvd, 0, c->nu);
+                    march_fn gen = c->peer ? march_halo_table(impl, tvd, c->nu)
+                                 : gk ? march_graph_table(impl, tvd, 0, c->nu) : march_table(impl, tvd, 0, c->nu);
                     gen<<<c->n_edge, MX, march_smem(c), as>>>(ma);
                     if (c->peer) { sts_status e = peer_signal(c, q, as); if (e) return e; }
                     if (overlap) CU(cudaEventRecord(c->ev_a[it & 1], as));
@@ -2099,15 +2118,8 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                     MarchParams mk = make_march(c, k);
                     mk.pass_key = pkey;
                     if (gk) mk.done = &c->d_ls->done;
-                    unsigned long long q = 0;
-                    if (c->peer) {              // no edge / interior split (narrow slab): the whole pass
-                        q = ++c->seq;
-                        sts_status e = peer_wait(c, q - 1, st);
-                        if (e) return e;
-                        peer_params(c, nw[r], mk);
-                    }
+                    if (c->peer) return fail(c, STS_E_ARG, "peer-connected rank without edge strips");
                     c->launches += launch_march(c, mk, gk, st, c->cta_order, c->n_gen, c->n_reg);
-                    if (c->peer) { sts_status e = peer_signal(c, q, st); if (e) return e; }
                     prof_end(c);
                 }
                 CU(cudaGetLastError());

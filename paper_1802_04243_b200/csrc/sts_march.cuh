@@ -335,14 +335,6 @@ struct StepVars {
     double rv1;                   // rho^v at v-face (i, j+1)
     double TN, uhat, du, utSn, FsSumN, vhatN, dvN, pn;
 };
-// The carry into row step j read straight from row step j-1's StepVars
-// (references: no copies once inlined).
-struct CarryView {
-    const double &ytS, &FS, &utS, &FsSum, &vcS, &FbS, &vhatP, &dvP, &pnP, &gcP, &rvS;
-    __device__ __forceinline__ explicit CarryView(const StepVars& p)
-        : ytS(p.ytSn), FS(p.Fy1), utS(p.utSn), FsSum(p.FsSumN), vcS(p.vcSn), FbS(p.FbN), vhatP(p.vhatN),
-          dvP(p.dvN), pnP(p.pn), gcP(p.gcN), rvS(p.rv1) {}
-};
 struct NM1 {                      // n-1 state / explicit planes at this thread's points
     double p1n, T1n;              // row j+1
     double T1c, u1c, v1n;         // T^{n-1}(i, j), u^{n-1}(i, j), v^{n-1}(i, j+1)
@@ -667,7 +659,7 @@ __device__ __forceinline__ void dp_general(const RingRow& R0, const RingRow& Ra,
 template <bool IMPL, bool TVD, bool REG, bool NU = false, bool L3 = false>
 __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
                                         const RingRow& R0, const RingRow& Ra, const RingRow& Rb,
-                                        const FluxRow& Fc, const FluxRow& Fn, const NM1& nm, const CarryView& c,
+                                        const FluxRow& Fc, const FluxRow& Fn, const NM1& nm, const Carry& c,
                                         StepVars& v, const Geo& g, const Tp3& q3 = Tp3{})
 {
     static_assert(!(NU && L3), "loop 3 runs on uniform meshes");
@@ -865,7 +857,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
 template <bool IMPL, bool TVD, bool REG, bool NU = false, bool L3 = false>
 __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int lc, const RingRow& Rm,
                                         const RingRow& R0, const RingRow& Ra, const FluxRow& Fc,
-                                        const FluxRow& Fn, const CarryView& c, StepVars& v, const Geo& g,
+                                        const FluxRow& Fn, const Carry& c, StepVars& v, const Geo& g,
                                         const Tp3& q3 = Tp3{})
 {
     const Params& k = m.k;
@@ -929,7 +921,7 @@ __host__ __device__ __forceinline__ unsigned long long bad_key(int pass_key, lon
 // ================= stage E: corrections, writes, residuals =================
 template <bool IMPL, bool TVD, bool REG, bool HALO = false>
 __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int lc, int gi, int j,
-                                        const RingRow& R0, const CarryView& c, const StepVars& v, Resid& rs)
+                                        const RingRow& R0, const Carry& c, const StepVars& v, Resid& rs)
 {
     const Params& k = m.k;
     const int id = j * k.pitch + (gi - k.gi0 + OFF);
@@ -992,9 +984,13 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
 // NU = true: the non-uniform-mesh kernel: every point runs the
 // general instances in their general-mesh form; the column widths of the ring
 // columns sit behind MarchSmem in shared memory, the row heights come from m.dyp.
-template <bool IMPL, bool TVD, bool GRAPH = false, bool REGK = false, bool NU = false, bool L3 = false>
+// HALO = true: the edge-strip kernel of a peer-connected rank (fused halo
+// stores in stage E, N1); every other launch compiles them out.
+template <bool IMPL, bool TVD, bool GRAPH = false, bool REGK = false, bool NU = false, bool L3 = false,
+          bool HALO = false>
 __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
 {
+    static_assert(!(HALO && (REGK || GRAPH || L3)), "fused halo stores: edge strips of the stream path only");
     static_assert(!(NU && REGK), "non-uniform meshes run the general kernel only");
     static_assert(!(NU && L3), "loop 3 runs on uniform meshes");
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1068,7 +1064,9 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
         if (!IMPL) { nm.Tec = ld(k.Te, js); nm.uec = ld(k.ue, js); nm.ven = ldv(k.ve, js + 1); }
     };
 
+    Carry c{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 1.0, 0.0};
     Resid rs{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, -1, 0, false};
+    StepVars v;
     int oj = js * k.pitch + col;                        // element offset of (row j, own column), + pitch per step (upwind prefetch)
 
     // The row loop: the all-regular kernel prefetches the n-1 values of its
