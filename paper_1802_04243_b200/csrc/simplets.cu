@@ -469,6 +469,7 @@ static MarchParams make_march(const sts_ctx* c, const Params& k)
     m.pass_key = 0xFFFFF;
     m.dxl = c->dxl;
     m.dyp = c->dyp;
+    m.force_general = getenv("STS_FORCE_GENERAL") ? 1 : 0;
     return m;
 }
 
@@ -497,7 +498,9 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     const int strips = (c->nloc + MW - 1) / MW;
     const int slots = dev_sms * per_sm;
     const int ny = c->ny;
-    double w_gen = 1.35, w_mix = 2.35;                  // warp costs relative to an all-regular warp
+    // warp costs relative to an all-regular warp: a warp with any general point runs
+    // the general instance (warp-uniform dispatch, sts_march_loop.inc)
+    double w_gen = 1.35, w_mix = 1.35;
     if (const char* cv = getenv("STS_COST")) sscanf(cv, "%lf,%lf", &w_gen, &w_mix);   // tuning hook
     // every CTA general: test hook, or a non-uniform mesh (the NU kernel has general instances only)
     const bool no_allreg = getenv("STS_NO_ALLREG") != nullptr || c->nu;

@@ -79,6 +79,7 @@ struct MarchParams {
     // T, unsteady density p/T and pressure work, the pressure equation's neighbour p
     const double* p3;
     const double* T3;
+    int force_general;           // test hook (STS_FORCE_GENERAL): every point of the general kernel general
 };
 // A point's view of the loop-3 iterate: element id = j pitch + local column.
 struct Tp3 {
@@ -609,6 +610,11 @@ __device__ __forceinline__ double shear_general(const RingRow& R0, const RingRow
         if (wallish(kN)) uN = slip(0.5 * us, kN == CK_WALLY ? k.u_wt : 0.0, 0.5 * dy);
         if (wallish(kS)) uS = slip(0.5 * us, kS == CK_WALLY ? k.u_wb : 0.0, 0.5 * dy);
     } else {
+        // no wall around the point: exactly the regular instance's operations, so a
+        // regular point gives the same bits in either instance (warp-uniform dispatch)
+        if (!wallish(kE) && !wallish(kW) && !wallish(kN) && !wallish(kS))
+            return ((R0.V[lc + 1] + Ra.V[lc + 1]) - (R0.V[lc - 1] + Ra.V[lc - 1])) * m.q_dx
+                 + ((Ra.U[lc] + Ra.U[lc + 1]) - (Rm.U[lc] + Rm.U[lc + 1])) * m.q_dy;
         vE = wallish(kE) ? slip(0.5 * vs, 0.0, 0.5 * dx) : 0.25 * (vs + (R0.V[lc + 1] + Ra.V[lc + 1]));
         vW = wallish(kW) ? slip(0.5 * vs, 0.0, 0.5 * dx) : 0.25 * ((R0.V[lc - 1] + Ra.V[lc - 1]) + vs);
         uN = wallish(kN) ? slip(0.5 * us, kN == CK_WALLY ? k.u_wt : 0.0, 0.5 * dy)
@@ -626,6 +632,13 @@ __device__ __forceinline__ void dp_general(const RingRow& R0, const RingRow& Ra,
                                            const MarchParams& m, const Geo& g, double& dpx, double& dpy,
                                            const Tp3& q3 = Tp3{})
 {
+    const bool nowall = !wallish(ckind(R0.KK[lc + 1])) && !wallish(ckind(R0.KK[lc - 1])) &&
+                        !wallish(ckind(Ra.KK[lc])) && !wallish(ckind(Rm.KK[lc]));
+    if (!NU && nowall) {                           // the regular instance's operations (same bits)
+        dpx = L3 ? (q3.P(1) - q3.P(-1)) * m.h_dx : (R0.P[lc + 1] - R0.P[lc - 1]) * m.h_dx;
+        dpy = L3 ? (q3.P(q3.pitch) - q3.P(-q3.pitch)) * m.h_dy : (Ra.P[lc] - Rm.P[lc]) * m.h_dy;
+        return;
+    }
     if (L3) {                                      // loop 3: the pressures of the previous sweep
         const double pc = q3.P(0);
         const double pe = wallish(ckind(R0.KK[lc + 1])) ? pc : 0.5 * (pc + q3.P(1));
@@ -897,6 +910,9 @@ __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int 
                 const double r = v.rv1;
                 apN = r * v.dvN * dx; bpN = r * v.vhatN * dx; sum += apN * PN();
             }
+            // four active faces: the regular instance's expression (same bits)
+            if (!NU && kwf == FK_ACTIVE && kef == FK_ACTIVE && vkind(kw0) == FK_ACTIVE && vkind(Ra.KK[lc]) == FK_ACTIVE)
+                sum = apW * PW() + apE * PE() + apS * PS() + apN * PN();
         }
         // a^p_0 = dV / T_new + dt sum a^p (Eq. pl24, R28); multiplied through by T_new
         // so one reciprocal serves: p = T_new (dt sum + b^p) / (dV + T_new dt sum a^p)

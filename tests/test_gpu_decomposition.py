@@ -237,3 +237,40 @@ def test_peer_group_no_halo_launches(S):
     for g in group:
         prof = g.profile_read(reset=True)
         assert prof["launches"] <= 3 * prof["pass_launches"], prof     # edge + general + regular sets only
+
+
+@pytest.mark.parametrize("variant", list(W.VARIANTS))
+def test_general_instance_same_bits(S, variant):
+    """The march kernel picks the regular or the general stage instances per warp
+    (a warp with any general point runs the general ones). That is only
+    decomposition-invariant because the general instance gives a regular point the
+    regular instance's bits: every point of the general kernel forced general
+    (STS_FORCE_GENERAL) must reproduce the default run bit for bit -- C1 and a
+    channel of squares touching each other and the walls."""
+    cases = [W.c1(variant, passes=3),
+             W.channel(75, 37, spacing=0.25, variant=variant, passes=3,
+                       squares=[(30, 14, 5, 4), (35, 18, 3, 3), (60, 0, 4, 6), (10, 31, 6, 6)])]
+    for case in cases:
+        out = []
+        for force in (False, True):
+            old = os.environ.pop("STS_FORCE_GENERAL", None)
+            old2 = os.environ.pop("STS_NO_ALLREG", None)
+            os.environ["STS_NO_ALLREG"] = "1"               # every CTA through the general kernel
+            if force:
+                os.environ["STS_FORCE_GENERAL"] = "1"
+            try:
+                g = S.Solver(case)
+                st = W.perturbed_state({f: g.get_field(f) for f in FIELDS}, W.perturbation(case, 9), vscale=0.05)
+                for f in ("p", "T", "u", "v"):
+                    g.set_field(f, st[f])
+                g.advance(3)
+                out.append({f: g.get_field(f) for f in FIELDS})
+            finally:
+                os.environ.pop("STS_FORCE_GENERAL", None)
+                os.environ.pop("STS_NO_ALLREG", None)
+                if old is not None:
+                    os.environ["STS_FORCE_GENERAL"] = old
+                if old2 is not None:
+                    os.environ["STS_NO_ALLREG"] = old2
+        for f in FIELDS:
+            assert np.array_equal(out[0][f], out[1][f]), (case["name"], f, np.abs(out[0][f] - out[1][f]).max())
