@@ -348,6 +348,26 @@ __global__ void red_push_kernel(const unsigned long long* slot, const unsigned l
 // ------------------------------------------------------------- kernel table
 typedef void (*march_fn)(MarchParams);
 // regk: the all-regular kernel (sts_march.cuh); nu: the non-uniform-mesh kernel
+// the first pass of an explicit step with the planes computed in the pass (N2)
+static march_fn march_fusec_table(int tvd, int regk, int graph)
+{
+    if (graph) {
+        if (regk) return tvd ? march_kernel<false, true, true, true, false, false, false, true> : march_kernel<false, false, true, true, false, false, false, true>;
+        return tvd ? march_kernel<false, true, true, false, false, false, false, true> : march_kernel<false, false, true, false, false, false, false, true>;
+    }
+    if (regk) return tvd ? march_kernel<false, true, false, true, false, false, false, true> : march_kernel<false, false, false, true, false, false, false, true>;
+    return tvd ? march_kernel<false, true, false, false, false, false, false, true> : march_kernel<false, false, false, false, false, false, false, true>;
+}
+static constexpr size_t FUSEC_SMEM = sizeof(MarchSmem) + 3 * RW * sizeof(double);
+// the explicit planes inside the first pass of each step: explicit variants on one
+// context without a halo, uniform mesh, no loop 3 (STS_NO_FUSE: the separate
+// conv kernel, as the paper does)
+static bool fuse_conv(const sts_ctx* c)
+{
+    return c->sch.time == STS_EXPLICIT && !c->nu && c->world == 1 && !c->comm && !c->peer && c->sch.loop3 <= 1 &&
+           !getenv("STS_NO_FUSE");
+}
+
 // the edge strips of a peer-connected rank: general kernel with the fused halo stores (N1)
 static march_fn march_halo_table(int impl, int tvd, int nu)
 {
@@ -424,6 +444,9 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
         CU(cudaFuncSetAttribute((const void*)march_halo_table(impl, tvd, nu), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(MarchSmem) + (nu ? RW * sizeof(double) : 0))));
     }
+    for (int q = 0; q < 8; q++)
+        CU(cudaFuncSetAttribute((const void*)march_fusec_table(q & 1, (q >> 1) & 1, q >> 2),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSEC_SMEM));
     for (int q = 0; q < 4; q++)
         CU(cudaFuncSetAttribute((const void*)conv_march_table(q & 1, q >> 1), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(ConvSmem) + ((q >> 1) ? RW * sizeof(double) : 0))));
@@ -637,25 +660,28 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
 // (fork / join by events; the same calls build the dependencies inside a graph
 // capture).  Returns the number of launches.
 static int launch_march(sts_ctx* c, const MarchParams& m, bool graph, cudaStream_t st, const int* order,
-                        int n_gen, int n_reg, bool l3 = false)
+                        int n_gen, int n_reg, bool l3 = false, bool fusec = false)
 {
     const int impl = c->sch.time == STS_IMPLICIT, tvd = c->sch.space == STS_TVD_VANLEER;
-    march_fn gen = l3 ? march_table(impl, tvd, 0, 0, 1) : graph ? march_graph_table(impl, tvd, 0, c->nu) : march_table(impl, tvd, 0, c->nu);
-    march_fn reg = l3 ? march_table(impl, tvd, 1, 0, 1) : graph ? march_graph_table(impl, tvd, 1) : march_table(impl, tvd, 1);
+    march_fn gen = fusec ? march_fusec_table(tvd, 0, graph)
+                 : l3 ? march_table(impl, tvd, 0, 0, 1) : graph ? march_graph_table(impl, tvd, 0, c->nu) : march_table(impl, tvd, 0, c->nu);
+    march_fn reg = fusec ? march_fusec_table(tvd, 1, graph)
+                 : l3 ? march_table(impl, tvd, 1, 0, 1) : graph ? march_graph_table(impl, tvd, 1) : march_table(impl, tvd, 1);
+    const size_t sm = fusec ? FUSEC_SMEM : march_smem(c);
     MarchParams mg = m, mr = m;
     mg.order = (const int4*)order;
     mr.order = (const int4*)order + n_gen;
     if (n_gen > 0 && n_reg > 0) {
         cudaEventRecord(c->ev_fork, st);
         cudaStreamWaitEvent(c->gstream, c->ev_fork, 0);
-        gen<<<n_gen, MX, march_smem(c), c->gstream>>>(mg);
+        gen<<<n_gen, MX, sm, c->gstream>>>(mg);
         cudaEventRecord(c->ev_join, c->gstream);
-        reg<<<n_reg, MX, march_smem(c), st>>>(mr);
+        reg<<<n_reg, MX, sm, st>>>(mr);
         cudaStreamWaitEvent(st, c->ev_join, 0);
         return 2;
     }
-    if (n_gen > 0) gen<<<n_gen, MX, march_smem(c), st>>>(mg);
-    else if (n_reg > 0) reg<<<n_reg, MX, march_smem(c), st>>>(mr);
+    if (n_gen > 0) gen<<<n_gen, MX, sm, st>>>(mg);
+    else if (n_reg > 0) reg<<<n_reg, MX, sm, st>>>(mr);
     return (n_gen > 0 || n_reg > 0) ? 1 : 0;
 }
 
@@ -1708,8 +1734,10 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
     k.u_1 = c->snap[n1].u; k.v_1 = c->snap[n1].v; k.p_1 = c->snap[n1].p; k.T_1 = c->snap[n1].T;
     k.ue = c->ue; k.ve = c->ve; k.Te = c->Te;
     const dim3 mgrid(c->n_gen + c->n_reg);                 // the conv kernel: every CTA of the schedule
-    auto pass = [&](int o, int w, int sl, cudaStream_t s) -> cudaError_t {
+    const bool fuse = fuse_conv(c);
+    auto pass = [&](int o, int w, int sl, cudaStream_t s, bool fz = false) -> cudaError_t {
         Params q = k;
+        if (fz) { q.ue_w = c->ue; q.ve_w = c->ve; q.Te_w = c->Te; }   // pass 1 computes the planes (N2)
         q.u_o = c->snap[o].u; q.v_o = c->snap[o].v; q.p_o = c->snap[o].p; q.T_o = c->snap[o].T;
         q.u_w = c->snap[w].u; q.v_w = c->snap[w].v; q.p_w = c->snap[w].p; q.T_w = c->snap[w].T;
         q.red = c->red2 + sl * 9;
@@ -1735,10 +1763,10 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
             mp.order = (const int4*)c->cta_order + (part ? c->n_gen : 0);
             void* args[] = {&mp};
             cudaKernelNodeParams kp = {};
-            kp.func = (void*)march_graph_table(impl, tvd, part, part ? 0 : c->nu);
+            kp.func = fz ? (void*)march_fusec_table(tvd, part, 1) : (void*)march_graph_table(impl, tvd, part, part ? 0 : c->nu);
             kp.gridDim = dim3(cnt);
             kp.blockDim = dim3(MX);
-            kp.sharedMemBytes = march_smem(c);
+            kp.sharedMemBytes = fz ? FUSEC_SMEM : march_smem(c);
             kp.kernelParams = args;
             e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
             if (e != cudaSuccess) return e;
@@ -1761,12 +1789,12 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
     CG(cudaGraphConditionalHandleCreate(&h, cg, 1, cudaGraphCondAssignDefault));
     CG(cudaMemsetAsync(c->red2, 0, 18 * sizeof(unsigned long long), cap));
     CG(cudaMemsetAsync(c->d_ls, 0, sizeof(LoopState), cap));
-    if (!impl) {                                  // a1: explicit planes of this step
+    if (!impl && !fuse) {                         // a1: explicit planes of this step
         Params q = k;
         q.ue_w = c->ue; q.ve_w = c->ve; q.Te_w = c->Te;
         conv_march_table(tvd, c->nu)<<<mgrid, MX, conv_smem(c), cap>>>(make_march(c, q));
     }
-    CG(pass(n1, a, 0, cap));
+    CG(pass(n1, a, 0, cap, fuse));
     loop_check_kernel<<<1, 32, 0, cap>>>(c->red2, c->d_ls, h, mn, mx, tol);
     CG(cudaGetLastError());
     CG(cudaStreamGetCaptureInfo(cap, &cst, nullptr, &cg, &deps, &nd));
@@ -1851,9 +1879,10 @@ static sts_status build_fix_graph(sts_ctx* ctx, int n1)
     Params k = make_params(c);
     k.u_1 = c->snap[n1].u; k.v_1 = c->snap[n1].v; k.p_1 = c->snap[n1].p; k.T_1 = c->snap[n1].T;
     k.ue = c->ue; k.ve = c->ve; k.Te = c->Te;
+    const bool fuse = fuse_conv(c);
     cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->red, 0, (size_t)c->sch.max_passes * 9 * sizeof(unsigned long long), cap);
-    if (e == cudaSuccess && !impl) {
+    if (e == cudaSuccess && !impl && !fuse) {
         Params q = k;
         q.ue_w = c->ue; q.ve_w = c->ve; q.Te_w = c->Te;
         conv_march_table(tvd, c->nu)<<<dim3(c->n_gen + c->n_reg), MX, conv_smem(c), cap>>>(make_march(c, q));
@@ -1865,6 +1894,8 @@ static sts_status build_fix_graph(sts_ctx* ctx, int n1)
         q.u_o = c->snap[old].u; q.v_o = c->snap[old].v; q.p_o = c->snap[old].p; q.T_o = c->snap[old].T;
         q.u_w = c->snap[nw].u; q.v_w = c->snap[nw].v; q.p_w = c->snap[nw].p; q.T_w = c->snap[nw].T;
         q.red = c->red + (size_t)it * 9;
+        const bool fz = fuse && it == 0;                  // pass 1 computes and stores the planes (N2)
+        if (fz) { q.ue_w = c->ue; q.ve_w = c->ve; q.Te_w = c->Te; }
         MarchParams m = make_march(c, q);
         m.pass_key = 0xFFFFF - it;
         cudaStreamCaptureStatus cs;
@@ -1883,10 +1914,10 @@ static sts_status build_fix_graph(sts_ctx* ctx, int n1)
             mp.order = (const int4*)c->cta_order + (part ? c->n_gen : 0);
             void* args[] = {&mp};
             cudaKernelNodeParams kp = {};
-            kp.func = (void*)march_table(impl, tvd, part, part ? 0 : c->nu);
+            kp.func = fz ? (void*)march_fusec_table(tvd, part, 0) : (void*)march_table(impl, tvd, part, part ? 0 : c->nu);
             kp.gridDim = dim3(cnt);
             kp.blockDim = dim3(MX);
-            kp.sharedMemBytes = march_smem(c);
+            kp.sharedMemBytes = fz ? FUSEC_SMEM : march_smem(c);
             kp.kernelParams = args;
             e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
             if (e == cudaSuccess && part == 0) e = graph_node_high_priority(nodes[nn]);
@@ -1996,7 +2027,8 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
             k.ue = c->ue; k.ve = c->ve; k.Te = c->Te;
             return k;
         };
-        if (!impl) {   // a1: explicit planes, once per time step
+        const bool fuse = n == 1 && fuse_conv(ctx);       // a1 inside pass 1 (N2)
+        if (!impl && !fuse) {   // a1: explicit planes, once per time step
             for (int r = 0; r < n; r++) {
                 sts_ctx* c = cs[r];
                 Params k = base(c, r);
@@ -2122,7 +2154,9 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
                     mk.pass_key = pkey;
                     if (gk) mk.done = &c->d_ls->done;
                     if (c->peer) return fail(c, STS_E_ARG, "peer-connected rank without edge strips");
-                    c->launches += launch_march(c, mk, gk, st, c->cta_order, c->n_gen, c->n_reg);
+                    const bool fz = fuse && it == 0;       // pass 1 computes and stores the planes
+                    if (fz) { mk.k.ue_w = c->ue; mk.k.ve_w = c->ve; mk.k.Te_w = c->Te; }
+                    c->launches += launch_march(c, mk, gk, st, c->cta_order, c->n_gen, c->n_reg, false, fz);
                     prof_end(c);
                 }
                 CU(cudaGetLastError());

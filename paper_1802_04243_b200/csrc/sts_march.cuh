@@ -298,13 +298,11 @@ __device__ __forceinline__ void ring_derive(ROW& r)
     for (int q = 0; q < n; q++) {
         const int lc = q == 0 ? t : MX + xl;
         const double Tv = r.T[lc];
-        if constexpr (WITH_GAMMA) {
-            const double y = frsqrt(Tv);
-            r.R[lc] = r.P[lc] * (y * y);
-            if constexpr (WITH_GAMMA) r.G[lc] = Tv * y;
-        } else {
-            r.R[lc] = fdiv(r.P[lc], Tv);
-        }
+        // the same rho bits with or without Gamma: the explicit planes computed in the
+        // first pass (N2) must equal conv_march_kernel's
+        const double y = frsqrt(Tv);
+        r.R[lc] = r.P[lc] * (y * y);
+        if constexpr (WITH_GAMMA) r.G[lc] = Tv * y;
     }
 }
 template <bool WITH_GAMMA = true>
@@ -923,6 +921,118 @@ __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int 
     s.PN[lc] = pn;
 }
 
+// ================= explicit planes inside the first pass of a step (N2) =================
+// In pass 1 of a time step the old iterate IS the n-1 state, so the ring
+// rows are exactly what conv_march_kernel reads and stage A's F^x, F^y of row j+1
+// are its fluxes.  The planes' face-value fluxes are computed here with the conv
+// kernel's operations (sts_conv_loop.inc, same order: same bits) and the planes
+// are formed in stage C, used by this pass, and stored for passes 2..N.
+// Shared rows (behind MarchSmem): TX (u-face i, row j), UX (cell i, row j), VX
+// (u-face column i, v-row j+1).  Carried: TY, uY, vY of the previous row step.
+struct ConvRows { double* TX; double* UX; double* VX; };
+template <bool TVD, bool REG>
+__device__ __forceinline__ void conv_A(const ConvRows& cr, int lc, const RingRow& Rm, const RingRow& R0,
+                                       const RingRow& Ra, const RingRow& Rb, const RingRow& Rc,
+                                       const FluxRow& Fc, const StepVars& v, double dx, double dy,
+                                       double& TYn, double& vYn)
+{
+    const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
+    const double Fx1 = v.Fx1, Fy1 = v.Fy1;
+    // TX at u-face (i, j): T flux through x^f_i (pl31_1)
+    {
+        double tx = 0.0;
+        if ((REG || flux_face(ukind(kw0)))) {
+            const double F = Fc.FX[lc], w = R0.U[lc], Tm = R0.T[lc - 1], Ti = R0.T[lc];
+            const double ps = (TVD && (REG || ckind(R0.KK[lc - 2]) == CK_FLUID) && (REG || ckind(R0.KK[lc - 1]) == CK_FLUID) &&
+                               (REG || ckind(kw0) == CK_FLUID) && (REG || ckind(R0.KK[lc + 1]) == CK_FLUID))
+                            ? psi_f(R0.T[lc - 2], Tm, Ti, R0.T[lc + 1], w) : 0.0;
+            tx = F * ((w > 0.0 ? Tm : Ti) + (Ti - Tm) * ps);
+        }
+        cr.TX[lc] = tx;
+    }
+    // TY at v-face (i, j+1)
+    TYn = 0.0;
+    if ((REG || vkind(kw1) == FK_ACTIVE)) {
+        const double w = Ra.V[lc], Tj = R0.T[lc], Tp = Ra.T[lc];
+        const double ps = (TVD && (REG || ckind(Rm.KK[lc]) == CK_FLUID) && (REG || ckind(kw0) == CK_FLUID) &&
+                           (REG || ckind(kw1) == CK_FLUID) && (REG || ckind(Rb.KK[lc]) == CK_FLUID))
+                        ? psi_f(Rm.T[lc], Tj, Tp, Rb.T[lc], w) : 0.0;
+        TYn = Fy1 * ((w > 0.0 ? Tj : Tp) + (Tp - Tj) * ps);
+    }
+    // uX at cell (i, j): u flux through the cell centre (transposed pl15_11 x-terms)
+    {
+        double ux = 0.0;
+        if ((REG || ckind(kw0) == CK_FLUID) && (REG || ukind(kw0) == FK_ACTIVE) && (REG || ukind(R0.KK[lc + 1]) == FK_ACTIVE)) {
+            const double ui = R0.U[lc], up = R0.U[lc + 1], ub = 0.5 * (ui + up);
+            const bool ok = TVD && (REG || ukind(R0.KK[lc - 1]) == FK_ACTIVE) && (REG || ukind(R0.KK[lc + 2]) == FK_ACTIVE);
+            const double ps = ok ? psi_f(R0.U[lc - 1], ui, up, R0.U[lc + 2], ub) : 0.0;
+            ux = dy * R0.R[lc] * ub * ((ub > 0.0 ? ui : up) + (up - ui) * ps);
+        } else if ((REG || ckind(kw0) == CK_FLUID)) {
+            const double ui = R0.U[lc], up = R0.U[lc + 1], ub = 0.5 * (ui + up);
+            ux = dy * R0.R[lc] * ub * (ub > 0.0 ? ui : up);
+        }
+        cr.UX[lc] = ux;
+    }
+    // vX at (u-face column i, v-row j+1): v flux through x^f_i, both half faces
+    {
+        double vx = 0.0;
+        if ((REG || vkind(kw1) == FK_ACTIVE) || (REG || vkind(Ra.KK[lc - 1]) == FK_ACTIVE)) {
+            const double vm = Ra.V[lc - 1], vi = Ra.V[lc];
+            const bool ok = TVD && (REG || vkind(Ra.KK[lc - 2]) == FK_ACTIVE) && (REG || vkind(Ra.KK[lc - 1]) == FK_ACTIVE) &&
+                            (REG || vkind(kw1) == FK_ACTIVE) && (REG || vkind(Ra.KK[lc + 1]) == FK_ACTIVE);
+            double sum = 0.0;
+            if ((REG || flux_face(ukind(kw0)))) {               // lower half: u-face (i, j)
+                const double F = Fc.FX[lc], w = R0.U[lc];
+                const double ps = ok ? psi_f(Ra.V[lc - 2], vm, vi, Ra.V[lc + 1], w) : 0.0;
+                sum += F * ((w > 0.0 ? vm : vi) + (vi - vm) * ps);
+            }
+            if ((REG || flux_face(ukind(kw1)))) {               // upper half: u-face (i, j+1)
+                const double F = Fx1, w = Ra.U[lc];
+                const double ps = ok ? psi_f(Ra.V[lc - 2], vm, vi, Ra.V[lc + 1], w) : 0.0;
+                sum += F * ((w > 0.0 ? vm : vi) + (vi - vm) * ps);
+            }
+            vx = 0.5 * sum;
+        }
+        cr.VX[lc] = vx;
+    }
+    // vY at cell (i, j+1): v flux through the cell centre (pl15_11 y-terms)
+    vYn = 0.0;
+    if ((REG || ckind(kw1) == CK_FLUID)) {
+        const double vi = Ra.V[lc], vp = Rb.V[lc], vb = 0.5 * (vi + vp);
+        const bool ok = TVD && (REG || vkind(kw1) == FK_ACTIVE) && (REG || vkind(Rb.KK[lc]) == FK_ACTIVE) &&
+                        (REG || vkind(kw0) == FK_ACTIVE) && (REG || vkind(Rc.KK[lc]) == FK_ACTIVE);
+        const double ps = ok ? psi_f(R0.V[lc], vi, vp, Rc.V[lc], vb) : 0.0;
+        vYn = dx * Ra.R[lc] * vb * ((vb > 0.0 ? vi : vp) + (vp - vi) * ps);
+    }
+}
+// uY at (u column i, y^f_{j+1}) (needs the neighbour's F^y: after B1), then the
+// planes of this point: T^exp(i, j), u^exp(i, j), v^exp(i, j+1).
+template <bool TVD, bool REG>
+__device__ __forceinline__ void conv_C(const ConvRows& cr, int lc, const RingRow& Rm, const RingRow& R0,
+                                       const RingRow& Ra, const RingRow& Rb, const FluxRow& Fn,
+                                       double TYc, double TYn, double uYc, double vYc, double vYn,
+                                       double& uYn, double& te, double& ue, double& ve)
+{
+    const uint32_t kw0 = R0.KK[lc], kw1 = Ra.KK[lc];
+    {
+        const double ui = R0.U[lc], up = Ra.U[lc];
+        const bool ok = TVD && (REG || ukind(Rm.KK[lc]) == FK_ACTIVE) && (REG || ukind(kw0) == FK_ACTIVE) &&
+                        (REG || ukind(kw1) == FK_ACTIVE) && (REG || ukind(Rb.KK[lc]) == FK_ACTIVE);
+        double sum = 0.0;
+        for (int h = 0; h < 2; h++) {
+            const int cc = lc - 1 + h;
+            if ((!REG && vkind(Ra.KK[cc]) != FK_ACTIVE)) continue;
+            const double F = Fn.FY[cc], w = Ra.V[cc];
+            const double ps = ok ? psi_f(Rm.U[lc], ui, up, Rb.U[lc], w) : 0.0;
+            sum += F * ((w > 0.0 ? ui : up) + (up - ui) * ps);
+        }
+        uYn = 0.5 * sum;
+    }
+    te = ckind(kw0) == CK_FLUID ? (cr.TX[lc] - cr.TX[lc + 1] + TYc - TYn) : 0.0;
+    ue = ukind(kw0) == FK_ACTIVE ? (cr.UX[lc - 1] - cr.UX[lc] + uYc - uYn) : 0.0;
+    ve = vkind(kw1) == FK_ACTIVE ? (cr.VX[lc] - cr.VX[lc + 1] + vYc - vYn) : 0.0;
+}
+
 struct Resid { double du, dv, dp, dT, vel, p, T; long long bad; int badf; bool nanv; };
 // Sticky bad-state key: bits 63..44 = 0xFFFFF - pass index (earliest pass wins
 // the max), 43..2 = 2^42 - 1 - flat cell index j nx + i (lowest cell wins),
@@ -1002,16 +1112,20 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
 // columns sit behind MarchSmem in shared memory, the row heights come from m.dyp.
 // HALO = true: the edge-strip kernel of a peer-connected rank (fused halo
 // stores in stage E, N1); every other launch compiles them out.
+// FUSEC = true: the first pass of an explicit step with the planes computed in
+// the pass (N2; single rank, uniform mesh), 3 more shared rows behind MarchSmem.
 template <bool IMPL, bool TVD, bool GRAPH = false, bool REGK = false, bool NU = false, bool L3 = false,
-          bool HALO = false>
+          bool HALO = false, bool FUSEC = false>
 __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
 {
+    static_assert(!(FUSEC && (IMPL || NU || L3 || HALO)), "plane fusion: explicit, uniform, single-rank passes");
     static_assert(!(HALO && (REGK || GRAPH || L3)), "fused halo stores: edge strips of the stream path only");
     static_assert(!(NU && REGK), "non-uniform meshes run the general kernel only");
     static_assert(!(NU && L3), "loop 3 runs on uniform meshes");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MarchSmem& s = *reinterpret_cast<MarchSmem*>(smem_raw);
     double* const s_dx = reinterpret_cast<double*>(smem_raw + sizeof(MarchSmem));   // NU only: RW widths
+    const ConvRows cr{s_dx, s_dx + RW, s_dx + 2 * RW};                               // FUSEC only
     const Params& k = m.k;
     // Early exit: loop 2 converged earlier in this graph launch, or a bad state
     // earlier in this advance call.  The bad key is written by other CTAs of this
@@ -1077,10 +1191,11 @@ __global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
     auto nm_prefetch_init = [&]() {
         nm.p1n = ld(k.p_1, js + 1); nm.T1n = ld(k.T_1, js + 1);
         nm.T1c = ld(k.T_1, js); nm.u1c = ld(k.u_1, js); nm.v1n = ldv(k.v_1, js + 1);
-        if (!IMPL) { nm.Tec = ld(k.Te, js); nm.uec = ld(k.ue, js); nm.ven = ldv(k.ve, js + 1); }
+        if (!IMPL && !FUSEC) { nm.Tec = ld(k.Te, js); nm.uec = ld(k.ue, js); nm.ven = ldv(k.ve, js + 1); }
     };
 
     Carry c{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 1.0, 0.0};
+    double cTY = 0.0, cuY = 0.0, cvY = 0.0;             // FUSEC: plane fluxes carried from the previous row
     Resid rs{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, -1, 0, false};
     StepVars v;
     int oj = js * k.pitch + col;                        // element offset of (row j, own column), + pitch per step (upwind prefetch)

@@ -138,3 +138,36 @@ def test_fixed_pass_graph_bad_state_step(S):
     st, stats = g.advance(3, check=False)
     assert st == S.STS_E_STATE
     assert stats["bad_pass"] == 4, stats
+
+
+@pytest.mark.parametrize("variant", ["explicit_upwind", "explicit_tvd"])
+@pytest.mark.parametrize("graph", [True, False])
+def test_planes_in_first_pass_match_conv_kernel(S, variant, graph):
+    """N2: the explicit planes computed inside the first pass of each step (the
+    default on one context) against the separate conv kernel (STS_NO_FUSE=1, as the
+    paper launches it): planes and fields bit for bit, C1 (square, walls,
+    inlet / outlet) and a periodic channel (wrapped ghost planes), graph and stream
+    drivers."""
+    for case in (W.c1(variant, passes=3), W.c2(small=True, variant=variant, passes=3)):
+        out = []
+        for fuse in (True, False):
+            saved = {k: os.environ.pop(k, None) for k in ("STS_NO_FUSE", "STS_NO_GRAPH")}
+            if not fuse:
+                os.environ["STS_NO_FUSE"] = "1"
+            if not graph:
+                os.environ["STS_NO_GRAPH"] = "1"
+            try:
+                g = S.Solver(case)
+                st = W.perturbed_state({f: g.get_field(f) for f in ("u", "v", "p", "T")},
+                                       W.perturbation(case, 13), vscale=0.01)
+                for f in ("p", "T", "u", "v"):
+                    g.set_field(f, st[f])
+                g.advance(3)
+                out.append({f: g.get_field(f) for f in FIELDS + ("uexp", "vexp", "Texp")})
+            finally:
+                for k in ("STS_NO_FUSE", "STS_NO_GRAPH"):
+                    os.environ.pop(k, None)
+                    if saved[k] is not None:
+                        os.environ[k] = saved[k]
+        for f in out[0]:
+            assert np.array_equal(out[0][f], out[1][f]), (case["name"], f, np.abs(out[0][f] - out[1][f]).max())
