@@ -1843,7 +1843,7 @@ static sts_status graph_step(sts_ctx* ctx, bool* conv)
     CU(cudaMemcpyAsync(c->h_ls, c->d_ls, sizeof(LoopState), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     const LoopState ls = *c->h_ls;
-    c->launches += 2 * ls.passes + (c->sch.time == STS_EXPLICIT ? 1 : 0);
+    c->launches += 2 * ls.passes + (c->sch.time == STS_EXPLICIT && !fuse_conv(c) ? 1 : 0);
     c->cur = (ls.passes & 1) ? a : b;             // pass 1 writes a, pass 2 b, ...
     *conv = ls.conv != 0;
     if (ls.checked) {
@@ -1955,7 +1955,7 @@ static sts_status fix_graph_advance(sts_ctx* ctx, int32_t n_steps, sts_stats* ou
         CU(cudaGraphLaunch(c->fix_exec[n1], c->stream));
         CU(cudaMemcpyAsync(c->h_badstep + s, c->bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
         c->cur = (P & 1) ? (n1 + 1) % 3 : (n1 + 2) % 3;          // pass 1 writes n1+1, pass 2 n1+2, ...
-        c->launches += 2 * P + (c->sch.time == STS_EXPLICIT ? 1 : 0);
+        c->launches += 2 * P + (c->sch.time == STS_EXPLICIT && !fuse_conv(c) ? 1 : 0);
         c->stats.steps_done++;
         c->stats.passes_done += P;
         c->stats.converged = 0;

@@ -1028,9 +1028,11 @@ __device__ __forceinline__ void conv_C(const ConvRows& cr, int lc, const RingRow
         }
         uYn = 0.5 * sum;
     }
-    te = ckind(kw0) == CK_FLUID ? (cr.TX[lc] - cr.TX[lc + 1] + TYc - TYn) : 0.0;
-    ue = ukind(kw0) == FK_ACTIVE ? (cr.UX[lc - 1] - cr.UX[lc] + uYc - uYn) : 0.0;
-    ve = vkind(kw1) == FK_ACTIVE ? (cr.VX[lc] - cr.VX[lc + 1] + vYc - vYn) : 0.0;
+    // (a regular point is a fluid cell with active faces; the all-regular kernel
+    // reads no kind words, so REG must not test them)
+    te = (REG || ckind(kw0) == CK_FLUID) ? (cr.TX[lc] - cr.TX[lc + 1] + TYc - TYn) : 0.0;
+    ue = (REG || ukind(kw0) == FK_ACTIVE) ? (cr.UX[lc - 1] - cr.UX[lc] + uYc - uYn) : 0.0;
+    ve = (REG || vkind(kw1) == FK_ACTIVE) ? (cr.VX[lc] - cr.VX[lc + 1] + vYc - vYn) : 0.0;
 }
 
 struct Resid { double du, dv, dp, dT, vel, p, T; long long bad; int badf; bool nanv; };
