@@ -136,12 +136,20 @@ def bench_case(args, world):
     weak scaling) are BASELINE.json's configs[3] and configs[4]."""
     from paper_1802_04243_b200 import workloads as W
     if args.workload == "C4":
-        return W.c4(args.variant, passes=args.passes)
-    if args.workload == "C5":
-        return W.c5(world, args.variant, passes=args.passes)
-    if world == 1:
-        return W.c3(200, args.variant, passes=args.passes)
-    return W.c3_long(world, args.variant, passes=args.passes)
+        case = W.c4(args.variant, passes=args.passes)
+    elif args.workload == "C5":
+        case = W.c5(world, args.variant, passes=args.passes)
+    elif world == 1:
+        case = W.c3(200, args.variant, passes=args.passes)
+    else:
+        case = W.c3_long(world, args.variant, passes=args.passes)
+    # feature paths (not the headline): loop 3 (N3), a stretched y mesh (N4)
+    if args.loop3 > 1:
+        case["loop3"] = args.loop3
+        case["name"] += f"_loop3x{args.loop3}"
+    if args.stretch > 0:
+        case = W.with_mesh(case, None, W.smooth_steps(case["ny"], case["spacing"], args.stretch))
+    return case
 
 
 # ------------------------------------------------------------ reference arm
@@ -444,6 +452,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     # N > 1 halo transport: the fused peer-memory path (N1, default) or NCCL send/recv
     ap.add_argument("--halo", default="peer", choices=["peer", "nccl"])
+    # feature paths: loop-3 sweeps per pass (N3) and a smoothly stretched y mesh (N4)
+    ap.add_argument("--loop3", type=int, default=1)
+    ap.add_argument("--stretch", type=float, default=0.0)
     args = ap.parse_args()
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         # communicator lines in the log (which ranks / devices / transports NCCL set up)

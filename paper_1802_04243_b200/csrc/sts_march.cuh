@@ -1116,9 +1116,12 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
 // stores in stage E, N1); every other launch compiles them out.
 // FUSEC = true: the first pass of an explicit step with the planes computed in
 // the pass (N2; single rank, uniform mesh), 3 more shared rows behind MarchSmem.
+#ifndef STS_GEN_CTAS
+#define STS_GEN_CTAS STS_MARCH_CTAS
+#endif
 template <bool IMPL, bool TVD, bool GRAPH = false, bool REGK = false, bool NU = false, bool L3 = false,
           bool HALO = false, bool FUSEC = false>
-__global__ void __launch_bounds__(MX, MARCH_CTAS) march_kernel(MarchParams m)
+__global__ void __launch_bounds__(MX, REGK ? MARCH_CTAS : STS_GEN_CTAS) march_kernel(MarchParams m)
 {
     static_assert(!(FUSEC && (IMPL || NU || L3 || HALO)), "plane fusion: explicit, uniform, single-rank passes");
     static_assert(!(HALO && (REGK || GRAPH || L3)), "fused halo stores: edge strips of the stream path only");
