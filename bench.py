@@ -262,27 +262,72 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     nccl_id = None
+    halo = args.halo if world > 1 else None
+    halo_note = None
     if world > 1:
         if os.environ.get("STS_BENCH_ONE_DEVICE"):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-        if args.halo == "nccl":
-            idt = torch.zeros(128, dtype=torch.uint8, device=dev)
-            if rank == 0:
-                idt.copy_(torch.frombuffer(bytearray(S.nccl_unique_id()), dtype=torch.uint8))
-            dist.broadcast(idt, 0)
-            nccl_id = bytes(idt.cpu().numpy().tolist())
 
     def make_solver(case, stream_ptr=None):
         """One rank's solver; N > 1: the fused halo over peer memory (N1, default)
         -- blobs of CUDA IPC handles exchanged over the process group -- or NCCL."""
         g = S.Solver(case, rank=rank, world=world, device=local, nccl_id=nccl_id, stream=stream_ptr)
-        if world > 1 and args.halo == "peer":
+        if world > 1 and halo == "peer":
             blobs = [None] * world
             dist.all_gather_object(blobs, g.peer_export())
             g.peer_connect(blobs)
         return g
+
+    def decomp_check():
+        """Every rank's slab of a small channel (96 columns per rank, a square each)
+        through the chosen transport against a one-slab run on rank 0, bit for bit;
+        True/False on rank 0 (None elsewhere), an exception text if it failed."""
+        small = W.channel(96 * world, 40, spacing=0.25, variant=args.variant, passes=4,
+                          squares=[(22 + 96 * q, 18, 4, 4) for q in range(world)])
+        err, same, parts = None, None, None
+        try:
+            gs = make_solver(small)
+            gs.advance(3)
+            parts = {f: gs.get_field(f) for f in ("u", "v", "p", "T")}
+            gs.close()
+        except Exception as e:      # a transport that does not work on this machine
+            err = f"{type(e).__name__}: {e}"
+        allp = [None] * world
+        dist.all_gather_object(allp, (err, parts))
+        errs = [e for e, _ in allp if e]
+        if rank == 0 and not errs:
+            ref = S.Solver(small, device=local)
+            ref.advance(3)
+            same = all(np.array_equal(ref.get_field(f), np.concatenate([p_[f] for _, p_ in allp], axis=1))
+                       for f in ("u", "v", "p", "T"))
+            ref.close()
+        flag = [same, errs[0] if errs else None]
+        dist.broadcast_object_list(flag, 0)
+        return flag
+
+    decomp = None
+    if world > 1:
+        # the transport is probed (and checked bit for bit) before the timed run; a
+        # peer transport that fails or disagrees here falls back to NCCL
+        if halo == "peer":
+            decomp, perr = decomp_check()
+            if perr or decomp is not True:
+                halo_note = f"peer transport unusable here ({perr or 'decomposition not bitwise'}); NCCL used"
+                halo = "nccl"
+        if halo == "nccl":
+            idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(S.nccl_unique_id()), dtype=torch.uint8))
+            if os.environ.get("STS_BENCH_ONE_DEVICE"):
+                ids = [bytes(idt.cpu().numpy().tolist())]
+                dist.broadcast_object_list(ids, 0)
+                nccl_id = ids[0]
+            else:
+                dist.broadcast(idt, 0)
+                nccl_id = bytes(idt.cpu().numpy().tolist())
+            decomp, _ = decomp_check()
 
     case = bench_case(args, world)
     stream = torch.cuda.current_stream(dev)
@@ -402,26 +447,6 @@ def run_ours(args):
                "wall_s": time.perf_counter() - t0,
                "path": "sts_set_field (pinned host -> device) x4, sts_advance(1), sts_get_field (device -> pinned host) x4"}
 
-    # N > 1: built-in decomposition check -- the same transport on a small channel
-    # (C1 geometry stretched to 96 columns per rank), every rank's slab against a
-    # single-slab run on rank 0, bit for bit (DESIGN 7: a cell's arithmetic does
-    # not depend on which slab owns it)
-    decomp = None
-    if world > 1:
-        small = W.channel(96 * world, 40, spacing=0.25, variant=args.variant, passes=4,
-                          squares=[(22 + 96 * q, 18, 4, 4) for q in range(world)])
-        gs = make_solver(small)
-        ref = S.Solver(small, device=local) if rank == 0 else None
-        gs.advance(3)
-        parts = [None] * world
-        dist.all_gather_object(parts, {f: gs.get_field(f) for f in ("u", "v", "p", "T")})
-        if ref is not None:
-            ref.advance(3)
-            decomp = all(np.array_equal(ref.get_field(f), np.concatenate([p_[f] for p_ in parts], axis=1))
-                         for f in ("u", "v", "p", "T"))
-            ref.close()
-        gs.close()
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.variant)
@@ -434,7 +459,7 @@ def run_ours(args):
             "config": {"workload": f"{case['name']}_{args.variant}", "nx": case["nx"], "ny": case["ny"],
                        "fv_per_gpu": nfv_rank, "passes_per_step": passes, "dt": case["dt"],
                        "parallelism": f"x-slabs{world}" if world > 1 else "single",
-                       "halo": (args.halo if world > 1 else None),
+                       "halo": halo, "halo_note": halo_note,
                        "l2": "inputs larger than L2 (>= 1.5 GB working set per GPU)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk.summary(),
