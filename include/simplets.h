@@ -177,11 +177,16 @@ sts_status sts_set_stream(sts_ctx* ctx, void* cuda_stream);
  * rho = p/T, u = u_in on every face, v = 0; fixed faces (solid, walls) 0. */
 sts_status sts_init_freestream(sts_ctx* ctx);
 
-/* Copy one global-shape field (STS_U, STS_V, STS_P or STS_T) from a host
- * buffer of n doubles into the current state; rho and Gamma follow from
- * p and T (Eqs. pl5, pl37); fixed faces are re-imposed. */
+/* Copy one field (STS_U, STS_V, STS_P or STS_T) from a host buffer of n
+ * doubles into the current state (all three snapshots); rho and Gamma follow
+ * from p and T (Eqs. pl5, pl37); ghost columns follow the BC spec and fixed
+ * faces are re-imposed (DESIGN 3.5).  The buffer is the GLOBAL shape, or on a
+ * multi-rank context this rank's owned slab (sts_shape); a slab-shaped input
+ * ends with a halo exchange, so every rank makes the call (collective).  On a
+ * peer-connected rank every call is a fenced halo phase (DESIGN 7.2).
+ * Synchronises the context stream; n of neither shape -> STS_E_ARG. */
 sts_status sts_set_field(sts_ctx* ctx, int32_t field, const double* host, int64_t n);
-/* Same from a DEVICE buffer (global shape). */
+/* Same from a DEVICE buffer (global or slab shape). */
 sts_status sts_set_field_device(sts_ctx* ctx, int32_t field, const double* dev, int64_t n);
 
 /* Non-uniform mesh (the general staggered mesh of Fig. 5, with the

@@ -171,3 +171,23 @@ def test_planes_in_first_pass_match_conv_kernel(S, variant, graph):
                         os.environ[k] = saved[k]
         for f in out[0]:
             assert np.array_equal(out[0][f], out[1][f]), (case["name"], f, np.abs(out[0][f] - out[1][f]).max())
+
+
+@pytest.mark.parametrize("variant", ["explicit_upwind", "explicit_tvd"])
+def test_graph_loop_vs_oracle_explicit(S, oracle_mod, variant):
+    """Tolerance mode for the explicit schemes: the conditional-WHILE graph with the
+    planes computed in the first pass (N2) takes the oracle's pass count (the oracle
+    computes the planes separately, before loop 2) and matches its fields."""
+    case = W.c1_small(variant, passes=300)
+    case["tol"] = 1e-9
+    g, o = seeded_pair(S, oracle_mod, case, seed=14)
+    done = 0
+    for _ in range(2):
+        st, stats = g.advance(1)
+        ost, ores, opasses = o.advance(1)
+        assert st == 0 and ost == 0 and stats["converged"] == 1
+        assert stats["passes_done"] - done == opasses, (stats["passes_done"] - done, opasses)
+        done = stats["passes_done"]
+    err = rel_errors({k: g.get_field(k) for k in FIELDS + ("uexp", "vexp", "Texp")},
+                     {**o.fields(), **{k: o.get(k) for k in ("uexp", "vexp", "Texp")}}, o.get_map(0) == 0)
+    assert max(err.values()) <= TOL, err
