@@ -9,6 +9,7 @@
 #include "../../include/simplets.h"
 #include "sts_common.cuh"
 #include "sts_march.cuh"
+#include "sts_regk.cuh"
 #include "sts_conv.cuh"
 
 #include <cuda.h>
@@ -378,6 +379,16 @@ static march_fn march_halo_table(int impl, int tvd, int nu)
     if (impl) return tvd ? march_kernel<true, true, false, false, false, false, true> : march_kernel<true, false, false, false, false, false, true>;
     return tvd ? march_kernel<false, true, false, false, false, false, true> : march_kernel<false, false, false, false, false, false, true>;
 }
+// the all-regular CTAs run regk_kernel (sts_regk.cuh, register-resident operands),
+// except implicit TVD (168 registers, 3 CTAs/SM and spills: 0.81 vs 0.74 ms/pass on
+// C3, profiles/r02_summary.md); STS_OLD_REGK=1 selects march_kernel<..., REGK = true>
+// for every variant, STS_OLD_REGK=0 regk_kernel for every variant (A/B, bitwise tests)
+static bool old_regk(int impl, int tvd)
+{
+    const char* v = getenv("STS_OLD_REGK");
+    if (v != nullptr && *v) return atoi(v) != 0;
+    return impl && tvd;
+}
 static march_fn march_table(int impl, int tvd, int regk, int nu = 0, int l3 = 0)
 {
     if (l3) {                                    // loop-3 sweeps k >= 2 (N3)
@@ -393,6 +404,10 @@ static march_fn march_table(int impl, int tvd, int regk, int nu = 0, int l3 = 0)
         return tvd ? march_kernel<false, true, false, false, true> : march_kernel<false, false, false, false, true>;
     }
     if (regk) {
+        if (!old_regk(impl, tvd)) {
+            if (impl) return tvd ? regk_kernel<true, true, false> : regk_kernel<true, false, false>;
+            return tvd ? regk_kernel<false, true, false> : regk_kernel<false, false, false>;
+        }
         if (impl) return tvd ? march_kernel<true, true, false, true> : march_kernel<true, false, false, true>;
         return tvd ? march_kernel<false, true, false, true> : march_kernel<false, false, false, true>;
     }
@@ -406,6 +421,10 @@ static march_fn march_graph_table(int impl, int tvd, int regk, int nu = 0)
         return tvd ? march_kernel<false, true, true, false, true> : march_kernel<false, false, true, false, true>;
     }
     if (regk) {
+        if (!old_regk(impl, tvd)) {
+            if (impl) return tvd ? regk_kernel<true, true, true> : regk_kernel<true, false, true>;
+            return tvd ? regk_kernel<false, true, true> : regk_kernel<false, false, true>;
+        }
         if (impl) return tvd ? march_kernel<true, true, true, true> : march_kernel<true, false, true, true>;
         return tvd ? march_kernel<false, true, true, true> : march_kernel<false, false, true, true>;
     }
@@ -438,6 +457,17 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
                         : graph ? march_graph_table(impl, tvd, regk, nu) : march_table(impl, tvd, regk, nu);
         CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(MarchSmem) + (nu ? RW * sizeof(double) : 0))));
+    }
+    {
+        const march_fn rk[] = {regk_kernel<false, false, false>, regk_kernel<false, true, false>, regk_kernel<true, false, false>,
+                               regk_kernel<true, true, false>, regk_kernel<false, false, true>, regk_kernel<false, true, true>,
+                               regk_kernel<true, false, true>, regk_kernel<true, true, true>,
+                               march_kernel<false, false, false, true>, march_kernel<false, true, false, true>,
+                               march_kernel<true, false, false, true>, march_kernel<true, true, false, true>,
+                               march_kernel<false, false, true, true>, march_kernel<false, true, true, true>,
+                               march_kernel<true, false, true, true>, march_kernel<true, true, true, true>};
+        for (march_fn f : rk)
+            CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));
     }
     for (int q = 0; q < 8; q++) {
         const int impl = q & 1, tvd = (q >> 1) & 1, nu = q >> 2;

@@ -52,6 +52,17 @@ __device__ __forceinline__ bool stored_col(const Params& k, int gi)
     return li >= 0 && li < k.pitch;
 }
 
+// Explicitly rounded products and fused multiply-adds.  The regular-point
+// arithmetic (the uniform-mesh stage expressions of sts_march.cuh and their
+// restatement in sts_regk.cuh) is written with these: a product that may feed an
+// addition is never a plain `*`, so the compiler has no contraction choice left
+// (its FMA-fusion heuristics depend on the surrounding code -- use counts, CSE --
+// and two kernels computing the same expression were measured to differ by one
+// ulp in ~5 % of the points).  Every kernel that computes a regular point then
+// gives the same bits, which the decomposition invariance relies on.
+__device__ __forceinline__ double MUL(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double FMA(double a, double b, double c) { return __fma_rn(a, b, c); }
+
 // max(0, a) exactly (also for -0 and NaN inputs of either sign' magnitude): clear
 // both words when the sign bit is set -- three integer ops, no fp64 compare/select
 __device__ __forceinline__ double max0(double a)

@@ -400,7 +400,7 @@ __device__ __forceinline__ void ring_issue_tma(SM& s, int sl, const MarchParams&
 // Convective part of an upwind/TVD link coefficient, max(0, F) - F psi (Eqs. pl15,
 // pl31); psi is the constant 0 without TVD, and F * 0 must not be formed
 // (IEEE cannot fold it: F * 0 is NaN for F = inf).
-#define STS_LINK(F, ps) (TVD ? max0(F) - (F) * (ps) : max0(F))
+#define STS_LINK(F, ps) (TVD ? FMA(-(F), (ps), max0(F)) : max0(F))
 
 // ================= stage A: row j+1 fluxes, link pieces =================
 // NU: the non-uniform-mesh instance (general points only): every step of the
@@ -426,9 +426,9 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             const double w = Ra.U[lc], r1 = Ra.R[lc - 1], r2 = Ra.R[lc];
             ru = w > 0.0 ? r1 : r2;
             if (TVD && cF<REG>(Ra.KK[lc - 2]) && cF<REG>(Ra.KK[lc - 1]) && cF<REG>(kw1) && cF<REG>(Ra.KK[lc + 1]))
-                ru += (NU ? psi_s_nu(Ra.R[lc - 2], r1, r2, Ra.R[lc + 1], X(-2), X(-1), X(0), X(1), w)
-                          : psi_f(Ra.R[lc - 2], r1, r2, Ra.R[lc + 1], w)) * (r2 - r1);
-            F = ru * w * dya;
+                ru = FMA(NU ? psi_s_nu(Ra.R[lc - 2], r1, r2, Ra.R[lc + 1], X(-2), X(-1), X(0), X(1), w)
+                            : psi_f(Ra.R[lc - 2], r1, r2, Ra.R[lc + 1], w), r2 - r1, ru);
+            F = MUL(MUL(ru, w), dya);
         }
         Fn.RU[lc] = ru;
         Fn.FX[lc] = F;
@@ -441,9 +441,9 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             const double w = Ra.V[lc], r1 = R0.R[lc], r2 = Ra.R[lc];
             rv = w > 0.0 ? r1 : r2;
             if (TVD && cF<REG>(Rm.KK[lc]) && cF<REG>(kw0) && cF<REG>(kw1) && cF<REG>(Rb.KK[lc]))
-                rv += (NU ? psi_s_nu(Rm.R[lc], r1, r2, Rb.R[lc], g.ym, g.y0, g.ya, g.yb, w)
-                          : psi_f(Rm.R[lc], r1, r2, Rb.R[lc], w)) * (r2 - r1);
-            F = rv * w * dx;
+                rv = FMA(NU ? psi_s_nu(Rm.R[lc], r1, r2, Rb.R[lc], g.ym, g.y0, g.ya, g.yb, w)
+                            : psi_f(Rm.R[lc], r1, r2, Rb.R[lc], w), r2 - r1, rv);
+            F = MUL(MUL(rv, w), dx);
         }
         v.rv1 = rv;
         Fn.FY[lc] = F;
@@ -459,13 +459,13 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             const double g1 = R0.G[lc - 1], g2 = R0.G[lc];
             // NU: C^T1 Gamma|_{x^f_i} Delta y_j / (0.5 (Delta x_{i-1} + Delta x_i)) with the harmonic
             // Gamma of Eq. pl33 = 2 C^T1 Delta y_j g1 g2 / (Delta x_{i-1} g2 + Delta x_i g1)
-            const double D = NU ? 2.0 * m.k.CT1 * g.y0 * g1 * g2 * rcp(X(-1) * g2 + dx * g1)
-                                : m.CT1_dydx * (2.0 * g1 * g2 * rcp(g1 + g2));
+            const double hg = MUL(MUL(MUL(2.0, g1), g2), rcp(g1 + g2));      // (uniform mesh)
             double ps = 0.0;
             if (IMPL && TVD && cF<REG>(R0.KK[lc - 2]) && cF<REG>(kl) && cF<REG>(kw0) && cF<REG>(R0.KK[lc + 1]))
                 ps = NU ? psi_s_nu(R0.T[lc - 2], R0.T[lc - 1], R0.T[lc], R0.T[lc + 1], X(-2), X(-1), X(0), X(1), R0.U[lc])
                         : psi_f(R0.T[lc - 2], R0.T[lc - 1], R0.T[lc], R0.T[lc + 1], R0.U[lc]);
-            pw = (IMPL ? STS_LINK(F, ps) : 0.0) + D;
+            pw = NU ? (IMPL ? STS_LINK(F, ps) : 0.0) + 2.0 * m.k.CT1 * g.y0 * g1 * g2 * rcp(X(-1) * g2 + dx * g1)
+                    : FMA(m.CT1_dydx, hg, IMPL ? STS_LINK(F, ps) : 0.0);
         }
         s.XTW[lc] = pw;
     }
@@ -475,29 +475,29 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
     if (!cW<REG>(kw0) && !cW<REG>(kw1)) {
         const double F = v.Fy1;
         const double g1 = R0.G[lc], g2 = Ra.G[lc];
-        const double D = NU ? 2.0 * m.k.CT1 * dx * g1 * g2 * rcp(g.y0 * g2 + g.ya * g1)
-                            : m.CT1_dxdy * (2.0 * g1 * g2 * rcp(g1 + g2));
+        const double hg = MUL(MUL(MUL(2.0, g1), g2), rcp(g1 + g2));          // (uniform mesh)
         double ps = 0.0;
         if (IMPL && TVD && cF<REG>(Rm.KK[lc]) && cF<REG>(kw0) && cF<REG>(kw1) && cF<REG>(Rb.KK[lc]))
             ps = NU ? psi_s_nu(Rm.T[lc], R0.T[lc], Ra.T[lc], Rb.T[lc], g.ym, g.y0, g.ya, g.yb, Ra.V[lc])
                     : psi_f(Rm.T[lc], R0.T[lc], Ra.T[lc], Rb.T[lc], Ra.V[lc]);
-        v.ytSn = (IMPL ? STS_LINK(F, ps) : 0.0) + D;
+        v.ytSn = NU ? (IMPL ? STS_LINK(F, ps) : 0.0) + 2.0 * m.k.CT1 * dx * g1 * g2 * rcp(g.y0 * g2 + g.ya * g1)
+                    : FMA(m.CT1_dxdy, hg, IMPL ? STS_LINK(F, ps) : 0.0);
         v.ytN = IMPL ? v.ytSn - F : v.ytSn;
     }
     // u-eq x pieces of cell (i, j): a^u_2 of face i, a^u_1 of face i+1 (transposed pl15)
     {
         double xe = 0.0, xw = 0.0, Fb = 0.0;
         if (cF<REG>(kw0)) {
-            const double ub = 0.5 * (R0.U[lc] + R0.U[lc + 1]);
-            Fb = R0.R[lc] * ub * (NU ? g.y0 : m.k.dy);
+            const double ub = MUL(0.5, R0.U[lc] + R0.U[lc + 1]);
+            Fb = MUL(MUL(R0.R[lc], ub), NU ? g.y0 : m.k.dy);
             // NU: 4/3 D^ux = 4/3 B Gamma_i Delta y_j / Delta x_i (transposed Eq. pl16)
-            const double D = NU ? 4.0 / 3.0 * m.k.B * R0.G[lc] * g.y0 * rcp(dx) : m.B43_dydx * R0.G[lc];
+            const double D = NU ? 4.0 / 3.0 * m.k.B * R0.G[lc] * g.y0 * rcp(dx) : 0.0;
             double ps = 0.0;
             if (IMPL && TVD && uA<REG>(R0.KK[lc - 1]) && uA<REG>(kw0) && uA<REG>(R0.KK[lc + 1]) &&
                 uA<REG>(R0.KK[lc + 2]))
                 ps = NU ? psi_c_nu(R0.U[lc - 1], R0.U[lc], R0.U[lc + 1], R0.U[lc + 2], X(-1), X(0), X(1), ub)
                         : psi_f(R0.U[lc - 1], R0.U[lc], R0.U[lc + 1], R0.U[lc + 2], ub);
-            xw = (IMPL ? STS_LINK(Fb, ps) : 0.0) + D;
+            xw = NU ? (IMPL ? STS_LINK(Fb, ps) : 0.0) + D : FMA(m.B43_dydx, R0.G[lc], IMPL ? STS_LINK(Fb, ps) : 0.0);
             xe = IMPL ? xw - Fb : xw;
         }
         s.XUW[lc] = xw;              // a^u_1 of face i+1 (neighbour); a^u_2 and F-bar stay here
@@ -522,20 +522,20 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
     v.vcSn = 0.0;
     v.FbN = 0.0;
     if (cF<REG>(kw1)) {
-        const double vb = 0.5 * (Ra.V[lc] + Rb.V[lc]);
-        v.FbN = Ra.R[lc] * vb * dx;
+        const double vb = MUL(0.5, Ra.V[lc] + Rb.V[lc]);
+        v.FbN = MUL(MUL(Ra.R[lc], vb), dx);
         // NU: 4/3 D^vy_{i,j+2} = 4/3 B Gamma_{i,j+1} Delta x_i / Delta y_{j+1} (Eq. pl16)
-        const double D = NU ? 4.0 / 3.0 * m.k.B * Ra.G[lc] * dx * rcp(g.ya) : m.B43_dxdy * Ra.G[lc];
+        const double D = NU ? 4.0 / 3.0 * m.k.B * Ra.G[lc] * dx * rcp(g.ya) : 0.0;
         double ps = 0.0;
         if (IMPL && TVD && vA<REG>(kw0) && vA<REG>(kw1) && vA<REG>(Rb.KK[lc]) && vA<REG>(Rc.KK[lc]))
             ps = NU ? psi_c_nu(R0.V[lc], Ra.V[lc], Rb.V[lc], Rc.V[lc], g.y0, g.ya, g.yb, vb)
                     : psi_f(R0.V[lc], Ra.V[lc], Rb.V[lc], Rc.V[lc], vb);
-        v.vcSn = (IMPL ? STS_LINK(v.FbN, ps) : 0.0) + D;
+        v.vcSn = NU ? (IMPL ? STS_LINK(v.FbN, ps) : 0.0) + D : FMA(m.B43_dxdy, Ra.G[lc], IMPL ? STS_LINK(v.FbN, ps) : 0.0);
         v.vcN = IMPL ? v.vcSn - v.FbN : v.vcSn;
     }
     // corner Gamma at (x^f_i, y^f_{j+1}) (R4, R5; BC spec 8)
     if (REG) {
-        v.gcN = 0.25 * (R0.G[lc - 1] + R0.G[lc] + Ra.G[lc - 1] + Ra.G[lc]);
+        v.gcN = MUL(0.25, R0.G[lc - 1] + R0.G[lc] + Ra.G[lc - 1] + Ra.G[lc]);
     } else if (NU) {
         // bilinear weights of the four cell centres, renormalised to the cells kept
         const double wxl = wleft(X(-1), dx), wxr = 1.0 - wxl;
@@ -553,7 +553,7 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
         if (!wallish(ckind(kw0))) { sum += R0.G[lc]; n++; }
         if (!wallish(ckind(Ra.KK[lc - 1]))) { sum += Ra.G[lc - 1]; n++; }
         if (!wallish(ckind(kw1))) { sum += Ra.G[lc]; n++; }
-        v.gcN = n == 4 ? 0.25 * sum : (n > 0 ? sum / n : 0.0);
+        v.gcN = n == 4 ? MUL(0.25, sum) : (n > 0 ? sum / n : 0.0);
     }
     // v-eq tangential pieces at (u-face column i, v-row j+1): a^v_1 of v-face (i, j+1),
     // a^v_2 of v-face (i-1, j+1)
@@ -572,9 +572,9 @@ __device__ __forceinline__ void stage_A(MarchSmem& s, const MarchParams& m, int 
             }
         }
         // NU: D^vx_{i,j+1} = B Gamma|_{x^f_i} (Delta y_j + Delta y_{j+1}) / (Delta x_{i-1} + Delta x_i) (Eq. pl16)
-        const double D = NU ? m.k.B * v.gcN * (g.y0 + g.ya) * rcp(X(-1) + dx) : m.B_dydx * v.gcN;
         v.FwSum = F1 + F2;
-        v.xvW = (IMPL ? 0.5 * (STS_LINK(F1, p1) + STS_LINK(F2, p2)) : 0.0) + D;
+        const double lk = IMPL ? MUL(0.5, STS_LINK(F1, p1) + STS_LINK(F2, p2)) : 0.0;
+        v.xvW = NU ? lk + m.k.B * v.gcN * (g.y0 + g.ya) * rcp(X(-1) + dx) : FMA(m.B_dydx, v.gcN, lk);
         s.XVW[lc] = v.xvW;           // the E side of v-face (i-1, j+1) is XVW - (F^x(j) + F^x(j+1))/2
     }
 }
@@ -611,8 +611,8 @@ __device__ __forceinline__ double shear_general(const RingRow& R0, const RingRow
         // no wall around the point: exactly the regular instance's operations, so a
         // regular point gives the same bits in either instance (warp-uniform dispatch)
         if (!wallish(kE) && !wallish(kW) && !wallish(kN) && !wallish(kS))
-            return ((R0.V[lc + 1] + Ra.V[lc + 1]) - (R0.V[lc - 1] + Ra.V[lc - 1])) * m.q_dx
-                 + ((Ra.U[lc] + Ra.U[lc + 1]) - (Rm.U[lc] + Rm.U[lc + 1])) * m.q_dy;
+            return FMA((R0.V[lc + 1] + Ra.V[lc + 1]) - (R0.V[lc - 1] + Ra.V[lc - 1]), m.q_dx,
+                       MUL((Ra.U[lc] + Ra.U[lc + 1]) - (Rm.U[lc] + Rm.U[lc + 1]), m.q_dy));
         vE = wallish(kE) ? slip(0.5 * vs, 0.0, 0.5 * dx) : 0.25 * (vs + (R0.V[lc + 1] + Ra.V[lc + 1]));
         vW = wallish(kW) ? slip(0.5 * vs, 0.0, 0.5 * dx) : 0.25 * ((R0.V[lc - 1] + Ra.V[lc - 1]) + vs);
         uN = wallish(kN) ? slip(0.5 * us, kN == CK_WALLY ? k.u_wt : 0.0, 0.5 * dy)
@@ -633,8 +633,8 @@ __device__ __forceinline__ void dp_general(const RingRow& R0, const RingRow& Ra,
     const bool nowall = !wallish(ckind(R0.KK[lc + 1])) && !wallish(ckind(R0.KK[lc - 1])) &&
                         !wallish(ckind(Ra.KK[lc])) && !wallish(ckind(Rm.KK[lc]));
     if (!NU && nowall) {                           // the regular instance's operations (same bits)
-        dpx = L3 ? (q3.P(1) - q3.P(-1)) * m.h_dx : (R0.P[lc + 1] - R0.P[lc - 1]) * m.h_dx;
-        dpy = L3 ? (q3.P(q3.pitch) - q3.P(-q3.pitch)) * m.h_dy : (Ra.P[lc] - Rm.P[lc]) * m.h_dy;
+        dpx = MUL(L3 ? q3.P(1) - q3.P(-1) : R0.P[lc + 1] - R0.P[lc - 1], m.h_dx);
+        dpy = MUL(L3 ? q3.P(q3.pitch) - q3.P(-q3.pitch) : Ra.P[lc] - Rm.P[lc], m.h_dy);
         return;
     }
     if (L3) {                                      // loop 3: the pressures of the previous sweep
@@ -713,19 +713,19 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         }
         // unsteady density: old iterate, or (loop 3) p / T of the previous sweep
         const double rq = L3 ? fdiv(q3.P(0), q3.Tt(0)) : rP;
-        const double a0 = IMPL ? dt * (a1 + a2 + a3 + a4 + FE - FW + FNl - FSl) + rq * dV
-                               : dt * (a1 + a2 + a3 + a4) + rq * dV;
+        const double a0 = IMPL ? FMA(dt, a1 + a2 + a3 + a4 + FE - FW + FNl - FSl, MUL(rq, dV))
+                               : FMA(dt, a1 + a2 + a3 + a4, MUL(rq, dV));
         // S^T_c, Eq. pl29 (R4 bilinear = 4-point mean on a uniform mesh); a mid-face
         // velocity on a wall face is the slip velocity of Eq. pl38 (R38)
         const double rdx = NU ? rcp(dx) : m.inv_dx, rdy = NU ? rcp(dy) : m.inv_dy;
-        const double dudx = (R0.U[lc + 1] - R0.U[lc]) * rdx;
-        const double dvdy = (Ra.V[lc] - R0.V[lc]) * rdy;
+        const double dudx = MUL(R0.U[lc + 1] - R0.U[lc], rdx);
+        const double dvdy = MUL(Ra.V[lc] - R0.V[lc], rdy);
         double shear;
         if (REG) {
             // dv/dx + du/dy from the bilinear face values (R4): v_E - v_W and u_N - u_S
             // as one difference each (the shared corner values cancel)
-            shear = ((R0.V[lc + 1] + Ra.V[lc + 1]) - (R0.V[lc - 1] + Ra.V[lc - 1])) * m.q_dx
-                  + ((Ra.U[lc] + Ra.U[lc + 1]) - (Rm.U[lc] + Rm.U[lc + 1])) * m.q_dy;
+            shear = FMA((R0.V[lc + 1] + Ra.V[lc + 1]) - (R0.V[lc - 1] + Ra.V[lc - 1]), m.q_dx,
+                        MUL((Ra.U[lc] + Ra.U[lc + 1]) - (Rm.U[lc] + Rm.U[lc + 1]), m.q_dy));
         } else {
             shear = shear_general<NU>(R0, Ra, Rm, lc, rP, m, g);
         }
@@ -737,36 +737,37 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         // p^{n-1} = rho^{n-1} T^{n-1} (the (p/T)^{n-1} row times T^{n-1}, within
         // 2 ulp of the stored p^{n-1})
         const double pc = L3 ? q3.P(0) : R0.P[lc];
-        const double p1 = s.R1[lc] * nm.T1c;
+        const double p1 = MUL(s.R1[lc], nm.T1c);
         double dpx, dpy;
         if (REG) {
-            dpx = L3 ? (q3.P(1) - q3.P(-1)) * m.h_dx : (R0.P[lc + 1] - R0.P[lc - 1]) * m.h_dx;
-            dpy = L3 ? (q3.P(q3.pitch) - q3.P(-q3.pitch)) * m.h_dy : (Ra.P[lc] - Rm.P[lc]) * m.h_dy;
+            dpx = MUL(L3 ? q3.P(1) - q3.P(-1) : R0.P[lc + 1] - R0.P[lc - 1], m.h_dx);
+            dpy = MUL(L3 ? q3.P(q3.pitch) - q3.P(-q3.pitch) : Ra.P[lc] - Rm.P[lc], m.h_dy);
         } else {
             dp_general<NU, L3>(R0, Ra, Rm, lc, m, g, dpx, dpy, q3);
         }
-        const double ub = 0.5 * (R0.U[lc] + R0.U[lc + 1]), vb = 0.5 * (R0.V[lc] + Ra.V[lc]);
-        const double pwork = m.pw_a * ((pc - p1) * m.inv_dt + ub * dpx + vb * dpy) + k.pwk * pc * div;
-        const double Sc = (k.CT2 * gP * (2.0 * (dudx * dudx + dvdy * dvdy) + shear * shear - 2.0 / 3.0 * div * div)
-                           + pwork) * dV;
-        const double rhs = dt * (a1 * T1 + a2 * T2 + a3 * T3 + a4 * T4 + (IMPL ? Sc : Sc + nm.Tec)) + p1 * dV;
-        v.TN = rhs * rcp(a0);
+        const double ub = MUL(0.5, R0.U[lc] + R0.U[lc + 1]), vb = MUL(0.5, R0.V[lc] + Ra.V[lc]);
+        const double pwork = FMA(m.pw_a, FMA(vb, dpy, FMA(ub, dpx, MUL(pc - p1, m.inv_dt))), MUL(MUL(k.pwk, pc), div));
+        const double Phi = FMA(MUL(-2.0 / 3.0, div), div, FMA(shear, shear, MUL(2.0, FMA(dvdy, dvdy, MUL(dudx, dudx)))));
+        const double Sc = MUL(FMA(MUL(k.CT2, gP), Phi, pwork), dV);
+        const double sT = FMA(a4, T4, FMA(a3, T3, FMA(a2, T2, MUL(a1, T1))));
+        const double rhs = FMA(dt, sT + (IMPL ? Sc : Sc + nm.Tec), MUL(p1, dV));
+        v.TN = MUL(rhs, rcp(a0));
     }
     // ---- u pseudo-velocity at u-face (i, j)
     {
         // N tangential link pieces at y^f_{j+1} (both sides; the S side is carried)
         const double F1 = v.Fy1, F2 = Fn.FY[lc - 1];
         // NU: D^uy = B Gamma|_{corner} (Delta x_{i-1} + Delta x_i) / (Delta y_j + Delta y_{j+1})
-        const double D = NU ? k.B * v.gcN * (dxw + dx) * rcp(dy + g.ya) : m.B_dxdy * v.gcN;
         v.FsSumN = F1 + F2;
-        v.utSn = (IMPL ? 0.5 * (STS_LINK(F1, v.upsi1) + STS_LINK(F2, v.upsi2)) : 0.0) + D;
-        const double a4p = IMPL ? v.utSn - 0.5 * v.FsSumN : v.utSn;
+        const double lk = IMPL ? MUL(0.5, STS_LINK(F1, v.upsi1) + STS_LINK(F2, v.upsi2)) : 0.0;
+        v.utSn = NU ? lk + k.B * v.gcN * (dxw + dx) * rcp(dy + g.ya) : FMA(m.B_dxdy, v.gcN, lk);
+        const double a4p = IMPL ? FMA(-0.5, v.FsSumN, v.utSn) : v.utSn;
         double uhat = 0.0, du = 0.0;
         if (uA<REG>(kw0)) {
             const double rL = R0.R[lc - 1], rR = rP, gL = R0.G[lc - 1], gR = gP;
             const double a1 = s.XUW[lc - 1], a2 = v.xe;
             // F-bar^x of cell i-1, recomputed with the same operations as its owner
-            const double FbW = rL * (0.5 * (R0.U[lc - 1] + R0.U[lc])) * dy, FbE = v.Fb;
+            const double FbW = MUL(MUL(rL, MUL(0.5, R0.U[lc - 1] + R0.U[lc])), dy), FbE = v.Fb;
             double a3, a4, uS, uN, FsS, FnS;
             if (REG) {
                 a3 = c.utS; FsS = c.FsSum; uS = Rm.U[lc];
@@ -786,18 +787,20 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
                 } else { a4 = a4p; FnS = v.FsSumN; uN = Ra.U[lc]; }
             }
             // unsteady term (rho_i Delta x_i + rho_{i-1} Delta x_{i-1}) Delta y_j / (2 dt) (transposed pl15)
-            const double tterm = NU ? (rR * dx + rL * dxw) * dy * (0.5 * m.inv_dt) : (rR + rL) * m.c_t;
-            const double a0 = IMPL ? a1 + a2 + a3 + a4 + FbE - FbW + 0.5 * (FnS - FsS) + tterm
+            const double tterm = NU ? (rR * dx + rL * dxw) * dy * (0.5 * m.inv_dt) : MUL(rR + rL, m.c_t);
+            const double a0 = IMPL ? FMA(0.5, FnS - FsS, a1 + a2 + a3 + a4 + FbE - FbW) + tterm
                                    : a1 + a2 + a3 + a4 + tterm;
-            const double b = (NU ? (s.R1[lc] * dx + s.R1[lc - 1] * dxw) * dy * (0.5 * m.inv_dt)
-                                 : (s.R1[lc] + s.R1[lc - 1]) * m.c_t) * nm.u1c
-                           + k.B * (v.gcN * (Ra.V[lc] - Ra.V[lc - 1]) - c.gcP * (R0.V[lc] - R0.V[lc - 1])
-                                    - 2.0 / 3.0 * gR * (Ra.V[lc] - R0.V[lc])
-                                    + 2.0 / 3.0 * gL * (Ra.V[lc - 1] - R0.V[lc - 1]))
-                           + (NU ? k.g_x * 0.5 * (rR * dx + rL * dxw) * dy : k.g_x * (rR + rL) * m.half_dV);
+            const double bt = NU ? (s.R1[lc] * dx + s.R1[lc - 1] * dxw) * dy * (0.5 * m.inv_dt)
+                                 : MUL(s.R1[lc] + s.R1[lc - 1], m.c_t);
+            const double bg = NU ? k.g_x * 0.5 * (rR * dx + rL * dxw) * dy : MUL(MUL(k.g_x, rR + rL), m.half_dV);
+            const double bv = FMA(MUL(2.0 / 3.0, gL), Ra.V[lc - 1] - R0.V[lc - 1],
+                              FMA(MUL(-2.0 / 3.0, gR), Ra.V[lc] - R0.V[lc],
+                              FMA(-c.gcP, R0.V[lc] - R0.V[lc - 1], MUL(v.gcN, Ra.V[lc] - Ra.V[lc - 1]))));
+            const double b = FMA(k.B, bv, MUL(bt, nm.u1c)) + bg;
             const double r = rcp(a0);
-            uhat = (a1 * R0.U[lc - 1] + a2 * R0.U[lc + 1] + a3 * uS + a4 * uN + (IMPL ? b : b + nm.uec)) * r;
-            du = (NU ? k.A * dy : m.A_dy) * r;
+            const double su = FMA(a4, uN, FMA(a3, uS, FMA(a2, R0.U[lc + 1], MUL(a1, R0.U[lc - 1]))));
+            uhat = MUL(su + (IMPL ? b : b + nm.uec), r);
+            du = MUL(NU ? k.A * dy : m.A_dy, r);
         }
         v.uhat = uhat;
         v.du = du;
@@ -813,7 +816,7 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
         double a1, a2, vW, vE, FwS, FeS;
         if (REG) {
             a1 = v.xvW; FwS = v.FwSum; vW = Ra.V[lc - 1];
-            FeS = Fn.FX[lc + 1] + Fc.FX[lc + 1]; a2 = IMPL ? s.XVW[lc + 1] - 0.5 * FeS : s.XVW[lc + 1]; vE = Ra.V[lc + 1];
+            FeS = Fn.FX[lc + 1] + Fc.FX[lc + 1]; a2 = IMPL ? FMA(-0.5, FeS, s.XVW[lc + 1]) : s.XVW[lc + 1]; vE = Ra.V[lc + 1];
         } else {
             FwS = FeS = 0.0;
             const double gadj = 0.5 * (gB + gT);
@@ -824,12 +827,12 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
             } else { a1 = v.xvW; FwS = v.FwSum; vW = Ra.V[lc - 1]; }
             if (ckind(R0.KK[lc + 1]) == CK_SOLID && ckind(Ra.KK[lc + 1]) == CK_SOLID) {
                 a2 = k.B * gadj * L * rcp(0.5 * dx + zeta); vE = 0.0;
-            } else { FeS = Fn.FX[lc + 1] + Fc.FX[lc + 1]; a2 = IMPL ? s.XVW[lc + 1] - 0.5 * FeS : s.XVW[lc + 1]; vE = Ra.V[lc + 1]; }
+            } else { FeS = Fn.FX[lc + 1] + Fc.FX[lc + 1]; a2 = IMPL ? FMA(-0.5, FeS, s.XVW[lc + 1]) : s.XVW[lc + 1]; vE = Ra.V[lc + 1]; }
         }
         // corner Gamma (i+1, j+1), recomputed with the same operations as its owner
         double gcE;
         if (REG) {
-            gcE = 0.25 * (R0.G[lc] + R0.G[lc + 1] + Ra.G[lc] + Ra.G[lc + 1]);
+            gcE = MUL(0.25, R0.G[lc] + R0.G[lc + 1] + Ra.G[lc] + Ra.G[lc + 1]);
         } else if (NU) {
             const double wxl = wleft(dx, g.dxr[lc + 1]), wxr = 1.0 - wxl;
             const double wyb = wleft(dy, dyT), wyt = 1.0 - wyb;
@@ -846,21 +849,23 @@ __device__ __forceinline__ void stage_C(MarchSmem& s, const MarchParams& m, int 
             if (!wallish(ckind(R0.KK[lc + 1]))) { sum += R0.G[lc + 1]; n++; }
             if (!wallish(ckind(Ra.KK[lc]))) { sum += Ra.G[lc]; n++; }
             if (!wallish(ckind(Ra.KK[lc + 1]))) { sum += Ra.G[lc + 1]; n++; }
-            gcE = n == 4 ? 0.25 * sum : (n > 0 ? sum / n : 0.0);
+            gcE = n == 4 ? MUL(0.25, sum) : (n > 0 ? sum / n : 0.0);
         }
         const double a3 = c.vcS, a4 = v.vcN;
         // unsteady term (rho_{j+1} Delta y_{j+1} + rho_j Delta y_j) Delta x_i / (2 dt) (Eq. pl15)
-        const double tterm = NU ? (rT * dyT + rB * dy) * dx * (0.5 * m.inv_dt) : (rT + rB) * m.c_t;
-        const double a0 = IMPL ? a1 + a2 + a3 + a4 + 0.5 * (FeS - FwS) + v.FbN - c.FbS + tterm
+        const double tterm = NU ? (rT * dyT + rB * dy) * dx * (0.5 * m.inv_dt) : MUL(rT + rB, m.c_t);
+        const double a0 = IMPL ? FMA(0.5, FeS - FwS, a1 + a2 + a3 + a4) + v.FbN - c.FbS + tterm
                                : a1 + a2 + a3 + a4 + tterm;
-        const double b = (NU ? (v.r1n * dyT + s.R1[lc] * dy) * dx * (0.5 * m.inv_dt) : (v.r1n + s.R1[lc]) * m.c_t) * nm.v1n
-                       + k.B * (gcE * (Ra.U[lc + 1] - R0.U[lc + 1]) - v.gcN * (Ra.U[lc] - R0.U[lc])
-                                - 2.0 / 3.0 * gT * (Ra.U[lc + 1] - Ra.U[lc])
-                                + 2.0 / 3.0 * gB * (R0.U[lc + 1] - R0.U[lc]))
-                       + (NU ? k.g_y * 0.5 * (rT * dyT + rB * dy) * dx : k.g_y * (rT + rB) * m.half_dV);
+        const double bt = NU ? (v.r1n * dyT + s.R1[lc] * dy) * dx * (0.5 * m.inv_dt) : MUL(v.r1n + s.R1[lc], m.c_t);
+        const double bg = NU ? k.g_y * 0.5 * (rT * dyT + rB * dy) * dx : MUL(MUL(k.g_y, rT + rB), m.half_dV);
+        const double bv = FMA(MUL(2.0 / 3.0, gB), R0.U[lc + 1] - R0.U[lc],
+                          FMA(MUL(-2.0 / 3.0, gT), Ra.U[lc + 1] - Ra.U[lc],
+                          FMA(-v.gcN, Ra.U[lc] - R0.U[lc], MUL(gcE, Ra.U[lc + 1] - R0.U[lc + 1]))));
+        const double b = FMA(k.B, bv, MUL(bt, nm.v1n)) + bg;
         const double r = rcp(a0);
-        v.vhatN = (a1 * vW + a2 * vE + a3 * R0.V[lc] + a4 * Rb.V[lc] + (IMPL ? b : b + nm.ven)) * r;
-        v.dvN = (NU ? k.A * dx : m.A_dx) * r;
+        const double sv = FMA(a4, Rb.V[lc], FMA(a3, R0.V[lc], FMA(a2, vE, MUL(a1, vW))));
+        v.vhatN = MUL(sv + (IMPL ? b : b + nm.ven), r);
+        v.dvN = MUL(NU ? k.A * dx : m.A_dx, r);
     }
 }
 
@@ -885,37 +890,37 @@ __device__ __forceinline__ void stage_D(MarchSmem& s, const MarchParams& m, int 
         auto PN = [&] { return L3 ? q3.P(q3.pitch) : Ra.P[lc]; };
         if (REG) {
             const double rw = Fc.RU[lc], re = Fc.RU[lc + 1], rs = c.rvS, rn = v.rv1;
-            apW = rw * v.du * dy; bpW = rw * v.uhat * dy;
-            apE = re * s.DU[lc + 1] * dy; bpE = re * s.UH[lc + 1] * dy;
-            apS = rs * c.dvP * dx; bpS = rs * c.vhatP * dx;
-            apN = rn * v.dvN * dx; bpN = rn * v.vhatN * dx;
-            sum = apW * PW() + apE * PE() + apS * PS() + apN * PN();
+            apW = MUL(MUL(rw, v.du), dy); bpW = MUL(MUL(rw, v.uhat), dy);
+            apE = MUL(MUL(re, s.DU[lc + 1]), dy); bpE = MUL(MUL(re, s.UH[lc + 1]), dy);
+            apS = MUL(MUL(rs, c.dvP), dx); bpS = MUL(MUL(rs, c.vhatP), dx);
+            apN = MUL(MUL(rn, v.dvN), dx); bpN = MUL(MUL(rn, v.vhatN), dx);
+            sum = FMA(apN, PN(), FMA(apS, PS(), FMA(apE, PE(), MUL(apW, PW()))));
         } else {
             const uint8_t kwf = ukind(kw0), kef = ukind(R0.KK[lc + 1]);
             if (kwf == FK_ACTIVE) {
                 const double r = Fc.RU[lc];
-                apW = r * v.du * dy; bpW = r * v.uhat * dy; sum += apW * PW();
-            } else if (kwf == FK_INLET) bpW = Fc.RU[lc] * k.u_in * dy;
+                apW = MUL(MUL(r, v.du), dy); bpW = MUL(MUL(r, v.uhat), dy); sum = FMA(apW, PW(), sum);
+            } else if (kwf == FK_INLET) bpW = MUL(MUL(Fc.RU[lc], k.u_in), dy);
             if (kef == FK_ACTIVE) {
                 const double r = Fc.RU[lc + 1];
-                apE = r * s.DU[lc + 1] * dy; bpE = r * s.UH[lc + 1] * dy; sum += apE * PE();
-            } else if (kef == FK_OUTLET) bpE = Fc.RU[lc + 1] * R0.U[lc] * dy;
+                apE = MUL(MUL(r, s.DU[lc + 1]), dy); bpE = MUL(MUL(r, s.UH[lc + 1]), dy); sum = FMA(apE, PE(), sum);
+            } else if (kef == FK_OUTLET) bpE = MUL(MUL(Fc.RU[lc + 1], R0.U[lc]), dy);
             if (vkind(kw0) == FK_ACTIVE) {
                 const double r = c.rvS;
-                apS = r * c.dvP * dx; bpS = r * c.vhatP * dx; sum += apS * PS();
+                apS = MUL(MUL(r, c.dvP), dx); bpS = MUL(MUL(r, c.vhatP), dx); sum = FMA(apS, PS(), sum);
             }
             if (vkind(Ra.KK[lc]) == FK_ACTIVE) {
                 const double r = v.rv1;
-                apN = r * v.dvN * dx; bpN = r * v.vhatN * dx; sum += apN * PN();
+                apN = MUL(MUL(r, v.dvN), dx); bpN = MUL(MUL(r, v.vhatN), dx); sum = FMA(apN, PN(), sum);
             }
             // four active faces: the regular instance's expression (same bits)
             if (!NU && kwf == FK_ACTIVE && kef == FK_ACTIVE && vkind(kw0) == FK_ACTIVE && vkind(Ra.KK[lc]) == FK_ACTIVE)
-                sum = apW * PW() + apE * PE() + apS * PS() + apN * PN();
+                sum = FMA(apN, PN(), FMA(apS, PS(), FMA(apE, PE(), MUL(apW, PW()))));
         }
         // a^p_0 = dV / T_new + dt sum a^p (Eq. pl24, R28); multiplied through by T_new
         // so one reciprocal serves: p = T_new (dt sum + b^p) / (dV + T_new dt sum a^p)
-        const double bp = s.R1[lc] * dV - (bpE - bpW + bpN - bpS) * dt;
-        pn = v.TN * (sum * dt + bp) * rcp(fma(v.TN * dt, apW + apE + apS + apN, dV));
+        const double bp = FMA(-(bpE - bpW + bpN - bpS), dt, MUL(s.R1[lc], dV));
+        pn = MUL(MUL(v.TN, FMA(sum, dt, bp)), rcp(FMA(MUL(v.TN, dt), apW + apE + apS + apN, dV)));
     }
     v.pn = pn;
     s.PN[lc] = pn;
@@ -1069,7 +1074,7 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
     }
     double un = 0.0;
     if (uA<REG>(kw0)) {
-        un = v.uhat - v.du * (v.pn - s.PN[lc - 1]);
+        un = FMA(-v.du, v.pn - s.PN[lc - 1], v.uhat);
         rs.du = dmax(rs.du, fabs(un - R0.U[lc]));
         rs.vel = dmax(rs.vel, fabs(un));
         rs.nanv |= un != un;
@@ -1077,7 +1082,7 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
     k.u_w[id] = un;
     double vn = 0.0;
     if (vA<REG>(kw0)) {
-        vn = c.vhatP - c.dvP * (v.pn - c.pnP);
+        vn = FMA(-c.dvP, v.pn - c.pnP, c.vhatP);
         rs.dv = dmax(rs.dv, fabs(vn - R0.V[lc]));
         rs.vel = dmax(rs.vel, fabs(vn));
         rs.nanv |= vn != vn;

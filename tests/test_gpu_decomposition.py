@@ -274,3 +274,37 @@ def test_general_instance_same_bits(S, variant):
                     os.environ["STS_NO_ALLREG"] = old2
         for f in FIELDS:
             assert np.array_equal(out[0][f], out[1][f]), (case["name"], f, np.abs(out[0][f] - out[1][f]).max())
+
+
+@pytest.mark.parametrize("variant", list(W.VARIANTS))
+def test_regk_same_bits(S, variant):
+    """The all-regular CTAs run regk_kernel (sts_regk.cuh: the regular stage
+    instances restated with register-resident operands); the round-2 kernel
+    (march_kernel<..., REGK>, STS_OLD_REGK=1) and every CTA through the general
+    kernel (STS_NO_ALLREG) must give the same bits, on the stream path and in the
+    fixed-pass step graphs."""
+    case = W.channel(520, 96, spacing=0.25, variant=variant, passes=4, squares=[(200, 40, 10, 10)])
+    out = []
+    for env in ({"STS_SEG": "16", "STS_OLD_REGK": "0"}, {"STS_SEG": "16", "STS_OLD_REGK": "1"}, {"STS_SEG": "16", "STS_NO_ALLREG": "1"}):
+        keys = ("STS_SEG", "STS_NO_ALLREG", "STS_OLD_REGK")
+        old = {k: os.environ.get(k) for k in keys}
+        for k in keys:
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        try:
+            g = S.Solver(case)
+            base = {k: g.get_field(k) for k in ("u", "v", "p", "T")}
+            st = W.perturbed_state(base, W.perturbation(case, seed=9), vscale=0.05)
+            for k in ("p", "T", "u", "v"):
+                g.set_field(k, st[k])
+            g.advance(3)
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        out.append({f: g.get_field(f) for f in FIELDS})
+    for f in FIELDS:
+        assert np.array_equal(out[0][f], out[1][f]), (f, np.abs(out[0][f] - out[1][f]).max())
+        assert np.array_equal(out[0][f], out[2][f]), (f, np.abs(out[0][f] - out[2][f]).max())
