@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -553,12 +554,23 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     const int ny = c->ny;
     // warp costs relative to an all-regular warp: a warp with any general point runs
     // the general instance (warp-uniform dispatch, sts_march_loop.inc)
-    double w_gen = 1.35, w_mix = 1.35;
+    // (regk_kernel, v10: a row of a general CTA costs ~3 regk rows -- the general kernel
+    // runs the round-2 regular instance at 4 CTAs/SM beside the general one; measured
+    // over 4032 x {200, 400, 4000}, profiles/r02_v10_seg_grid.txt)
+    double w_gen = 3.0, w_mix = 3.0;
     if (const char* cv = getenv("STS_COST")) sscanf(cv, "%lf,%lf", &w_gen, &w_mix);   // tuning hook
     // every CTA general: test hook, or a non-uniform mesh (the NU kernel has general instances only)
     const bool no_allreg = getenv("STS_NO_ALLREG") != nullptr || c->nu;
-    int forced = 0;
-    if (const char* sv = getenv("STS_SEG")) forced = std::max(0, atoi(sv));   // test hook: all heights
+    int forced = 0, forced_r = 0;
+    if (const char* sv = getenv("STS_SEG")) {                 // test hook: all heights, or "Hg,Hr"
+        forced = std::max(0, atoi(sv));
+        const char* cm = strchr(sv, ',');
+        forced_r = cm ? std::max(0, atoi(cm + 1)) : forced;
+    }
+    // fixed cost of a CTA in row steps (prologue: 5 ring rows, 4 derives, the
+    // residual epilogue, launch) -- tuning hook STS_CTA_OVH
+    double ovh = 0.0;
+    if (const char* ov = getenv("STS_CTA_OVH")) ovh = atof(ov);
     // per (strip, row): cost of a row step and "all 128 points regular"
     std::vector<double> rcost((size_t)strips * ny);
     std::vector<uint8_t> rreg((size_t)strips * ny);
@@ -588,7 +600,7 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
         double cst = 0.0;
         for (int q = std::max(0, J0 - WARM); q < J1; q++) cst += rcost[(size_t)st * ny + q];
         if (J0 - WARM < 0) cst += (WARM - J0) * rcost[(size_t)st * ny + 0];
-        return cst;
+        return cst + ovh;
     };
     // the CTAs of one strip for heights (Hg, Hr)
     auto cut = [&](int st, int Hg, int Hr, std::vector<CtaE>& out) {
@@ -623,26 +635,47 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     double best_ms = 1e300;
     int best_hg = 8, best_hr = 8;
     std::vector<int> hg_c, hr_c;
-    if (forced > 0) { hg_c = {forced}; hr_c = {forced}; }
+    if (forced > 0) { hg_c = {forced}; hr_c = {forced_r > 0 ? forced_r : forced}; }
     else {
-        hg_c = {4, 6, 8, 12, 16, 24, 32, 48};
-        // Hr: 8, 10, ..., 64.  Longer regular CTAs look cheaper to the model (fewer
-        // warm-up rows) but measure slower: a slot is not a processor -- the CTAs
-        // resident on one SM share its issue rate, so a schedule of few long CTAs
-        // leaves SMs with 3 CTAs beside SMs with 4 and a long tail (C3: Hr 252,
-        // 501 CTAs 0.630 ms/pass; forced 48-row CTAs 0.606 ms, profiles/r02_summary.md)
+        hg_c = {4, 6, 8, 12, 16};   // short general CTAs: 24-48 rows measured 3-6 % slower (C3)
+        // Hr: 4, 6, ..., 96.  Longer regular CTAs look cheaper to the model (fewer
+        // warm-up rows) but measure slower past a point: a slot is not a processor --
+        // the CTAs resident on one SM share its issue rate, so a schedule of few long
+        // CTAs leaves a long tail (round 2, march_kernel: Hr 252, 501 CTAs 0.630
+        // ms/pass, 64 0.614; regk_kernel at 3 CTAs/SM, graph path, C3: Hg 16 with
+        // Hr 48 / 64 / 96 29.1 / 29.6 / 29.8 G FVU/s, profiles/r02_v10_seg_grid.txt)
         // (from 4 rows: the paper's 4032 x 200 mesh cannot fill 148 SMs x 4 CTAs with
         // longer segments -- 6-row segments measured 0.63 ms/step, 8-row ones 0.72)
-        for (int h = std::min(ny, 4); h <= std::min(ny, 64); h += 2) hr_c.push_back(h);
+        for (int h = std::min(ny, 4); h <= std::min(ny, 96); h += 2) hr_c.push_back(h);
         if (hr_c.empty()) hr_c.push_back(std::max(1, ny));
     }
+    // the longest regular CTAs (then general ones) whose makespan is within 4 % of the best: the model
+    // ignores that CTAs sharing an SM share its issue rate, and longer regular CTAs
+    // (fewer warm-up rows and prologues) measured faster at equal model makespan
+    // (C3: Hr 74 vs 94 at Hg 16, 28.9 vs 29.8 G FVU/s; 4032 x 200: Hr 10 vs 20 at
+    // Hg 6, 15.2 vs 15.5 G FVU/s)
+    std::vector<std::array<double, 3>> scored;
     for (int hg : hg_c)
         for (int hr : hr_c) {
             cur.clear();
             for (int st = 0; st < strips; st++) cut(st, hg, hr, cur);
             const double ms = makespan(cur);
-            if (ms < best_ms * (1.0 - 1e-3)) { best_ms = ms; best = cur; best_hg = hg; best_hr = hr; }
+            scored.push_back({ms, (double)hg, (double)hr});
+            best_ms = std::min(best_ms, ms);
         }
+    {
+        double pick_ms = 1e300;
+        best_hr = 0;
+        best_hg = 0;
+        for (auto& q : scored) {
+            if (q[0] > best_ms * 1.04) continue;
+            if (q[2] > best_hr || (q[2] == best_hr && q[1] > best_hg)) { best_hr = (int)q[2]; best_hg = (int)q[1]; pick_ms = q[0]; }
+        }
+        cur.clear();
+        for (int st = 0; st < strips; st++) cut(st, best_hg, best_hr, cur);
+        best_ms = makespan(cur);
+        best = cur;
+    }
     c->march_seg = best_hr;
     c->march_nstrips = strips;
     // launch order: general CTAs (longest first), then the all-regular ones

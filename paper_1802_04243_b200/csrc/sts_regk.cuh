@@ -101,6 +101,11 @@ __global__ void __launch_bounds__(MX, STS_REGK_CTAS) regk_kernel(MarchParams m)
     int oj = js * k.pitch + col;
     const double dt = k.dt, dx = k.dx, dy = k.dy, dV = m.dV;
 
+#if defined(STS_REGK_UNROLL) && STS_REGK_UNROLL == 2
+#pragma unroll 2
+#elif defined(STS_REGK_UNROLL) && STS_REGK_UNROLL == 3
+#pragma unroll 3
+#endif
     for (int j = js; j < J1; j++) {
         RingRow& Rm = *pm;
         RingRow& R0 = *p0;

@@ -6,6 +6,7 @@ import subprocess
 import sys
 
 lib, name = sys.argv[1], sys.argv[2]
+FULL = len(sys.argv) > 3
 sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
 body, on = [], False
 for l in sass.splitlines():
@@ -29,6 +30,6 @@ for a, ins in body:
         if ins.startswith('@'):
             ins = ins.split(None, 1)[1]
         op = ins.split()[0]
-        ops[op if op.startswith(('LDS', 'STS')) else op.split('.')[0]] += 1
+        ops[op if (FULL or op.startswith(("LDS", "STS"))) else op.split(".")[0]] += 1
 print(hex(best[0]), hex(best[1]), "total", sum(ops.values()))
 print(" ".join(f"{k}:{v}" for k, v in ops.most_common(40)))
