@@ -390,6 +390,26 @@ static bool old_regk(int impl, int tvd)
     if (v != nullptr && *v) return atoi(v) != 0;
     return impl && tvd;
 }
+// one launch per pass (march_fused_kernel, sts_regk.cuh) for the general + all-regular
+// CTAs of a uniform-mesh pass without plane fusion or loop 3; STS_NO_FUSED=1: the two
+// kernels as two launches / parallel graph nodes (A/B)
+static bool use_fused(const sts_ctx* c, bool fusec, bool l3)
+{
+    const char* v = getenv("STS_NO_FUSED");
+    // implicit TVD: the two-kernel launch (the general kernel at 4 CTAs/SM beside
+    // march_kernel<REGK>) measured faster than one launch at 3 CTAs/SM (22.0 vs 20.6 G FVU/s)
+    const bool itvd = c->sch.time == STS_IMPLICIT && c->sch.space == STS_TVD_VANLEER;
+    return !fusec && !l3 && !c->nu && !itvd && !(v != nullptr && atoi(v) != 0) && !old_regk(0, 0);
+}
+static march_fn fused_table(int impl, int tvd, int graph)
+{
+    if (graph) {
+        if (impl) return tvd ? march_fused_kernel<true, true, true> : march_fused_kernel<true, false, true>;
+        return tvd ? march_fused_kernel<false, true, true> : march_fused_kernel<false, false, true>;
+    }
+    if (impl) return tvd ? march_fused_kernel<true, true, false> : march_fused_kernel<true, false, false>;
+    return tvd ? march_fused_kernel<false, true, false> : march_fused_kernel<false, false, false>;
+}
 static march_fn march_table(int impl, int tvd, int regk, int nu = 0, int l3 = 0)
 {
     if (l3) {                                    // loop-3 sweeps k >= 2 (N3)
@@ -469,6 +489,9 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
                                march_kernel<true, false, true, true>, march_kernel<true, true, true, true>};
         for (march_fn f : rk)
             CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));
+        for (int q = 0; q < 8; q++)
+            CU(cudaFuncSetAttribute((const void*)fused_table(q & 1, (q >> 1) & 1, q >> 2),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));
     }
     for (int q = 0; q < 8; q++) {
         const int impl = q & 1, tvd = (q >> 1) & 1, nu = q >> 2;
@@ -731,6 +754,12 @@ static int launch_march(sts_ctx* c, const MarchParams& m, bool graph, cudaStream
     march_fn reg = fusec ? march_fusec_table(tvd, 1, graph)
                  : l3 ? march_table(impl, tvd, 1, 0, 1) : graph ? march_graph_table(impl, tvd, 1) : march_table(impl, tvd, 1);
     const size_t sm = fusec ? FUSEC_SMEM : march_smem(c);
+    if (use_fused(c, fusec, l3) && n_gen + n_reg > 0) {
+        MarchParams mf = m;
+        mf.order = (const int4*)order;
+        fused_table(impl, tvd, graph)<<<n_gen + n_reg, MX, sm, st>>>(mf);
+        return 1;
+    }
     MarchParams mg = m, mr = m;
     mg.order = (const int4*)order;
     mr.order = (const int4*)order + n_gen;
@@ -1819,6 +1848,21 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
         std::vector<cudaGraphNode_t> deps(dp, dp + n);
         cudaGraphNode_t nodes[2];
         int nn = 0;
+        if (use_fused(c, fz, false) && c->n_gen + c->n_reg > 0) {     // one node: general CTAs first
+            MarchParams mp = m;
+            mp.order = (const int4*)c->cta_order;
+            void* args[] = {&mp};
+            cudaKernelNodeParams kp = {};
+            kp.func = (void*)fused_table(impl, tvd, 1);
+            kp.gridDim = dim3(c->n_gen + c->n_reg);
+            kp.blockDim = dim3(MX);
+            kp.sharedMemBytes = march_smem(c);
+            kp.kernelParams = args;
+            e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
+            if (e != cudaSuccess) return e;
+            nn++;
+            return cudaStreamUpdateCaptureDependencies(s, nodes, nn, cudaStreamSetCaptureDependencies);
+        }
         for (int part = 0; part < 2; part++) {
             const int cnt = part == 0 ? c->n_gen : c->n_reg;
             if (cnt == 0) continue;
@@ -1970,7 +2014,21 @@ static sts_status build_fix_graph(sts_ctx* ctx, int n1)
         std::vector<cudaGraphNode_t> deps(dp, dp + nd);
         cudaGraphNode_t nodes[2];
         int nn = 0;
-        for (int part = 0; part < 2 && e == cudaSuccess; part++) {
+        const bool one = use_fused(c, fz, false) && c->n_gen + c->n_reg > 0;
+        if (one) {                                        // one node: general CTAs first
+            MarchParams mp = m;
+            mp.order = (const int4*)c->cta_order;
+            void* args[] = {&mp};
+            cudaKernelNodeParams kp = {};
+            kp.func = (void*)fused_table(impl, tvd, 0);
+            kp.gridDim = dim3(c->n_gen + c->n_reg);
+            kp.blockDim = dim3(MX);
+            kp.sharedMemBytes = march_smem(c);
+            kp.kernelParams = args;
+            e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
+            nn++;
+        }
+        for (int part = 0; part < 2 && e == cudaSuccess && !one; part++) {
             const int cnt = part == 0 ? c->n_gen : c->n_reg;
             if (cnt == 0) continue;
             MarchParams mp = m;

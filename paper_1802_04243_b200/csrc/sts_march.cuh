@@ -1126,7 +1126,7 @@ __device__ __forceinline__ void stage_E(MarchSmem& s, const MarchParams& m, int 
 #endif
 template <bool IMPL, bool TVD, bool GRAPH = false, bool REGK = false, bool NU = false, bool L3 = false,
           bool HALO = false, bool FUSEC = false>
-__global__ void __launch_bounds__(MX, REGK ? MARCH_CTAS : STS_GEN_CTAS) march_kernel(MarchParams m)
+__device__ __forceinline__ void march_body(const MarchParams m)
 {
     static_assert(!(FUSEC && (IMPL || NU || L3 || HALO)), "plane fusion: explicit, uniform, single-rank passes");
     static_assert(!(HALO && (REGK || GRAPH || L3)), "fused halo stores: edge strips of the stream path only");
@@ -1251,6 +1251,12 @@ __global__ void __launch_bounds__(MX, REGK ? MARCH_CTAS : STS_GEN_CTAS) march_ke
         const long long flat = rs.bad >= 0 ? rs.bad : BAD_NOCELL;
         atomicMax(m.bad, bad_key(m.pass_key, flat, rs.bad >= 0 ? rs.badf : 0));
     }
+}
+template <bool IMPL, bool TVD, bool GRAPH = false, bool REGK = false, bool NU = false, bool L3 = false,
+          bool HALO = false, bool FUSEC = false>
+__global__ void __launch_bounds__(MX, REGK ? MARCH_CTAS : STS_GEN_CTAS) march_kernel(MarchParams m)
+{
+    march_body<IMPL, TVD, GRAPH, REGK, NU, L3, HALO, FUSEC>(m);
 }
 
 }  // namespace sts

@@ -32,7 +32,7 @@ namespace sts {
 #endif
 
 template <bool IMPL, bool TVD, bool GRAPH>
-__global__ void __launch_bounds__(MX, STS_REGK_CTAS) regk_kernel(MarchParams m)
+__device__ __forceinline__ void regk_body(const MarchParams m)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MarchSmem& s = *reinterpret_cast<MarchSmem*>(smem_raw);
@@ -398,6 +398,29 @@ __global__ void __launch_bounds__(MX, STS_REGK_CTAS) regk_kernel(MarchParams m)
     if (rs.bad >= 0 || rs.nanv) {
         const long long flat = rs.bad >= 0 ? rs.bad : BAD_NOCELL;
         atomicMax(m.bad, bad_key(m.pass_key, flat, rs.bad >= 0 ? rs.badf : 0));
+    }
+}
+template <bool IMPL, bool TVD, bool GRAPH>
+__global__ void __launch_bounds__(MX, STS_REGK_CTAS) regk_kernel(MarchParams m)
+{
+    regk_body<IMPL, TVD, GRAPH>(m);
+}
+
+// One launch per loop-2 pass: the CTA schedule (order[], general CTAs first) runs
+// the general CTAs through march_body and the all-regular ones through regk_body
+// (implicit TVD: march_body<REGK>), so the general CTAs are dispatched first
+// inside a graph too (two parallel kernel nodes left their order to the hardware:
+// the general CTAs could queue behind the regular grid and form the pass's tail),
+// and the general code runs with the all-regular kernel's register budget (no
+// spills).  Same instance code per CTA as the two-kernel launch: same bits.
+template <bool IMPL, bool TVD, bool GRAPH>
+__global__ void __launch_bounds__(MX, STS_REGK_CTAS) march_fused_kernel(MarchParams m)
+{
+    if (m.order[blockIdx.x].w & ALLREG_BIT) {
+        if (IMPL && TVD) march_body<IMPL, TVD, GRAPH, true>(m);
+        else regk_body<IMPL, TVD, GRAPH>(m);
+    } else {
+        march_body<IMPL, TVD, GRAPH, false>(m);
     }
 }
 

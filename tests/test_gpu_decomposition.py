@@ -278,15 +278,17 @@ def test_general_instance_same_bits(S, variant):
 
 @pytest.mark.parametrize("variant", list(W.VARIANTS))
 def test_regk_same_bits(S, variant):
-    """The all-regular CTAs run regk_kernel (sts_regk.cuh: the regular stage
-    instances restated with register-resident operands); the round-2 kernel
-    (march_kernel<..., REGK>, STS_OLD_REGK=1) and every CTA through the general
-    kernel (STS_NO_ALLREG) must give the same bits, on the stream path and in the
-    fixed-pass step graphs."""
+    """The all-regular CTAs run regk_body (sts_regk.cuh: the regular stage
+    instances restated with register-resident operands) inside the one-launch
+    march_fused_kernel; the two-kernel launch with regk_kernel for every variant
+    (STS_NO_FUSED, STS_OLD_REGK=0), the round-2 kernel (march_kernel<..., REGK>,
+    STS_OLD_REGK=1) and every CTA through the general kernel (STS_NO_ALLREG)
+    must give the same bits (fixed-pass step graphs)."""
     case = W.channel(520, 96, spacing=0.25, variant=variant, passes=4, squares=[(200, 40, 10, 10)])
     out = []
-    for env in ({"STS_SEG": "16", "STS_OLD_REGK": "0"}, {"STS_SEG": "16", "STS_OLD_REGK": "1"}, {"STS_SEG": "16", "STS_NO_ALLREG": "1"}):
-        keys = ("STS_SEG", "STS_NO_ALLREG", "STS_OLD_REGK")
+    for env in ({"STS_SEG": "16"}, {"STS_SEG": "16", "STS_OLD_REGK": "0", "STS_NO_FUSED": "1"},
+                {"STS_SEG": "16", "STS_OLD_REGK": "1"}, {"STS_SEG": "16", "STS_NO_ALLREG": "1"}):
+        keys = ("STS_SEG", "STS_NO_ALLREG", "STS_OLD_REGK", "STS_NO_FUSED")
         old = {k: os.environ.get(k) for k in keys}
         for k in keys:
             os.environ.pop(k, None)
@@ -306,5 +308,5 @@ def test_regk_same_bits(S, variant):
                     os.environ[k] = v
         out.append({f: g.get_field(f) for f in FIELDS})
     for f in FIELDS:
-        assert np.array_equal(out[0][f], out[1][f]), (f, np.abs(out[0][f] - out[1][f]).max())
-        assert np.array_equal(out[0][f], out[2][f]), (f, np.abs(out[0][f] - out[2][f]).max())
+        for q in range(1, len(out)):
+            assert np.array_equal(out[0][f], out[q][f]), (q, f, np.abs(out[0][f] - out[q][f]).max())
