@@ -10,6 +10,7 @@
 #include "sts_common.cuh"
 #include "sts_march.cuh"
 #include "sts_regk.cuh"
+#include "sts_regk2.cuh"
 #include "sts_conv.cuh"
 
 #include <cuda.h>
@@ -384,6 +385,13 @@ static march_fn march_halo_table(int impl, int tvd, int nu)
 // except implicit TVD (168 registers, 3 CTAs/SM and spills: 0.81 vs 0.74 ms/pass on
 // C3, profiles/r02_summary.md); STS_OLD_REGK=1 selects march_kernel<..., REGK = true>
 // for every variant, STS_OLD_REGK=0 regk_kernel for every variant (A/B, bitwise tests)
+// two rows per row step for the all-regular CTAs (regk2_kernel, sts_regk2.cuh): STS_REGK2=1
+static bool use_regk2(int impl, int tvd)
+{
+    (void)impl; (void)tvd;
+    const char* v = getenv("STS_REGK2");
+    return v != nullptr && atoi(v) != 0;
+}
 static bool old_regk(int impl, int tvd)
 {
     const char* v = getenv("STS_OLD_REGK");
@@ -399,7 +407,7 @@ static bool use_fused(const sts_ctx* c, bool fusec, bool l3)
     // implicit TVD: the two-kernel launch (the general kernel at 4 CTAs/SM beside
     // march_kernel<REGK>) measured faster than one launch at 3 CTAs/SM (22.0 vs 20.6 G FVU/s)
     const bool itvd = c->sch.time == STS_IMPLICIT && c->sch.space == STS_TVD_VANLEER;
-    return !fusec && !l3 && !c->nu && !itvd && !(v != nullptr && atoi(v) != 0) && !old_regk(0, 0);
+    return !fusec && !l3 && !c->nu && !itvd && !(v != nullptr && atoi(v) != 0) && !old_regk(0, 0) && !use_regk2(0, 0);
 }
 static march_fn fused_table(int impl, int tvd, int graph)
 {
@@ -425,6 +433,10 @@ static march_fn march_table(int impl, int tvd, int regk, int nu = 0, int l3 = 0)
         return tvd ? march_kernel<false, true, false, false, true> : march_kernel<false, false, false, false, true>;
     }
     if (regk) {
+        if (use_regk2(impl, tvd)) {
+            if (impl) return tvd ? regk2_kernel<true, true, false> : regk2_kernel<true, false, false>;
+            return tvd ? regk2_kernel<false, true, false> : regk2_kernel<false, false, false>;
+        }
         if (!old_regk(impl, tvd)) {
             if (impl) return tvd ? regk_kernel<true, true, false> : regk_kernel<true, false, false>;
             return tvd ? regk_kernel<false, true, false> : regk_kernel<false, false, false>;
@@ -442,6 +454,10 @@ static march_fn march_graph_table(int impl, int tvd, int regk, int nu = 0)
         return tvd ? march_kernel<false, true, true, false, true> : march_kernel<false, false, true, false, true>;
     }
     if (regk) {
+        if (use_regk2(impl, tvd)) {
+            if (impl) return tvd ? regk2_kernel<true, true, true> : regk2_kernel<true, false, true>;
+            return tvd ? regk2_kernel<false, true, true> : regk2_kernel<false, false, true>;
+        }
         if (!old_regk(impl, tvd)) {
             if (impl) return tvd ? regk_kernel<true, true, true> : regk_kernel<true, false, true>;
             return tvd ? regk_kernel<false, true, true> : regk_kernel<false, false, true>;
@@ -460,6 +476,14 @@ static march_fn conv_march_table(int tvd, int nu = 0)
 // dynamic shared memory of the march / conv kernels: the NU instances keep the
 // column widths of their ring columns behind the struct
 static size_t march_smem(const sts_ctx* c) { return sizeof(MarchSmem) + (c->nu ? RW * sizeof(double) : 0); }
+static bool use_regk2(int impl, int tvd);
+// dynamic shared memory of the all-regular kernel of a (non-fused, non-loop-3) pass
+static size_t regk_smem(const sts_ctx* c, bool fusec, bool l3)
+{
+    const bool impl = c->sch.time == STS_IMPLICIT, tvd = c->sch.space == STS_TVD_VANLEER;
+    if (fusec) return sizeof(MarchSmem) + 3 * RW * sizeof(double);
+    return (!l3 && !c->nu && use_regk2(impl, tvd)) ? sizeof(Regk2Smem) : march_smem(c);
+}
 static size_t conv_smem(const sts_ctx* c) { return sizeof(ConvSmem) + (c->nu ? RW * sizeof(double) : 0); }
 
 // The shared-memory opt-in is a per-device function attribute: one bit per
@@ -489,6 +513,12 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
                                march_kernel<true, false, true, true>, march_kernel<true, true, true, true>};
         for (march_fn f : rk)
             CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));
+        const march_fn rk2[] = {regk2_kernel<false, false, false>, regk2_kernel<false, true, false>,
+                                regk2_kernel<true, false, false>, regk2_kernel<true, true, false>,
+                                regk2_kernel<false, false, true>, regk2_kernel<false, true, true>,
+                                regk2_kernel<true, false, true>, regk2_kernel<true, true, true>};
+        for (march_fn f : rk2)
+            CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Regk2Smem)));
         for (int q = 0; q < 8; q++)
             CU(cudaFuncSetAttribute((const void*)fused_table(q & 1, (q >> 1) & 1, q >> 2),
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));
@@ -570,7 +600,7 @@ static void choose_segments(sts_ctx* c, const std::vector<uint32_t>& packed)
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
     int nb = 0;
     const void* fn = (const void*)march_table(c->sch.time == STS_IMPLICIT, c->sch.space == STS_TVD_VANLEER, !c->nu, c->nu);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, MX, march_smem(c)) == cudaSuccess && nb > 0)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, MX, regk_smem(c, false, false)) == cudaSuccess && nb > 0)
         per_sm = nb;
     const int strips = (c->nloc + MW - 1) / MW;
     const int slots = dev_sms * per_sm;
@@ -768,12 +798,12 @@ static int launch_march(sts_ctx* c, const MarchParams& m, bool graph, cudaStream
         cudaStreamWaitEvent(c->gstream, c->ev_fork, 0);
         gen<<<n_gen, MX, sm, c->gstream>>>(mg);
         cudaEventRecord(c->ev_join, c->gstream);
-        reg<<<n_reg, MX, sm, st>>>(mr);
+        reg<<<n_reg, MX, regk_smem(c, fusec, l3), st>>>(mr);
         cudaStreamWaitEvent(st, c->ev_join, 0);
         return 2;
     }
     if (n_gen > 0) gen<<<n_gen, MX, sm, st>>>(mg);
-    else if (n_reg > 0) reg<<<n_reg, MX, sm, st>>>(mr);
+    else if (n_reg > 0) reg<<<n_reg, MX, regk_smem(c, fusec, l3), st>>>(mr);
     return (n_gen > 0 || n_reg > 0) ? 1 : 0;
 }
 
@@ -1873,7 +1903,7 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
             kp.func = fz ? (void*)march_fusec_table(tvd, part, 1) : (void*)march_graph_table(impl, tvd, part, part ? 0 : c->nu);
             kp.gridDim = dim3(cnt);
             kp.blockDim = dim3(MX);
-            kp.sharedMemBytes = fz ? FUSEC_SMEM : march_smem(c);
+            kp.sharedMemBytes = part ? regk_smem(c, fz, false) : (fz ? FUSEC_SMEM : march_smem(c));
             kp.kernelParams = args;
             e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
             if (e != cudaSuccess) return e;
@@ -2038,7 +2068,7 @@ static sts_status build_fix_graph(sts_ctx* ctx, int n1)
             kp.func = fz ? (void*)march_fusec_table(tvd, part, 0) : (void*)march_table(impl, tvd, part, part ? 0 : c->nu);
             kp.gridDim = dim3(cnt);
             kp.blockDim = dim3(MX);
-            kp.sharedMemBytes = fz ? FUSEC_SMEM : march_smem(c);
+            kp.sharedMemBytes = part ? regk_smem(c, fz, false) : (fz ? FUSEC_SMEM : march_smem(c));
             kp.kernelParams = args;
             e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
             if (e == cudaSuccess && part == 0) e = graph_node_high_priority(nodes[nn]);
