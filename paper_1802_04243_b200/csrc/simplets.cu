@@ -10,7 +10,6 @@
 #include "sts_common.cuh"
 #include "sts_march.cuh"
 #include "sts_regk.cuh"
-#include "sts_regk2.cuh"
 #include "sts_conv.cuh"
 
 #include <cuda.h>
@@ -385,13 +384,6 @@ static march_fn march_halo_table(int impl, int tvd, int nu)
 // except implicit TVD (168 registers, 3 CTAs/SM and spills: 0.81 vs 0.74 ms/pass on
 // C3, profiles/r02_summary.md); STS_OLD_REGK=1 selects march_kernel<..., REGK = true>
 // for every variant, STS_OLD_REGK=0 regk_kernel for every variant (A/B, bitwise tests)
-// two rows per row step for the all-regular CTAs (regk2_kernel, sts_regk2.cuh): STS_REGK2=1
-static bool use_regk2(int impl, int tvd)
-{
-    (void)impl; (void)tvd;
-    const char* v = getenv("STS_REGK2");
-    return v != nullptr && atoi(v) != 0;
-}
 static bool old_regk(int impl, int tvd)
 {
     const char* v = getenv("STS_OLD_REGK");
@@ -407,7 +399,7 @@ static bool use_fused(const sts_ctx* c, bool fusec, bool l3)
     // implicit TVD: the two-kernel launch (the general kernel at 4 CTAs/SM beside
     // march_kernel<REGK>) measured faster than one launch at 3 CTAs/SM (22.0 vs 20.6 G FVU/s)
     const bool itvd = c->sch.time == STS_IMPLICIT && c->sch.space == STS_TVD_VANLEER;
-    return !fusec && !l3 && !c->nu && !itvd && !(v != nullptr && atoi(v) != 0) && !old_regk(0, 0) && !use_regk2(0, 0);
+    return !fusec && !l3 && !c->nu && !itvd && !(v != nullptr && atoi(v) != 0) && !old_regk(0, 0);
 }
 static march_fn fused_table(int impl, int tvd, int graph)
 {
@@ -433,10 +425,6 @@ static march_fn march_table(int impl, int tvd, int regk, int nu = 0, int l3 = 0)
         return tvd ? march_kernel<false, true, false, false, true> : march_kernel<false, false, false, false, true>;
     }
     if (regk) {
-        if (use_regk2(impl, tvd)) {
-            if (impl) return tvd ? regk2_kernel<true, true, false> : regk2_kernel<true, false, false>;
-            return tvd ? regk2_kernel<false, true, false> : regk2_kernel<false, false, false>;
-        }
         if (!old_regk(impl, tvd)) {
             if (impl) return tvd ? regk_kernel<true, true, false> : regk_kernel<true, false, false>;
             return tvd ? regk_kernel<false, true, false> : regk_kernel<false, false, false>;
@@ -454,10 +442,6 @@ static march_fn march_graph_table(int impl, int tvd, int regk, int nu = 0)
         return tvd ? march_kernel<false, true, true, false, true> : march_kernel<false, false, true, false, true>;
     }
     if (regk) {
-        if (use_regk2(impl, tvd)) {
-            if (impl) return tvd ? regk2_kernel<true, true, true> : regk2_kernel<true, false, true>;
-            return tvd ? regk2_kernel<false, true, true> : regk2_kernel<false, false, true>;
-        }
         if (!old_regk(impl, tvd)) {
             if (impl) return tvd ? regk_kernel<true, true, true> : regk_kernel<true, false, true>;
             return tvd ? regk_kernel<false, true, true> : regk_kernel<false, false, true>;
@@ -476,13 +460,11 @@ static march_fn conv_march_table(int tvd, int nu = 0)
 // dynamic shared memory of the march / conv kernels: the NU instances keep the
 // column widths of their ring columns behind the struct
 static size_t march_smem(const sts_ctx* c) { return sizeof(MarchSmem) + (c->nu ? RW * sizeof(double) : 0); }
-static bool use_regk2(int impl, int tvd);
-// dynamic shared memory of the all-regular kernel of a (non-fused, non-loop-3) pass
+// dynamic shared memory of the all-regular kernel of a pass
 static size_t regk_smem(const sts_ctx* c, bool fusec, bool l3)
 {
-    const bool impl = c->sch.time == STS_IMPLICIT, tvd = c->sch.space == STS_TVD_VANLEER;
-    if (fusec) return sizeof(MarchSmem) + 3 * RW * sizeof(double);
-    return (!l3 && !c->nu && use_regk2(impl, tvd)) ? sizeof(Regk2Smem) : march_smem(c);
+    (void)l3;
+    return fusec ? sizeof(MarchSmem) + 3 * RW * sizeof(double) : march_smem(c);
 }
 static size_t conv_smem(const sts_ctx* c) { return sizeof(ConvSmem) + (c->nu ? RW * sizeof(double) : 0); }
 
@@ -513,12 +495,6 @@ static sts_status set_smem_attrs(sts_ctx* ctx)
                                march_kernel<true, false, true, true>, march_kernel<true, true, true, true>};
         for (march_fn f : rk)
             CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));
-        const march_fn rk2[] = {regk2_kernel<false, false, false>, regk2_kernel<false, true, false>,
-                                regk2_kernel<true, false, false>, regk2_kernel<true, true, false>,
-                                regk2_kernel<false, false, true>, regk2_kernel<false, true, true>,
-                                regk2_kernel<true, false, true>, regk2_kernel<true, true, true>};
-        for (march_fn f : rk2)
-            CU(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Regk2Smem)));
         for (int q = 0; q < 8; q++)
             CU(cudaFuncSetAttribute((const void*)fused_table(q & 1, (q >> 1) & 1, q >> 2),
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MarchSmem)));

@@ -19,5 +19,7 @@ for v in implicit_upwind implicit_tvd explicit_upwind explicit_tvd; do
   c=1; [ $v = implicit_tvd ] && c=2
   ncu --set full --clock-control none --import-source on -k regex:"march_" -s 6 -c $c -o $O/prof_${T}_$v \
       python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --variant $v > $O/ncu_${T}_$v.log 2>&1
+  ncu -i $O/prof_${T}_$v.ncu-rep --page raw --csv > $O/prof_${T}_$v.raw.csv 2>/dev/null
+  [ $v = implicit_upwind ] || rm -f $O/prof_${T}_$v.ncu-rep      # gpurun_out is capped at 64 MiB
 done
 python tools/sweep.py > $O/sweep_$T.jsonl 2>/dev/null
