@@ -1,7 +1,7 @@
 #!/bin/bash
 # compute-sanitizer over the CUDA path on small cases (GPU box): memcheck, racecheck (shared-memory
 # ring / row buffers), initcheck, synccheck.  usage: tools/sanitize.sh > gpurun_out/sanitize.log
-K='test_parity_small_square or test_parity_ragged_tiles or test_parity_periodic or test_slabs_bitwise or test_nonuniform_small_square or test_loop3_small_square or test_peer_group_bitwise'
+K='test_regk_same_bits or test_allreg_loop_bitwise or test_parity_small_square or test_parity_ragged_tiles or test_parity_periodic or test_slabs_bitwise or test_nonuniform_small_square or test_loop3_small_square or test_peer_group_bitwise'
 for tool in memcheck racecheck initcheck synccheck; do
   echo "== $tool"
   timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 \

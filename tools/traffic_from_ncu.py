@@ -20,7 +20,10 @@ def metrics(rep):
     """Per-pass totals over the kernels of one pass in the capture (the general
     and the all-regular march kernel): DRAM bytes and warp instructions summed,
     serialised durations summed, pipe activities duration-weighted."""
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):                     # raw page exported on the GPU box
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h, u = rows[0], rows[1]
 
@@ -49,11 +52,13 @@ def metrics(rep):
 
 def main():
     tag = sys.argv[1]
-    res = {"_source": f"ncu --set full --clock-control none, the march kernels of one pass (general + all-regular, serialised by ncu) after warm-up, C3 4032 x 4000 "
+    res = {"_source": f"ncu --set full --clock-control none, the march kernels of one pass (march_fused_kernel; implicit TVD: the general + all-regular kernels, serialised by ncu) after warm-up, C3 4032 x 4000 "
                       f"(16.128 M FVs); dram__bytes_read.sum + dram__bytes_write.sum per launch ({tag}, "
                       f"profiles/{tag}_summary.md)."}
     for var in ("implicit_upwind", "implicit_tvd", "explicit_upwind", "explicit_tvd"):
         rep = os.path.join(ROOT, "gpurun_out", f"prof_{tag}_{var}.ncu-rep")
+        if not os.path.exists(rep):
+            rep = os.path.join(ROOT, "gpurun_out", f"prof_{tag}_{var}.raw.csv")
         if not os.path.exists(rep):
             continue
         m = metrics(rep)
