@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(MX, 5) conv_march_kernel(MarchParams m)
         constexpr bool ALLREG = false;
 #include "sts_conv_loop.inc"
     }
+    mbar_wait(&s.mbar[slot(J1 + 3)], ((J1 + 4 - js) / RS) & 1);   // the last TMA row lands before exit
     cp_wait_all();
 }
 

@@ -1224,6 +1224,10 @@ __device__ __forceinline__ void march_body(const MarchParams m)
         if (PREF_L) nm_prefetch_init();
 #include "sts_march_loop.inc"
     }
+    {   // the last step's TMA row (J1 + 3) lands before the CTA's shared memory is released
+        const int qo = J1 + 4 - js;
+        mbar_wait(&s.mbar[qo % RS], (qo / RS) & 1);
+    }
     cp_wait_all();
     const double qnan = __longlong_as_double(0x7ff8000000000000LL);
     double vals[7] = {rs.nanv ? qnan : rs.du, rs.nanv ? qnan : rs.dv, rs.dp, rs.dT, rs.vel, rs.p, rs.T};

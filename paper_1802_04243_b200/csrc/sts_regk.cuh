@@ -375,6 +375,10 @@ __device__ __forceinline__ void regk_body(const MarchParams m)
         pm = p0; p0 = pa; pa = pb; pb = pc; pc = pd; pd = pf;
         oj += k.pitch;
     }
+    {   // the last step's TMA row (J1 + 3) lands before the CTA's shared memory is released
+        const int qo = J1 + 4 - js;
+        mbar_wait(&s.mbar[qo % RS], (qo / RS) & 1);
+    }
     cp_wait_all();
     const double qnan = __longlong_as_double(0x7ff8000000000000LL);
     double vals[7] = {rs.nanv ? qnan : rs.du, rs.nanv ? qnan : rs.dv, rs.dp, rs.dT, rs.vel, rs.p, rs.T};
