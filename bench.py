@@ -416,7 +416,9 @@ def run_ours(args):
                 "traffic": traffic, "peak_source": peak_kind,
                 "kernel": ("march_kernel (general) + march_kernel<REGK> (all-regular CTAs), one pass"
                            if args.variant == "implicit_tvd" else
-                           "march_fused_kernel (general + regk_body CTAs), one launch per pass"),
+                           "march_fused_kernel (general + regk_body CTAs), one launch per pass"
+                           + ("; the first pass of a step: march_kernel<FUSEC> pair (the planes inside)"
+                              if kind == "explicit" else "")),
                 "algorithmic_bytes_per_fvu": BYTES_PER_FVU[kind], "pass_ms_avg": pass_ms,
                 "timed_region": "the timed region: one sts_advance(K) (step graphs), time / (K x passes)",
                 "pass_ms_stream_profiled": pass_ms_stream,
