@@ -221,13 +221,23 @@ __device__ __forceinline__ void regk_body(const MarchParams m)
             xvW = FMA(m.B_dydx, gcN, lk);
             s.XVW[lc] = xvW;
         }
+        // ring values of stage C: the rows do not change during the step, so the implicit
+        // variants load the first ones before the barrier and hide their latency behind it
+        // (implicit upwind +1.6 %, explicit upwind -0.4 %: explicit loads them after)
+        double p0W, p0E;
+        if (IMPL) {
+            if (!TVD) { t0W = R0.T[lc - 1]; t0E = R0.T[lc + 1]; u0W = R0.U[lc - 1]; vaW = Ra.V[lc - 1]; vaE = Ra.V[lc + 1]; }
+            p0W = R0.P[lc - 1]; p0E = R0.P[lc + 1];
+        }
         __syncthreads();                                    // B1
 
         // ================= stage C (stage_C, REG) =================
-        if (!TVD) { t0W = R0.T[lc - 1]; t0E = R0.T[lc + 1]; u0W = R0.U[lc - 1]; vaW = Ra.V[lc - 1]; vaE = Ra.V[lc + 1]; }
+        if (!IMPL) {
+            if (!TVD) { t0W = R0.T[lc - 1]; t0E = R0.T[lc + 1]; u0W = R0.U[lc - 1]; vaW = Ra.V[lc - 1]; vaE = Ra.V[lc + 1]; }
+            p0W = R0.P[lc - 1]; p0E = R0.P[lc + 1];
+        }
         const double v0W = R0.V[lc - 1], v0E = R0.V[lc + 1];
         const double uaE = Ra.U[lc + 1], umE = Rm.U[lc + 1];
-        const double p0W = R0.P[lc - 1], p0E = R0.P[lc + 1];
         const double xtwE = s.XTW[lc + 1], fyW = Fn.FY[lc - 1], xuwW = s.XUW[lc - 1], r1W = s.R1[lc - 1];
         const double fxnE = Fn.FX[lc + 1], xvwE = s.XVW[lc + 1];
         double TN;
