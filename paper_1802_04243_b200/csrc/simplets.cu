@@ -1982,6 +1982,29 @@ static bool fix_graph_ok(const sts_ctx* c)
     return c->sch.tol <= 0 && c->world == 1 && !c->comm && !c->peer && !c->profiling && c->sch.loop3 <= 1 &&
            !getenv("STS_NO_GRAPH") && !getenv("STS_GRAPH_KERNEL");
 }
+// A pass's kernel node; with `programmatic` every edge from the previous pass's
+// node(s) is a programmatic (PDL) edge: the node's CTAs may launch once every CTA of
+// the previous pass has started, and each waits in griddepcontrol.wait (first
+// statement of the march kernels) for the previous pass to complete.
+static cudaError_t add_pass_node(cudaGraphNode_t* node, cudaGraph_t g, const std::vector<cudaGraphNode_t>& deps,
+                                 const cudaKernelNodeParams& kp, bool programmatic)
+{
+    if (!programmatic || deps.empty()) return cudaGraphAddKernelNode(node, g, deps.data(), deps.size(), &kp);
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeKernel;
+    np.kernel.func = kp.func;
+    np.kernel.gridDim = kp.gridDim;
+    np.kernel.blockDim = kp.blockDim;
+    np.kernel.sharedMemBytes = kp.sharedMemBytes;
+    np.kernel.kernelParams = kp.kernelParams;
+    std::vector<cudaGraphEdgeData> ed(deps.size());
+    for (cudaGraphEdgeData& x : ed) {
+        x = cudaGraphEdgeData{};
+        x.from_port = cudaGraphKernelNodePortProgrammatic;
+        x.type = cudaGraphDependencyTypeProgrammatic;
+    }
+    return cudaGraphAddNode_v2(node, g, deps.data(), ed.data(), deps.size(), &np);
+}
 static sts_status build_fix_graph(sts_ctx* ctx, int n1)
 {
     sts_ctx* const c = ctx;
@@ -2002,6 +2025,11 @@ static sts_status build_fix_graph(sts_ctx* ctx, int n1)
         e = cudaGetLastError();
     }
     int old = n1, nw = a;
+    // consecutive one-node passes are joined by programmatic edges (PDL): pass k+1's
+    // CTAs launch once every CTA of pass k has started and wait on the device for its
+    // completion (griddepcontrol.wait in march_fused_kernel) -- the launch latency of a
+    // pass hides behind the previous pass's tail.  STS_NO_PDL=1: full edges.
+    const bool pdl = !(getenv("STS_NO_PDL") && atoi(getenv("STS_NO_PDL")) != 0);
     for (int it = 0; it < c->sch.max_passes && e == cudaSuccess; it++) {
         Params q = k;
         q.u_o = c->snap[old].u; q.v_o = c->snap[old].v; q.p_o = c->snap[old].p; q.T_o = c->snap[old].T;
@@ -2031,7 +2059,7 @@ static sts_status build_fix_graph(sts_ctx* ctx, int n1)
             kp.blockDim = dim3(MX);
             kp.sharedMemBytes = march_smem(c);
             kp.kernelParams = args;
-            e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
+            e = add_pass_node(&nodes[nn], g, deps, kp, pdl && it > 0);
             nn++;
         }
         for (int part = 0; part < 2 && e == cudaSuccess && !one; part++) {
@@ -2046,7 +2074,7 @@ static sts_status build_fix_graph(sts_ctx* ctx, int n1)
             kp.blockDim = dim3(MX);
             kp.sharedMemBytes = part ? regk_smem(c, fz, false) : (fz ? FUSEC_SMEM : march_smem(c));
             kp.kernelParams = args;
-            e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
+            e = add_pass_node(&nodes[nn], g, deps, kp, pdl && it > 0);
             if (e == cudaSuccess && part == 0) e = graph_node_high_priority(nodes[nn]);
             nn++;
         }

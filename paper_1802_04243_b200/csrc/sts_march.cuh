@@ -1260,6 +1260,8 @@ template <bool IMPL, bool TVD, bool GRAPH = false, bool REGK = false, bool NU = 
           bool HALO = false, bool FUSEC = false>
 __global__ void __launch_bounds__(MX, REGK ? MARCH_CTAS : STS_GEN_CTAS) march_kernel(MarchParams m)
 {
+    asm volatile("griddepcontrol.wait;" ::: "memory");                 // PDL: see march_fused_kernel
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     march_body<IMPL, TVD, GRAPH, REGK, NU, L3, HALO, FUSEC>(m);
 }
 

@@ -417,6 +417,8 @@ __device__ __forceinline__ void regk_body(const MarchParams m)
 template <bool IMPL, bool TVD, bool GRAPH>
 __global__ void __launch_bounds__(MX, STS_REGK_CTAS) regk_kernel(MarchParams m)
 {
+    asm volatile("griddepcontrol.wait;" ::: "memory");                 // PDL: see march_fused_kernel
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     regk_body<IMPL, TVD, GRAPH>(m);
 }
 
@@ -430,6 +432,13 @@ __global__ void __launch_bounds__(MX, STS_REGK_CTAS) regk_kernel(MarchParams m)
 template <bool IMPL, bool TVD, bool GRAPH>
 __global__ void __launch_bounds__(MX, STS_REGK_CTAS) march_fused_kernel(MarchParams m)
 {
+    // Programmatic dependent launch (fixed-pass step graphs, §5.5): the pass may be
+    // launched while the previous pass drains; every read of its outputs comes after
+    // this wait (which returns once the previous grid has completed and its writes
+    // are visible), and the next pass is released only after it.  No-ops without a
+    // programmatic edge (stream launches).
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (m.order[blockIdx.x].w & ALLREG_BIT) {
         if (IMPL && TVD) march_body<IMPL, TVD, GRAPH, true>(m);
         else regk_body<IMPL, TVD, GRAPH>(m);
