@@ -217,6 +217,33 @@ sts_status sts_get_field(sts_ctx* ctx, int32_t field, double* host, int64_t n);
 /* Same into a DEVICE buffer (async on the context stream). */
 sts_status sts_get_field_device(sts_ctx* ctx, int32_t field, double* dev, int64_t n);
 
+/* Asynchronous host I/O for pipelined time loops (a user's loop 1 of Figs. 1-2,
+ * P:165, with its state kept on the host between steps).  Same shapes, same
+ * arithmetic and the same resulting state as sts_set_field / sts_get_field; only
+ * the copies move to two copy streams of the context (one per direction) so the
+ * host<->device transfers of one step overlap the loop-2 passes of another.
+ *
+ * sts_stage_field: starts the H2D copy of a host buffer of n doubles (global or
+ *   slab shape, as sts_set_field; pinned memory for a truly asynchronous copy)
+ *   into the context's device staging slot of `field` (STS_U..STS_T) and returns.
+ *   The caller keeps ownership and must not modify the buffer until the matching
+ *   sts_set_staged has been made and the context stream has passed it (or
+ *   sts_io_sync returns).  A second stage of the same field waits (on the device)
+ *   until the previous staged copy has been set.
+ * sts_set_staged: the context stream waits for that copy, then sets the field
+ *   from the slot exactly as sts_set_field_device does.  Does not synchronise.
+ *   STS_E_ARG if nothing is staged for the field.
+ * sts_fetch_field: on the context stream, copies this rank's owned part of the
+ *   current state of `field` (STS_U..STS_T) into a device slot, then starts the
+ *   D2H copy of the slot into the host buffer of n doubles (shape as
+ *   sts_get_field) and returns; the host buffer is valid after sts_io_sync.
+ * sts_io_sync: blocks until every started H2D and D2H copy has completed.
+ * Errors as the synchronous calls (STS_E_ARG on sizes, STS_E_CUDA). */
+sts_status sts_stage_field(sts_ctx* ctx, int32_t field, const double* host, int64_t n);
+sts_status sts_set_staged(sts_ctx* ctx, int32_t field);
+sts_status sts_fetch_field(sts_ctx* ctx, int32_t field, double* host, int64_t n);
+sts_status sts_io_sync(sts_ctx* ctx);
+
 /* Integer maps, global shape for a single GPU: which = 0 cell kinds
  * (0 fluid, 1 solid), 1 u-face kinds, 2 v-face kinds (0 active, 1 fixed-0,
  * 2 inlet, 3 outlet, 4 wall), 3 the owned global column range of every rank

@@ -167,6 +167,17 @@ struct sts_ctx {
     std::vector<std::pair<int, int>> ev_used;   // (start idx, kind)
     double prof_pass_n = 0, prof_pass_ms = 0, prof_conv_n = 0, prof_conv_ms = 0, launches = 0;
     std::string err;
+    // asynchronous host I/O (sts_stage_field / sts_set_staged / sts_fetch_field / sts_io_sync):
+    // per field (u, v, p, T) one device staging slot per direction, copy streams for
+    // each direction and the events that order slot reuse against the context stream
+    struct IoSlot {
+        double* d = nullptr;
+        int64_t cap = 0, n = 0;
+        cudaEvent_t copied = nullptr, consumed = nullptr;   // H2D / D2H done; slot read / written on `stream`
+        bool pending = false;                               // staged, not yet set (in) / fetch in flight (out)
+    };
+    IoSlot io_in[4], io_out[4];
+    cudaStream_t io_h2d = nullptr, io_d2h = nullptr;
 };
 
 static sts_status fail(sts_ctx* c, sts_status st, const std::string& msg)
@@ -1261,6 +1272,14 @@ extern "C" void sts_destroy(sts_ctx* ctx)
     for (cudaGraphExec_t& g : ctx->fix_exec) if (g) cudaGraphExecDestroy(g);
     if (ctx->h_badstep) cudaFreeHost(ctx->h_badstep);
     cudaFree(ctx->red2); cudaFree(ctx->d_ls);
+    for (int d = 0; d < 2; d++)
+        for (sts_ctx::IoSlot& q : d ? ctx->io_out : ctx->io_in) {
+            cudaFree(q.d);
+            if (q.copied) cudaEventDestroy(q.copied);
+            if (q.consumed) cudaEventDestroy(q.consumed);
+        }
+    if (ctx->io_h2d) cudaStreamDestroy(ctx->io_h2d);
+    if (ctx->io_d2h) cudaStreamDestroy(ctx->io_d2h);
     if (ctx->h_ls) cudaFreeHost(ctx->h_ls);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : {ctx->ev_a[0], ctx->ev_a[1], ctx->ev_b, ctx->ev_s, ctx->ev_h}) if (e) cudaEventDestroy(e);
@@ -1443,6 +1462,93 @@ extern "C" sts_status sts_get_field(sts_ctx* ctx, int32_t field, double* host, i
 extern "C" sts_status sts_get_field_device(sts_ctx* ctx, int32_t field, double* dev, int64_t n)
 {
     return get_field_any(ctx, field, dev, n);
+}
+
+// ---- asynchronous host I/O: H2D / D2H on their own copy streams, overlapping the
+// pass kernels of the context stream (and each other: the two directions of the
+// host link are independent).  The staging slots are compact device buffers of the
+// caller's shape; set / fetch run the same set_field_any / get_field_any as the
+// synchronous calls, from / into the slot.
+static sts_status io_slot(sts_ctx* ctx, sts_ctx::IoSlot& q, int64_t n)
+{
+    sts_ctx* const c = ctx;
+    if (!c->io_h2d) {
+        CU(cudaStreamCreateWithFlags(&c->io_h2d, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&c->io_d2h, cudaStreamNonBlocking));
+    }
+    if (!q.copied) {
+        CU(cudaEventCreateWithFlags(&q.copied, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&q.consumed, cudaEventDisableTiming));
+    }
+    if (q.cap < n) {
+        if (q.d) { CU(cudaStreamSynchronize(c->stream)); CU(cudaStreamSynchronize(c->io_h2d)); CU(cudaStreamSynchronize(c->io_d2h)); }
+        cudaFree(q.d);
+        q.d = nullptr;
+        q.cap = 0;
+        CU(cudaMalloc(&q.d, (size_t)n * sizeof(double)));
+        q.cap = n;
+    }
+    return STS_OK;
+}
+
+extern "C" sts_status sts_stage_field(sts_ctx* ctx, int32_t field, const double* host, int64_t n)
+{
+    if (!ctx || !host || n <= 0) return fail(ctx, STS_E_ARG, "null argument");
+    if (field < STS_U || field > STS_T) return fail(ctx, STS_E_ARG, "field not settable");
+    CU(cudaSetDevice(ctx->device));
+    sts_ctx::IoSlot& q = ctx->io_in[field];
+    sts_status st = io_slot(ctx, q, n);
+    if (st) return st;
+    CU(cudaStreamWaitEvent(ctx->io_h2d, q.consumed, 0));     // the previous set has read the slot
+    CU(cudaMemcpyAsync(q.d, host, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, ctx->io_h2d));
+    CU(cudaEventRecord(q.copied, ctx->io_h2d));
+    q.n = n;
+    q.pending = true;
+    return STS_OK;
+}
+
+extern "C" sts_status sts_set_staged(sts_ctx* ctx, int32_t field)
+{
+    if (!ctx) return fail(ctx, STS_E_ARG, "null ctx");
+    if (field < STS_U || field > STS_T) return fail(ctx, STS_E_ARG, "field not settable");
+    sts_ctx::IoSlot& q = ctx->io_in[field];
+    if (!q.pending) return fail(ctx, STS_E_ARG, "no staged copy of this field");
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaStreamWaitEvent(ctx->stream, q.copied, 0));
+    sts_status st = set_field_any(ctx, field, q.d, q.n);
+    if (st) return st;
+    CU(cudaEventRecord(q.consumed, ctx->stream));
+    q.pending = false;
+    return STS_OK;
+}
+
+extern "C" sts_status sts_fetch_field(sts_ctx* ctx, int32_t field, double* host, int64_t n)
+{
+    if (!ctx || !host || n <= 0) return fail(ctx, STS_E_ARG, "null argument");
+    if (field < STS_U || field > STS_T) return fail(ctx, STS_E_ARG, "field not fetchable asynchronously");
+    CU(cudaSetDevice(ctx->device));
+    sts_ctx::IoSlot& q = ctx->io_out[field];
+    sts_status st = io_slot(ctx, q, n);
+    if (st) return st;
+    CU(cudaStreamWaitEvent(ctx->stream, q.copied, 0));       // the previous D2H has read the slot
+    st = get_field_any(ctx, field, q.d, n);
+    if (st) return st;
+    CU(cudaEventRecord(q.consumed, ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->io_d2h, q.consumed, 0));
+    CU(cudaMemcpyAsync(host, q.d, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->io_d2h));
+    CU(cudaEventRecord(q.copied, ctx->io_d2h));
+    q.pending = true;
+    return STS_OK;
+}
+
+extern "C" sts_status sts_io_sync(sts_ctx* ctx)
+{
+    if (!ctx) return fail(ctx, STS_E_ARG, "null ctx");
+    CU(cudaSetDevice(ctx->device));
+    if (ctx->io_h2d) CU(cudaStreamSynchronize(ctx->io_h2d));
+    if (ctx->io_d2h) CU(cudaStreamSynchronize(ctx->io_d2h));
+    for (sts_ctx::IoSlot& q : ctx->io_out) q.pending = false;
+    return STS_OK;
 }
 
 extern "C" sts_status sts_get_map(sts_ctx* ctx, int32_t which, int32_t* host, int64_t n)

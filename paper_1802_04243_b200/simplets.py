@@ -28,7 +28,8 @@ FIELDS = {"u": 0, "v": 1, "p": 2, "T": 3, "rho": 4, "uexp": 6, "vexp": 7, "Texp"
 EXPORTS = ["sts_create", "sts_destroy", "sts_last_error", "sts_set_stream", "sts_init_freestream",
            "sts_set_field", "sts_set_field_device", "sts_advance", "sts_advance_group", "sts_get_field", "sts_get_field_device",
            "sts_get_map", "sts_shape", "sts_constants", "sts_profile", "sts_profile_read", "sts_nccl_unique_id",
-           "sts_plan", "sts_set_mesh", "sts_peer_export", "sts_peer_connect", "sts_peer_connect_group"]
+           "sts_plan", "sts_set_mesh", "sts_peer_export", "sts_peer_connect", "sts_peer_connect_group",
+           "sts_stage_field", "sts_set_staged", "sts_fetch_field", "sts_io_sync"]
 
 
 class StsError(RuntimeError):
@@ -107,6 +108,13 @@ def lib():
         for f in ("sts_set_field_device", "sts_get_field_device"):
             getattr(L, f).restype = st
             getattr(L, f).argtypes = [vp, ctypes.c_int32, vp, ctypes.c_int64]
+        for f in ("sts_stage_field", "sts_fetch_field"):
+            getattr(L, f).restype = st
+            getattr(L, f).argtypes = [vp, ctypes.c_int32, vp, ctypes.c_int64]
+        L.sts_set_staged.restype = st
+        L.sts_set_staged.argtypes = [vp, ctypes.c_int32]
+        L.sts_io_sync.restype = st
+        L.sts_io_sync.argtypes = [vp]
         L.sts_advance.restype = st
         L.sts_advance.argtypes = [vp, ctypes.c_int32, ctypes.POINTER(sts_stats)]
         L.sts_advance_group.restype = st
@@ -297,6 +305,20 @@ class Solver:
 
     def get_field_device(self, name, dev_ptr: int, n: int):
         _check(lib().sts_get_field_device(self._h, FIELDS[name], ctypes.c_void_p(dev_ptr), n), self._h)
+
+    # asynchronous host I/O (include/simplets.h): host_ptr is the address of a
+    # (pinned) host buffer of n doubles that the caller keeps alive
+    def stage_field(self, name, host_ptr: int, n: int):
+        _check(lib().sts_stage_field(self._h, FIELDS[name], ctypes.c_void_p(host_ptr), n), self._h)
+
+    def set_staged(self, name):
+        _check(lib().sts_set_staged(self._h, FIELDS[name]), self._h)
+
+    def fetch_field(self, name, host_ptr: int, n: int):
+        _check(lib().sts_fetch_field(self._h, FIELDS[name], ctypes.c_void_p(host_ptr), n), self._h)
+
+    def io_sync(self):
+        _check(lib().sts_io_sync(self._h), self._h)
 
     def get_map(self, which):
         if which == 3:
