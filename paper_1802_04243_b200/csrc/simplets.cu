@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <array>
@@ -28,6 +29,16 @@
 #include <mutex>
 #include <queue>
 #include <vector>
+
+// NVTX ranges (header-only NVTX3: a no-op unless a tool such as nsys / ncu with
+// --nvtx is attached) around the ABI calls, every time step and every halo phase,
+// so a trace shows loop 1, the state transfers and the comm / compute overlap.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 using namespace sts;
 
@@ -885,6 +896,7 @@ static Snapshot pick(sts_ctx* c, int which)
 }
 static sts_status exchange_group(sts_ctx** cs, int n, const int* which, cudaStream_t st)
 {
+    NvtxRange nv("halo_exchange");
     if ((cs[0]->world == 1 && !cs[0]->comm) || cs[0]->peer) return STS_OK;   // peers: stored in the epilogues
     for (int r = 0; r < n; r++) { sts_status e = halo_pack(cs[r], pick(cs[r], which[r]), st); if (e) return e; }
     if (n == 1) {
@@ -991,6 +1003,7 @@ static sts_status peer_fence(sts_ctx* c)
 // wait until both neighbours have pushed theirs into mine.
 static sts_status peer_exchange(sts_ctx* ctx, int which, cudaStream_t st)
 {
+    NvtxRange nv("halo_peer");
     sts_ctx* const c = ctx;
     const unsigned long long q = ++c->seq;
     sts_status e = peer_wait(c, q - 1, st);
@@ -1323,6 +1336,7 @@ static void owned_shape(const sts_ctx* c, int field, int* rows, int* ncols)
 // context ends with one halo exchange (every rank calls it, collectively).
 static sts_status set_field_any(sts_ctx* ctx, int field, const double* src, int64_t n)
 {
+    NvtxRange nv("sts_set_field");
     if (!ctx || !src) return fail(ctx, STS_E_ARG, "null argument");
     if (field < STS_U || field > STS_T) return fail(ctx, STS_E_ARG, "field not settable");
     CU(cudaSetDevice(ctx->device));
@@ -1423,6 +1437,7 @@ extern "C" sts_status sts_init_freestream(sts_ctx* ctx)
 // device, compact rows x ncols), asynchronously on the context stream.
 static sts_status get_field_any(sts_ctx* ctx, int field, double* dst, int64_t n)
 {
+    NvtxRange nv("sts_get_field");
     if (!ctx || !dst) return fail(ctx, STS_E_ARG, "null argument");
     CU(cudaSetDevice(ctx->device));
     int rows, ncols;
@@ -1493,6 +1508,7 @@ static sts_status io_slot(sts_ctx* ctx, sts_ctx::IoSlot& q, int64_t n)
 
 extern "C" sts_status sts_stage_field(sts_ctx* ctx, int32_t field, const double* host, int64_t n)
 {
+    NvtxRange nv("sts_stage_field");
     if (!ctx || !host || n <= 0) return fail(ctx, STS_E_ARG, "null argument");
     if (field < STS_U || field > STS_T) return fail(ctx, STS_E_ARG, "field not settable");
     CU(cudaSetDevice(ctx->device));
@@ -1524,6 +1540,7 @@ extern "C" sts_status sts_set_staged(sts_ctx* ctx, int32_t field)
 
 extern "C" sts_status sts_fetch_field(sts_ctx* ctx, int32_t field, double* host, int64_t n)
 {
+    NvtxRange nv("sts_fetch_field");
     if (!ctx || !host || n <= 0) return fail(ctx, STS_E_ARG, "null argument");
     if (field < STS_U || field > STS_T) return fail(ctx, STS_E_ARG, "field not fetchable asynchronously");
     CU(cudaSetDevice(ctx->device));
@@ -1543,6 +1560,7 @@ extern "C" sts_status sts_fetch_field(sts_ctx* ctx, int32_t field, double* host,
 
 extern "C" sts_status sts_io_sync(sts_ctx* ctx)
 {
+    NvtxRange nv("sts_io_sync");
     if (!ctx) return fail(ctx, STS_E_ARG, "null ctx");
     CU(cudaSetDevice(ctx->device));
     if (ctx->io_h2d) CU(cudaStreamSynchronize(ctx->io_h2d));
@@ -2212,6 +2230,7 @@ static sts_status fix_graph_advance(sts_ctx* ctx, int32_t n_steps, sts_stats* ou
     const long long pass0 = c->stats.passes_done;
     const int P = c->sch.max_passes;
     for (int s = 0; s < n_steps; s++) {
+        NvtxRange nv_step("time step");
         const int n1 = c->cur;
         CU(cudaGraphLaunch(c->fix_exec[n1], c->stream));
         CU(cudaMemcpyAsync(c->h_badstep + s, c->bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
@@ -2265,6 +2284,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
     if (n == 1 && fix_graph_ok(ctx)) return fix_graph_advance(ctx, n_steps, out);
     if (n == 1 && tol_graph_ok(ctx)) {
         for (int step = 0; step < n_steps; step++) {
+            NvtxRange nv_step("time step");
             bool conv = false;
             sts_status e = graph_step(ctx, &conv);
             if (e) { if (out) *out = ctx->stats; return e; }
@@ -2275,6 +2295,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
         return STS_OK;
     }
     for (int step = 0; step < n_steps; step++) {
+        NvtxRange nv_step("time step");
         for (int r = 0; r < n; r++) {
             sts_ctx* c = cs[r];
             // a0: n-1 := current state; old := n-1; ping-pong between the other two
@@ -2474,6 +2495,7 @@ static sts_status drive(sts_ctx** cs, int n, int32_t n_steps, sts_stats* out)
 
 extern "C" sts_status sts_advance(sts_ctx* ctx, int32_t n_steps, sts_stats* out)
 {
+    NvtxRange nv("sts_advance");
     if (!ctx || n_steps < 0) return fail(ctx, STS_E_ARG, "bad argument");
     if (ctx->local_group) return fail(ctx, STS_E_ARG, "in-process slab contexts advance with sts_advance_group");
     return drive(&ctx, 1, n_steps, out);
@@ -2481,6 +2503,7 @@ extern "C" sts_status sts_advance(sts_ctx* ctx, int32_t n_steps, sts_stats* out)
 
 extern "C" sts_status sts_advance_group(sts_ctx** ctxs, int32_t n, int32_t n_steps, sts_stats* out)
 {
+    NvtxRange nv("sts_advance_group");
     sts_ctx* ctx = nullptr;
     if (!ctxs || n < 1 || n_steps < 0) return fail(ctx, STS_E_ARG, "bad argument");
     for (int r = 0; r < n; r++) {
