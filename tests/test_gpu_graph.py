@@ -126,6 +126,29 @@ def test_fixed_pass_graph_matches_stream(S, variant):
     _same(a, b)
 
 
+@pytest.mark.parametrize("variant", ["implicit_upwind", "implicit_tvd", "explicit_tvd"])
+def test_pdl_edges_same_bits(S, variant):
+    """The programmatic (PDL) edges between the passes of a step graph (DESIGN 5.5)
+    change only when a pass's CTAs are launched, never what they read: graph with
+    PDL, graph with full edges (STS_NO_PDL=1) and stream launches agree bit for bit
+    on the paper's 4032 x 400 mesh (hundreds of CTAs per pass, several per SM, so a
+    pass that read its predecessor's output early would differ)."""
+    case = W.c3(20, variant, passes=3)
+    out = []
+    for env in ({}, {"STS_NO_PDL": "1"}):
+        saved = os.environ.pop("STS_NO_PDL", None)
+        os.environ.update(env)
+        try:
+            out.append(_run(S, case, 3, graph=True))
+        finally:
+            os.environ.pop("STS_NO_PDL", None)
+            if saved is not None:
+                os.environ["STS_NO_PDL"] = saved
+    out.append(_run(S, case, 3, graph=False))
+    _same(out[0], out[1])
+    _same(out[0], out[2])
+
+
 def test_fixed_pass_graph_bad_state_step(S):
     """A bad state in step 3 of a 4-step call made of graph launches: reported with
     its cumulative pass index (2 steps x 2 passes + its pass within step 3)."""
