@@ -420,7 +420,7 @@ static bool use_fused(const sts_ctx* c, bool fusec, bool l3)
     const char* v = getenv("STS_NO_FUSED");
     // implicit TVD: the two-kernel launch (the general kernel at 4 CTAs/SM beside
     // march_kernel<REGK>) measured faster than one launch at 3 CTAs/SM (22.0 vs 20.6 G FVU/s)
-    const bool itvd = c->sch.time == STS_IMPLICIT && c->sch.space == STS_TVD_VANLEER;
+    const bool itvd = c->sch.time == STS_IMPLICIT && c->sch.space == STS_TVD_VANLEER && !getenv("STS_ITVD_FUSED");
     return !fusec && !l3 && !c->nu && !itvd && !(v != nullptr && atoi(v) != 0) && !old_regk(0, 0);
 }
 static march_fn fused_table(int impl, int tvd, int graph)

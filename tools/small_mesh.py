@@ -15,7 +15,7 @@ H = int(os.environ.get("H", "10"))
 variant = os.environ.get("V", "implicit_upwind")
 for spec in sys.argv[1:] or ["auto="]:
     name, _, envs = spec.partition("=")
-    for k in ("STS_SEG", "STS_OLD_REGK", "STS_CTA_OVH", "STS_COST", "STS_NO_PDL"):
+    for k in ("STS_SEG", "STS_OLD_REGK", "STS_CTA_OVH", "STS_COST", "STS_NO_PDL", "STS_ITVD_FUSED"):
         os.environ.pop(k, None)
     for kv in filter(None, envs.split(";")):
         k, v = kv.split(":")
