@@ -1900,9 +1900,34 @@ struct LoopState {
     unsigned long long bad;      // sticky bad-state key (the march kernels' MarchParams.bad)
 };
 
+// A pass's kernel node; with `programmatic` every edge from the previous pass's
+// node(s) is a programmatic (PDL) edge: the node's CTAs may launch once every CTA of
+// the previous pass has started, and each waits in griddepcontrol.wait (first
+// statement of the march kernels) for the previous pass to complete.
+static cudaError_t add_pass_node(cudaGraphNode_t* node, cudaGraph_t g, const std::vector<cudaGraphNode_t>& deps,
+                                 const cudaKernelNodeParams& kp, bool programmatic)
+{
+    if (!programmatic || deps.empty()) return cudaGraphAddKernelNode(node, g, deps.data(), deps.size(), &kp);
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeKernel;
+    np.kernel.func = kp.func;
+    np.kernel.gridDim = kp.gridDim;
+    np.kernel.blockDim = kp.blockDim;
+    np.kernel.sharedMemBytes = kp.sharedMemBytes;
+    np.kernel.kernelParams = kp.kernelParams;
+    std::vector<cudaGraphEdgeData> ed(deps.size());
+    for (cudaGraphEdgeData& x : ed) {
+        x = cudaGraphEdgeData{};
+        x.from_port = cudaGraphKernelNodePortProgrammatic;
+        x.type = cudaGraphDependencyTypeProgrammatic;
+    }
+    return cudaGraphAddNode_v2(node, g, deps.data(), ed.data(), deps.size(), &np);
+}
 __global__ void loop_check_kernel(unsigned long long* slot, LoopState* ls, cudaGraphConditionalHandle h,
                                   int min_passes, int max_passes, double tol)
 {
+    asm volatile("griddepcontrol.wait;" ::: "memory");      // PDL (tolerance graphs): after the pass
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x != 0) return;
     if (ls->done) { cudaGraphSetConditional(h, 0); return; }
     const int passes = ls->passes + 1;
@@ -1940,7 +1965,25 @@ static bool tol_graph_ok(const sts_ctx* c)
     if (cap) { cudaGraph_t g_ = nullptr; cudaStreamEndCapture(cap, &g_); if (g_) cudaGraphDestroy(g_); cudaStreamDestroy(cap); } \
     return fail(c, STS_E_CUDA, std::string("graph build: ") + cudaGetErrorString(e_)); } } while (0)
 
-static sts_status build_tol_graph(sts_ctx* c, int n1)
+// the convergence check after a pass; `pdl`: a programmatic edge from the pass
+static cudaError_t launch_check(cudaStream_t s, unsigned long long* slot, LoopState* ls, cudaGraphConditionalHandle h,
+                                int mn, int mx, double tol, bool pdl)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, loop_check_kernel, slot, ls, h, mn, mx, tol);
+}
+// pdl: programmatic edges pass -> check -> pass inside the step (the first pass of
+// the step and of the WHILE body keep full edges); the caller falls back to pdl =
+// false when the driver rejects them
+static sts_status build_tol_graph(sts_ctx* c, int n1, bool pdl)
 {
     cudaStream_t cap = nullptr, cap2 = nullptr;
     const int impl = c->sch.time == STS_IMPLICIT, tvd = c->sch.space == STS_TVD_VANLEER;
@@ -1957,7 +2000,7 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
     k.ue = c->ue; k.ve = c->ve; k.Te = c->Te;
     const dim3 mgrid(c->n_gen + c->n_reg);                 // the conv kernel: every CTA of the schedule
     const bool fuse = fuse_conv(c);
-    auto pass = [&](int o, int w, int sl, cudaStream_t s, bool fz = false) -> cudaError_t {
+    auto pass = [&](int o, int w, int sl, cudaStream_t s, bool fz = false, bool pin = false) -> cudaError_t {
         Params q = k;
         if (fz) { q.ue_w = c->ue; q.ve_w = c->ve; q.Te_w = c->Te; }   // pass 1 computes the planes (N2)
         q.u_o = c->snap[o].u; q.v_o = c->snap[o].v; q.p_o = c->snap[o].p; q.T_o = c->snap[o].T;
@@ -1988,7 +2031,7 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
             kp.blockDim = dim3(MX);
             kp.sharedMemBytes = march_smem(c);
             kp.kernelParams = args;
-            e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
+            e = add_pass_node(&nodes[nn], g, deps, kp, pdl && pin);
             if (e != cudaSuccess) return e;
             nn++;
             return cudaStreamUpdateCaptureDependencies(s, nodes, nn, cudaStreamSetCaptureDependencies);
@@ -2005,7 +2048,7 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
             kp.blockDim = dim3(MX);
             kp.sharedMemBytes = part ? regk_smem(c, fz, false) : (fz ? FUSEC_SMEM : march_smem(c));
             kp.kernelParams = args;
-            e = cudaGraphAddKernelNode(&nodes[nn], g, deps.data(), deps.size(), &kp);
+            e = add_pass_node(&nodes[nn], g, deps, kp, pdl && pin);
             if (e != cudaSuccess) return e;
             if (part == 0) e = graph_node_high_priority(nodes[nn]);   // general CTAs first, as on the stream path
             if (e != cudaSuccess) return e;
@@ -2032,8 +2075,7 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
         conv_march_table(tvd, c->nu)<<<mgrid, MX, conv_smem(c), cap>>>(make_march(c, q));
     }
     CG(pass(n1, a, 0, cap, fuse));
-    loop_check_kernel<<<1, 32, 0, cap>>>(c->red2, c->d_ls, h, mn, mx, tol);
-    CG(cudaGetLastError());
+    CG(launch_check(cap, c->red2, c->d_ls, h, mn, mx, tol, pdl));
     CG(cudaStreamGetCaptureInfo(cap, &cst, nullptr, &cg, &deps, &nd));
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
@@ -2046,10 +2088,9 @@ static sts_status build_tol_graph(sts_ctx* c, int n1)
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     CG(cudaStreamBeginCaptureToGraph(cap2, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     CG(pass(a, b, 1, cap2));
-    loop_check_kernel<<<1, 32, 0, cap2>>>(c->red2 + 9, c->d_ls, h, mn, mx, tol);
-    CG(pass(b, a, 0, cap2));
-    loop_check_kernel<<<1, 32, 0, cap2>>>(c->red2, c->d_ls, h, mn, mx, tol);
-    CG(cudaGetLastError());
+    CG(launch_check(cap2, c->red2 + 9, c->d_ls, h, mn, mx, tol, pdl));
+    CG(pass(b, a, 0, cap2, false, true));
+    CG(launch_check(cap2, c->red2, c->d_ls, h, mn, mx, tol, pdl));
     cudaGraph_t bo = nullptr;
     CG(cudaStreamEndCapture(cap2, &bo));
     cudaGraph_t g = nullptr;
@@ -2073,7 +2114,14 @@ static sts_status graph_step(sts_ctx* ctx, bool* conv)
     const int n1 = c->cur, a = (n1 + 1) % 3, b = (n1 + 2) % 3;
     for (int r = 0; r < 3; r++)                   // all three rotations at once: no build inside later steps
         if (!c->tol_exec[r]) {
-            sts_status e = build_tol_graph(c, r);
+            const bool pdl = !(getenv("STS_NO_PDL") && atoi(getenv("STS_NO_PDL")) != 0);
+            sts_status e = build_tol_graph(c, r, pdl);
+            if (e && pdl) {                       // programmatic edges rejected: full edges
+                fprintf(stderr, "sts: tolerance-mode graph without PDL edges (%s)\n", c->err.c_str());
+                cudaGetLastError();
+                if (c->tol_exec[r]) { cudaGraphExecDestroy(c->tol_exec[r]); c->tol_exec[r] = nullptr; }
+                e = build_tol_graph(c, r, false);
+            }
             if (e) return e;
         }
     CU(cudaGraphLaunch(c->tol_exec[n1], c->stream));
@@ -2105,29 +2153,6 @@ static bool fix_graph_ok(const sts_ctx* c)
 {
     return c->sch.tol <= 0 && c->world == 1 && !c->comm && !c->peer && !c->profiling && c->sch.loop3 <= 1 &&
            !getenv("STS_NO_GRAPH") && !getenv("STS_GRAPH_KERNEL");
-}
-// A pass's kernel node; with `programmatic` every edge from the previous pass's
-// node(s) is a programmatic (PDL) edge: the node's CTAs may launch once every CTA of
-// the previous pass has started, and each waits in griddepcontrol.wait (first
-// statement of the march kernels) for the previous pass to complete.
-static cudaError_t add_pass_node(cudaGraphNode_t* node, cudaGraph_t g, const std::vector<cudaGraphNode_t>& deps,
-                                 const cudaKernelNodeParams& kp, bool programmatic)
-{
-    if (!programmatic || deps.empty()) return cudaGraphAddKernelNode(node, g, deps.data(), deps.size(), &kp);
-    cudaGraphNodeParams np = {};
-    np.type = cudaGraphNodeTypeKernel;
-    np.kernel.func = kp.func;
-    np.kernel.gridDim = kp.gridDim;
-    np.kernel.blockDim = kp.blockDim;
-    np.kernel.sharedMemBytes = kp.sharedMemBytes;
-    np.kernel.kernelParams = kp.kernelParams;
-    std::vector<cudaGraphEdgeData> ed(deps.size());
-    for (cudaGraphEdgeData& x : ed) {
-        x = cudaGraphEdgeData{};
-        x.from_port = cudaGraphKernelNodePortProgrammatic;
-        x.type = cudaGraphDependencyTypeProgrammatic;
-    }
-    return cudaGraphAddNode_v2(node, g, deps.data(), ed.data(), deps.size(), &np);
 }
 static sts_status build_fix_graph(sts_ctx* ctx, int n1)
 {
